@@ -1,0 +1,230 @@
+"""Float64 reference of the meta-network path: encode -> score every candidate -> arg-max -> adapt.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py). Citations: P:n = PAPER.md line n (the paper's
+LaTeX source); R#n = reading n in DESIGN.md §3 (where the paper is silent or garbled).
+
+Weights are the dict produced by synth.make_weights (canonical names, fp32); every array is
+promoted to float64 before use, so the oracle's arithmetic is float64 end to end.
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+N_MAX = 16
+
+
+def _f64(a) -> np.ndarray:
+    return np.asarray(a, dtype=np.float64)
+
+
+def _sigmoid(z):
+    # logistic sigmoid (R#5: Keras >= 2.3 default recurrent activation)
+    return 1.0 / (1.0 + np.exp(-z))
+
+
+# -------------------------------------------------------------------------------------------
+# candidate encoding: <S_p, S_c> -> u  (P:245-255 partition / credit; P:415 ranges; R#8, R#9)
+# -------------------------------------------------------------------------------------------
+def encode_candidate(S_p_bytes, S_c_mult) -> np.ndarray:
+    """u = ((log2 S_p - 21)/8, (S_c - 8.5)/8).  R#8: fixed transforms, divisor 8 keeps
+    power-of-two S_p and integer S_c dyadic."""
+    return np.array([(np.log2(float(S_p_bytes)) - 21.0) / 8.0,
+                     (float(S_c_mult) - 8.5) / 8.0], dtype=np.float64)
+
+
+def encode_grid(S_p, S_c) -> np.ndarray:
+    """All C = P*Q candidate encodings, index c = p*Q + q (partition-major; R#11 tie order)."""
+    P, Q = len(S_p), len(S_c)
+    u = np.empty((P * Q, 2), np.float64)
+    for p in range(P):
+        for q in range(Q):
+            u[p * Q + q] = encode_candidate(S_p[p], S_c[q])
+    return u
+
+
+# -------------------------------------------------------------------------------------------
+# job encoding (P:402 components 1-3; Table 2; R#4-R#8)
+# -------------------------------------------------------------------------------------------
+def lstm_step(Wx, Wh, b, x, h, c) -> Tuple[np.ndarray, np.ndarray]:
+    """One standard LSTM step, gate order i, f, g, o (R#5); a single bias vector per layer."""
+    hd = h.shape[0]
+    z = _f64(Wx) @ x + _f64(Wh) @ h + _f64(b)
+    i = _sigmoid(z[0 * hd:1 * hd])
+    f = _sigmoid(z[1 * hd:2 * hd])
+    g = np.tanh(z[2 * hd:3 * hd])
+    o = _sigmoid(z[3 * hd:4 * hd])
+    c_new = f * c + i * g
+    h_new = o * np.tanh(c_new)
+    return h_new, c_new
+
+
+def encode_job(W: Dict[str, np.ndarray], T, B_d, B_u, n: int, l: int, m: int, arc: int) -> np.ndarray:
+    """x_j in R^82 from one job's Table-2 statistics.
+
+    1. "embed layer-wise computation time T into a fixed dimension feature space":
+       per layer i, t'_i[w] = log2(1 + T[i][w] / 1 ms) for valid workers w < n, 0 on padding
+       (R#7, R#8); e_i = W_e t'_i + b_e (R#4).
+    2. "apply two-layer LSTM to extract the sequential features in T": h0 = c0 = 0,
+       steps i = 0..l-1 in stored layer order, output = top layer's final h (R#5).
+    3. bandwidth series B_d, B_u ("B_d B_mu", R#15 B_mu == B_u): log2(Gbps) on valid
+       workers, 0 on padding (R#8).
+    4. static group ("total number of workers"; Table 2 n, l, m, arc): n/16, l/64,
+       learned embeddings E_m[m], E_arc[arc] (R#6).
+    x = [h (32) | log2 B_d (16) | log2 B_u (16) | n/16 | l/64 | E_m[m] (8) | E_arc[arc] (8)].
+    """
+    n, l = int(n), int(l)
+    T = _f64(T)
+    hd = W["lstm1_Wh"].shape[1]
+    h1 = np.zeros(hd); c1 = np.zeros(hd)
+    h2 = np.zeros(hd); c2 = np.zeros(hd)
+    valid = np.arange(N_MAX) < n
+    for i in range(l):
+        t_feat = np.where(valid, np.log2(1.0 + np.where(valid, T[i], 0.0) / 1.0), 0.0)
+        e = _f64(W["W_e"]) @ t_feat + _f64(W["b_e"])
+        h1, c1 = lstm_step(W["lstm1_Wx"], W["lstm1_Wh"], W["lstm1_b"], e, h1, c1)
+        h2, c2 = lstm_step(W["lstm2_Wx"], W["lstm2_Wh"], W["lstm2_b"], h1, h2, c2)
+    bd = np.where(valid, np.log2(np.where(valid, _f64(B_d), 1.0)), 0.0)
+    bu = np.where(valid, np.log2(np.where(valid, _f64(B_u), 1.0)), 0.0)
+    statics = np.array([n / 16.0, l / 64.0])
+    return np.concatenate([h2, bd, bu, statics, _f64(W["E_m"][m]), _f64(W["E_arc"][arc])])
+
+
+def encode_jobs(W, jobs, idx=None) -> np.ndarray:
+    idx = range(jobs.J) if idx is None else idx
+    return np.stack([encode_job(W, jobs.T[j], jobs.B_d[j], jobs.B_u[j], jobs.n[j], jobs.l[j],
+                                jobs.m[j], jobs.arc[j]) for j in idx])
+
+
+# -------------------------------------------------------------------------------------------
+# the dense head: concat -> L hidden ReLU layers -> linear n_max output (R#1-R#3)
+# -------------------------------------------------------------------------------------------
+def n_hidden(W) -> int:
+    L = 1
+    while f"W{L + 1}" in W:
+        L += 1
+    return L
+
+
+def head_forward(W, z_in: np.ndarray, stash: bool = False):
+    """V_hat = W_o h_L + b_o with h_1 = ReLU(W1 z_in + b1), h_k = ReLU(W_k h_{k-1} + b_k).
+
+    z_in is [N][84] = [x_j | u_c] — the concatenation of the four feature groups (P:402
+    "We concatenate the features ... After applying two dense layers ... V is predicted").
+    Row-vector convention: rows are (job, candidate) pairs."""
+    L = n_hidden(W)
+    z_in = _f64(z_in)
+    hs, zs = [z_in], []
+    h = z_in
+    for k in range(1, L + 1):
+        z = h @ _f64(W[f"W{k}"]).T + _f64(W[f"b{k}"])
+        zs.append(z)
+        h = np.maximum(z, 0.0)          # ReLU (R#2)
+        hs.append(h)
+    V = h @ _f64(W["W_o"]).T + _f64(W["b_o"])
+    if stash:
+        return V, hs, zs
+    return V
+
+
+def speed(V_hat: np.ndarray, n: int) -> np.ndarray:
+    """Scalar predicted speed of a configuration = mean over the n valid workers of the
+    per-worker V_hat (Table 2: V is n x 1; R#3)."""
+    return V_hat[..., :int(n)].mean(axis=-1)
+
+
+def score_pairs(W, x_j: np.ndarray, n: int, u: np.ndarray) -> np.ndarray:
+    """Scores of one job against candidate encodings u[N][2]."""
+    z_in = np.concatenate([np.broadcast_to(_f64(x_j), (u.shape[0], x_j.shape[0])), _f64(u)], axis=1)
+    return speed(head_forward(W, z_in), n)
+
+
+def score_matrix(W, jobs, grid, job_idx=None, c_begin: int = 0, c_end: Optional[int] = None) -> np.ndarray:
+    """s[j][c] for the selected jobs and candidates [c_begin, c_end) ("a prediction of
+    training speed under different pairs of parameter settings")."""
+    u = encode_grid(grid.S_p, grid.S_c)
+    c_end = u.shape[0] if c_end is None else c_end
+    u = u[c_begin:c_end]
+    job_idx = list(range(jobs.J)) if job_idx is None else list(job_idx)
+    X = encode_jobs(W, jobs, job_idx)
+    return np.stack([score_pairs(W, X[r], jobs.n[j], u) for r, j in enumerate(job_idx)])
+
+
+def argmax_rows(s: np.ndarray, c_offset: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+    """Per-row best candidate: the maximum score; ties go to the smallest index, i.e. the
+    smaller S_p, then the smaller S_c (R#11); NaN never wins; an all-NaN row gives -1.
+    Written as the literal scan so it doubles as brute-force enumeration."""
+    best_idx = np.full(s.shape[0], -1, np.int64)
+    best_val = np.full(s.shape[0], np.nan)
+    for r in range(s.shape[0]):
+        for c in range(s.shape[1]):
+            v = s[r, c]
+            if np.isnan(v):
+                continue
+            if best_idx[r] < 0 or v > best_val[r]:
+                best_idx[r], best_val[r] = c + c_offset, v
+    return best_idx, best_val
+
+
+# -------------------------------------------------------------------------------------------
+# Eq. 2 loss and online adaptation (R#12, R#13)
+# -------------------------------------------------------------------------------------------
+def loss_norm(V_hat, V_bar) -> float:
+    """Eq. 2: L(V, V_bar) = || V - V_bar ||_2 (a norm, not squared)."""
+    d = _f64(V_hat) - _f64(V_bar)
+    return float(np.sqrt(np.sum(d * d)))
+
+
+def HEAD_PARAMS(W):
+    L = n_hidden(W)
+    names = ["W1", "b1"]
+    for k in range(2, L + 1):
+        names += [f"W{k}", f"b{k}"]
+    return names + ["W_o", "b_o"]
+
+
+def head_loss_and_grad(W, Z_in: np.ndarray, V_bar: np.ndarray, n: np.ndarray):
+    """Objective (R#12): (1/B) sum_b 1/2 ||r_b||^2 with r_b = (V_hat_b - V_bar_b) masked to
+    the n_b valid workers; its gradient w.r.t. every head parameter by the chain rule (the
+    encoder is frozen, R#13). Returns (objective, mean Eq.2 norm, grads)."""
+    Bn = Z_in.shape[0]
+    V, hs, zs = head_forward(W, Z_in, stash=True)
+    mask = (np.arange(V.shape[1])[None, :] < np.asarray(n)[:, None]).astype(np.float64)
+    r = (V - _f64(V_bar)) * mask
+    obj = 0.5 * np.sum(r * r) / Bn
+    norms = np.sqrt(np.sum(r * r, axis=1))
+    g = {}
+    dV = r / Bn                                   # d obj / d V_hat
+    L = n_hidden(W)
+    g["W_o"] = dV.T @ hs[L]
+    g["b_o"] = dV.sum(axis=0)
+    delta = (dV @ _f64(W["W_o"])) * (zs[L - 1] > 0)          # d obj / d z_L
+    for k in range(L, 0, -1):
+        g[f"W{k}"] = delta.T @ hs[k - 1]
+        g[f"b{k}"] = delta.sum(axis=0)
+        if k > 1:
+            delta = (delta @ _f64(W[f"W{k}"])) * (zs[k - 2] > 0)   # uses the pre-update W_k
+    return obj, float(norms.mean()), g
+
+
+def adapt(W, batch, lr: float, steps: int):
+    """Online adaptation ("use transfer learning to quickly adapt the meta-network", P:423;
+    triggered by >10% prediction error): `steps` plain SGD steps theta <- theta - lr*grad
+    on the head parameters (R#13), encoder frozen, on one minibatch of observed samples.
+    Returns (new weights as float64 dict, mean Eq.2 norm before the first step)."""
+    Wn = {k: _f64(v).copy() for k, v in W.items()}
+    jobs = batch.jobs
+    X = encode_jobs(Wn, jobs)                      # frozen encoder: computed once
+    U = np.stack([encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(jobs.J)])
+    Z_in = np.concatenate([X, U], axis=1)
+    loss_before = None
+    for _ in range(int(steps)):
+        _, norm_mean, g = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
+        if loss_before is None:
+            loss_before = norm_mean
+        for name in HEAD_PARAMS(Wn):
+            Wn[name] = Wn[name] - lr * g[name]
+    if loss_before is None:
+        _, loss_before, _ = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
+    return Wn, loss_before

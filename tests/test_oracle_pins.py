@@ -1,0 +1,285 @@
+"""Pins for the float64 oracle, each against something other than the oracle itself:
+hand-computed values (tests/golden/hand_net.json), closed forms, torch float64 library
+routines (nn.LSTM, nn.Linear, autograd), central finite differences and brute force."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.helpers import hand_net
+
+torch.set_default_dtype(torch.float64)
+
+
+# ---------------------------------------------------------------- candidate encoding (R#8)
+def test_candidate_encoding_closed_form():
+    assert np.array_equal(oracle.encode_candidate(1 << 21, 8.5), [0.0, 0.0])
+    assert np.array_equal(oracle.encode_candidate(1 << 29, 16.5), [1.0, 1.0])
+    assert np.array_equal(oracle.encode_candidate(4096, 1.0), [-9.0 / 8, -7.5 / 8])
+    assert np.array_equal(oracle.encode_candidate(1 << 30, 16.0), [9.0 / 8, 7.5 / 8])
+
+
+def test_grid_order_partition_major():
+    g = synth.Grid(np.array([1 << 20, 1 << 22, 1 << 24], np.int64), np.array([1.0, 2.0], np.float32))
+    u = oracle.encode_grid(g.S_p, g.S_c)
+    # c = p*Q + q: S_p changes slowest
+    assert u.shape == (6, 2)
+    assert np.array_equal(u[:, 0], np.repeat([-1 / 8, 1 / 8, 3 / 8], 2))
+    assert np.array_equal(u[:, 1], np.tile([-7.5 / 8, -6.5 / 8], 3))
+
+
+# ---------------------------------------------------------------- hand-computed nets
+@pytest.mark.parametrize("L", [1, 2])
+def test_hand_computed_net(L):
+    desc, W, jobs, grid, expected, best = hand_net(L)
+    s = oracle.score_matrix(W, jobs, grid)
+    assert np.array_equal(s[0], expected)          # every value is exact in binary
+    idx, val = oracle.argmax_rows(s)
+    assert idx[0] == best and val[0] == expected[best]
+
+
+def test_zero_network_gives_bias_mean_and_first_index():
+    """All weights zero -> V_hat = b_o for every candidate (SPEC zero-network example), the
+    score is the mean of b_o over valid workers and the tie goes to c = 0 (R#11)."""
+    desc = synth.NetDesc(3, 32)
+    W = {k: np.zeros(s, np.float32) for k, s in synth.param_shapes(desc).items()}
+    W["b_o"] = np.arange(16, dtype=np.float32)
+    jobs = synth.small_fleet(5, 7)
+    s = oracle.score_matrix(W, jobs, synth.log_grid(4, 3))
+    for j in range(5):
+        n = jobs.n[j]
+        assert np.all(s[j] == np.arange(n).mean())
+    idx, _ = oracle.argmax_rows(s)
+    assert np.all(idx == 0)
+
+
+# ---------------------------------------------------------------- encoder vs torch.nn.LSTM
+def _torch_encoder(W, T, n, l):
+    valid = torch.arange(16) < n
+    Tt = torch.tensor(np.asarray(T[:l], np.float64))
+    feat = torch.where(valid, torch.log2(1.0 + torch.where(valid, Tt, torch.zeros_like(Tt))), torch.zeros_like(Tt))
+    emb = torch.nn.Linear(16, 16)
+    lstm = torch.nn.LSTM(16, 32, num_layers=2, batch_first=True)
+    with torch.no_grad():
+        emb.weight.copy_(torch.tensor(W["W_e"], dtype=torch.float64))
+        emb.bias.copy_(torch.tensor(W["b_e"], dtype=torch.float64))
+        for layer in (1, 2):
+            getattr(lstm, f"weight_ih_l{layer - 1}").copy_(torch.tensor(W[f"lstm{layer}_Wx"], dtype=torch.float64))
+            getattr(lstm, f"weight_hh_l{layer - 1}").copy_(torch.tensor(W[f"lstm{layer}_Wh"], dtype=torch.float64))
+            getattr(lstm, f"bias_ih_l{layer - 1}").copy_(torch.tensor(W[f"lstm{layer}_b"], dtype=torch.float64))
+            getattr(lstm, f"bias_hh_l{layer - 1}").zero_()
+        out, (h, c) = lstm(emb(feat)[None])
+    return h[1, 0].numpy()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_encoder_matches_torch_lstm(seed):
+    desc = synth.NetDesc(2, 64)
+    W = synth.make_weights(desc, seed=100 + seed)
+    jobs = synth.small_fleet(4, seed)
+    for j in range(4):
+        x = oracle.encode_job(W, jobs.T[j], jobs.B_d[j], jobs.B_u[j], jobs.n[j], jobs.l[j], jobs.m[j], jobs.arc[j])
+        ref = _torch_encoder(W, jobs.T[j], int(jobs.n[j]), int(jobs.l[j]))
+        np.testing.assert_allclose(x[:32], ref, rtol=0, atol=1e-12)
+
+
+def test_encoder_static_features_closed_form():
+    desc = synth.NetDesc(2, 64)
+    W = synth.make_weights(desc)
+    T = np.zeros((54, 16), np.float32)
+    B_d = np.zeros(16, np.float32); B_d[:3] = [2.0, 8.0, 0.5]
+    B_u = np.zeros(16, np.float32); B_u[:3] = [4.0, 1.0, 16.0]
+    x = oracle.encode_job(W, T, B_d, B_u, 3, 5, 6, 1)
+    assert np.array_equal(x[32:48], [1, 3, -1] + [0] * 13)
+    assert np.array_equal(x[48:64], [2, 0, 4] + [0] * 13)
+    assert x[64] == 3 / 16 and x[65] == 5 / 64
+    assert np.array_equal(x[66:74], W["E_m"][6].astype(np.float64))
+    assert np.array_equal(x[74:82], W["E_arc"][1].astype(np.float64))
+
+
+def test_encoder_ignores_padding():
+    """Values stored in padded workers / layers never reach x (R#7)."""
+    desc = synth.NetDesc(2, 64)
+    W = synth.make_weights(desc)
+    jobs = synth.small_fleet(3, 11)
+    for j in range(3):
+        n, l = jobs.n[j], jobs.l[j]
+        T2, Bd2, Bu2 = jobs.T[j].copy(), jobs.B_d[j].copy(), jobs.B_u[j].copy()
+        T2[:, n:] = 123.0; T2[l:, :] = 77.0; Bd2[n:] = 5.0; Bu2[n:] = 9.0
+        a = oracle.encode_job(W, jobs.T[j], jobs.B_d[j], jobs.B_u[j], n, l, jobs.m[j], jobs.arc[j])
+        b = oracle.encode_job(W, T2, Bd2, Bu2, n, l, jobs.m[j], jobs.arc[j])
+        assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- head vs torch
+@pytest.mark.parametrize("L,H", [(1, 8), (2, 64), (3, 32), (4, 16)])
+def test_head_matches_torch_sequential(L, H):
+    desc = synth.NetDesc(L, H)
+    W = synth.make_weights(desc, seed=5 + L)
+    rng = np.random.default_rng(L)
+    Z = rng.normal(size=(37, 84))
+    layers = []
+    dims = [84] + [H] * L
+    for k in range(1, L + 1):
+        lin = torch.nn.Linear(dims[k - 1], H)
+        with torch.no_grad():
+            lin.weight.copy_(torch.tensor(W[f"W{k}"], dtype=torch.float64))
+            lin.bias.copy_(torch.tensor(W[f"b{k}"], dtype=torch.float64))
+        layers += [lin, torch.nn.ReLU()]
+    out = torch.nn.Linear(H, 16)
+    with torch.no_grad():
+        out.weight.copy_(torch.tensor(W["W_o"], dtype=torch.float64))
+        out.bias.copy_(torch.tensor(W["b_o"], dtype=torch.float64))
+    net = torch.nn.Sequential(*layers, out)
+    with torch.no_grad():
+        ref = net(torch.tensor(Z)).numpy()
+    np.testing.assert_allclose(oracle.head_forward(W, Z), ref, rtol=1e-13, atol=1e-13)
+
+
+def test_speed_is_masked_worker_mean():
+    V = np.arange(32, dtype=np.float64).reshape(2, 16)
+    assert oracle.speed(V[0], 4) == 1.5
+    assert np.array_equal(oracle.speed(V, 16), [7.5, 23.5])
+
+
+# ---------------------------------------------------------------- scoring invariances
+def test_job_and_candidate_permutation_equivariance():
+    desc = synth.NetDesc(2, 32)
+    W = synth.make_weights(desc)
+    jobs = synth.small_fleet(6, 3)
+    grid = synth.log_grid(5, 4)
+    s = oracle.score_matrix(W, jobs, grid)
+    perm = np.array([3, 0, 5, 1, 4, 2])
+    s_p = oracle.score_matrix(W, jobs.subset(perm), grid)
+    assert np.array_equal(s_p, s[perm])
+    u = oracle.encode_grid(grid.S_p, grid.S_c)
+    cperm = np.random.default_rng(0).permutation(u.shape[0])
+    x = oracle.encode_jobs(W, jobs, [2])[0]
+    np.testing.assert_allclose(oracle.score_pairs(W, x, jobs.n[2], u[cperm]), s[2, cperm], rtol=1e-14, atol=1e-14)
+
+
+# ---------------------------------------------------------------- arg-max
+def test_argmax_bruteforce_matches_numpy_first_max():
+    rng = np.random.default_rng(1)
+    s = rng.integers(0, 5, size=(40, 64)).astype(np.float64)    # many exact ties
+    idx, val = oracle.argmax_rows(s, c_offset=100)
+    assert np.array_equal(idx, np.argmax(s, axis=1) + 100)
+    assert np.array_equal(val, s.max(axis=1))
+
+
+def test_argmax_nan_never_wins():
+    s = np.array([[np.nan, 1.0, 2.0, np.nan], [np.nan] * 4, [3.0, np.nan, 3.0, -1.0]])
+    idx, val = oracle.argmax_rows(s)
+    assert idx.tolist() == [2, -1, 0]
+    assert val[0] == 2.0 and np.isnan(val[1]) and val[2] == 3.0
+
+
+# ---------------------------------------------------------------- Eq. 2 loss and adaptation
+def test_loss_norm_examples():
+    assert oracle.loss_norm([3.0, 4.0], [0.0, 0.0]) == 5.0
+    assert oracle.loss_norm([1.0, 2.0], [1.0, 2.0]) == 0.0
+
+
+def _small_problem(seed, L=3, H=6, B=5):
+    desc = synth.NetDesc(L, H)
+    W = {k: v.astype(np.float64) for k, v in synth.make_weights(desc, seed=seed).items()}
+    rng = np.random.default_rng(seed)
+    Z = rng.normal(size=(B, 84))
+    V_bar = rng.uniform(0.5, 1.5, size=(B, 16))
+    n = rng.integers(1, 17, size=B)
+    return W, Z, V_bar, n
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gradient_matches_central_differences(seed):
+    W, Z, V_bar, n = _small_problem(seed, L=1 + seed % 3)
+    _, _, g = oracle.head_loss_and_grad(W, Z, V_bar, n)
+    eps = 1e-6
+    rng = np.random.default_rng(seed + 1000)
+    for name in oracle.HEAD_PARAMS(W):
+        flat = W[name].reshape(-1)
+        for idx in rng.choice(flat.size, size=min(6, flat.size), replace=False):
+            old = flat[idx]
+            flat[idx] = old + eps
+            fp, _, _ = oracle.head_loss_and_grad(W, Z, V_bar, n)
+            flat[idx] = old - eps
+            fm, _, _ = oracle.head_loss_and_grad(W, Z, V_bar, n)
+            flat[idx] = old
+            fd = (fp - fm) / (2 * eps)
+            an = g[name].reshape(-1)[idx]
+            assert abs(fd - an) <= 1e-4 * max(abs(fd), abs(an)) + 1e-9, (name, idx, fd, an)
+
+
+def test_gradient_matches_torch_autograd():
+    W, Z, V_bar, n = _small_problem(3, L=4, H=9, B=7)
+    obj, norm_mean, g = oracle.head_loss_and_grad(W, Z, V_bar, n)
+    P = {k: torch.tensor(W[k], requires_grad=True) for k in oracle.HEAD_PARAMS(W)}
+    h = torch.tensor(Z)
+    L = 4
+    for k in range(1, L + 1):
+        h = torch.relu(h @ P[f"W{k}"].T + P[f"b{k}"])
+    V = h @ P["W_o"].T + P["b_o"]
+    mask = torch.tensor((np.arange(16)[None, :] < n[:, None]).astype(np.float64))
+    r = (V - torch.tensor(V_bar)) * mask
+    loss = 0.5 * (r * r).sum() / Z.shape[0]
+    loss.backward()
+    assert abs(loss.item() - obj) <= 1e-14 * abs(obj)
+    assert abs(torch.linalg.vector_norm(r, dim=1).mean().item() - norm_mean) <= 1e-13
+    for k, p in P.items():
+        np.testing.assert_allclose(g[k], p.grad.numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_last_layer_gradient_closed_form():
+    """dW_o = (1/B) sum_b r_b h_L,b^T (masked residual), db_o = (1/B) sum_b r_b."""
+    W, Z, V_bar, n = _small_problem(9, L=1, H=4, B=3)
+    _, _, g = oracle.head_loss_and_grad(W, Z, V_bar, n)
+    h = np.maximum(Z @ W["W1"].T + W["b1"], 0)
+    V = h @ W["W_o"].T + W["b_o"]
+    r = (V - V_bar) * (np.arange(16)[None, :] < n[:, None])
+    dWo = sum(np.outer(r[b], h[b]) for b in range(3)) / 3
+    np.testing.assert_allclose(g["W_o"], dWo, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(g["b_o"], r.sum(0) / 3, rtol=1e-13, atol=1e-15)
+
+
+def _tiny_batch(seed, J=6):
+    jobs = synth.small_fleet(J, seed)
+    grid = synth.log_grid(8, 8)
+    return synth.make_adapt_batch(jobs, grid, seed + 1)
+
+
+def test_adapt_zero_residual_is_fixed_point():
+    desc = synth.NetDesc(2, 16)
+    W = synth.make_weights(desc)
+    batch = _tiny_batch(1)
+    X = oracle.encode_jobs(W, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    V = oracle.head_forward(W, np.concatenate([X, U], 1))
+    batch.V_bar = (V * (np.arange(16)[None, :] < batch.jobs.n[:, None])).astype(np.float64)
+    Wn, loss = oracle.adapt(W, batch, lr=0.1, steps=3)
+    assert loss < 1e-12
+    for k in W:
+        np.testing.assert_allclose(Wn[k], W[k].astype(np.float64), rtol=0, atol=1e-12)
+
+
+def test_adapt_noop_cases_and_frozen_encoder():
+    desc = synth.NetDesc(3, 16)
+    W = synth.make_weights(desc)
+    batch = _tiny_batch(2)
+    for lr, steps in [(0.0, 3), (0.1, 0)]:
+        Wn, _ = oracle.adapt(W, batch, lr=lr, steps=steps)
+        for k in W:
+            assert np.array_equal(Wn[k], W[k].astype(np.float64)), k
+    Wn, _ = oracle.adapt(W, batch, lr=0.05, steps=2)
+    for k in ["E_m", "E_arc", "W_e", "b_e", "lstm1_Wx", "lstm1_Wh", "lstm1_b", "lstm2_Wx", "lstm2_Wh", "lstm2_b"]:
+        assert np.array_equal(Wn[k], W[k].astype(np.float64)), k
+    assert not np.array_equal(Wn["W1"], W["W1"].astype(np.float64))
+
+
+def test_adapt_descends():
+    desc = synth.NetDesc(3, 32)
+    W = synth.make_weights(desc)
+    batch = _tiny_batch(3, J=16)
+    Wn, before = oracle.adapt(W, batch, lr=1e-3, steps=1)
+    _, after = oracle.adapt(Wn, batch, lr=0.0, steps=1)
+    assert after < before
