@@ -1,0 +1,218 @@
+/*
+ * autobyte.h — C ABI of the B200-native AutoByte meta-network candidate scorer.
+ *
+ * The library implements ONE hot path of "AutoByte: Automatic Configuration for Optimal
+ * Communication Scheduling in DNN Training" (arXiv 2112.13509): the Meta Network Optimizer.
+ * Citations: P:n = line n of the paper's LaTeX source; R#n = reading n of
+ * DESIGN.md §3 (where the paper is silent, garbled or ambiguous).
+ *
+ *   f : (T, B, S_c, S_p) -> V                        (Eq. 1)
+ *   "select the optimal pair with the maximum training speedup at the cost of one
+ *    inference"
+ *   L(V, V_bar) = || V - V_bar ||_2, online adaptation by transfer learning
+ *                                                     (Eq. 2)
+ *
+ * Conventions that hold for every entry point unless stated otherwise:
+ *  - Status: every call returns an autobyte_status; AB_OK == 0, errors are negative.
+ *    Host-side checks (sizes, ranges of descriptors, NULL pointers) fail synchronously
+ *    with NO kernel launched and no state changed. autobyte_last_error(ctx) returns a
+ *    human-readable reason for the last failure on that ctx.
+ *  - Pointers: "DEVICE" pointers must be device memory on the ctx's device (e.g. torch
+ *    CUDA tensors); "HOST" pointers are ordinary host memory. All arrays are dense,
+ *    row-major, naturally aligned, and owned by the caller for the duration of the call.
+ *  - Asynchrony: device-pointer calls enqueue work on the ctx stream and return without
+ *    synchronising; results are valid once that stream reaches them. *_host calls and
+ *    autobyte_get_weights synchronise the ctx stream before returning.
+ *  - Data-dependent ranges (n_workers in 1..n_max, n_layers in 1..l_max, type ids in
+ *    range, partition sizes >= 4096, credit >= 1, bandwidth > 0) are the caller's
+ *    contract; they are checked on the device only when the environment variable
+ *    AUTOBYTE_CHECK=1 is set at autobyte_create time (then violations return
+ *    AB_E_INVALID from the next call). Otherwise out-of-range data is undefined behaviour.
+ *  - Threading: a ctx serves one stream and is not thread-safe. Score/argmax only read
+ *    the weights; adapt mutates them in stream order.
+ *  - No CPU fallback: without a usable sm_100a device, autobyte_create fails with
+ *    AB_E_CUDA / AB_E_UNSUPPORTED.
+ */
+#ifndef AUTOBYTE_H_
+#define AUTOBYTE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AUTOBYTE_ABI_VERSION 1
+#define AUTOBYTE_BLOB_MAGIC "ABYT"
+#define AUTOBYTE_BLOB_VERSION 1u
+#define AUTOBYTE_X_DIM 82      /* job feature vector x_j (R#4-R#8): 32 + 16 + 16 + 2 + 8 + 8 */
+#define AUTOBYTE_U_DIM 2       /* candidate encoding u_c (R#8) */
+
+typedef struct autobyte_ctx autobyte_ctx;   /* opaque; owned by the library */
+
+typedef enum {
+  AB_OK = 0,
+  AB_E_INVALID = -1,       /* bad argument value / NULL pointer / bad blob / device data check */
+  AB_E_SHAPE = -2,         /* inconsistent sizes (J, P, Q, shard, blob length) */
+  AB_E_CUDA = -3,          /* CUDA runtime error (message in autobyte_last_error) */
+  AB_E_NCCL = -4,          /* NCCL error */
+  AB_E_NONFINITE = -5,     /* non-finite weights in a blob */
+  AB_E_UNSUPPORTED = -6,   /* valid request this build does not implement (e.g. precision) */
+  AB_E_NOMEM = -7          /* allocation failure */
+} autobyte_status;
+
+typedef enum {
+  AB_PREC_BF16 = 0,   /* bf16 tensor-core operands, fp32 accumulate (parity 2e-2, R#16) */
+  AB_PREC_FP32 = 1    /* split-operand bf16x3 emulation of fp32 products (parity 1e-4) */
+} autobyte_precision;
+
+/* Shape of the meta-network (R#1-R#6). Supported: hidden_layers (L) in 1..8,
+ * hidden_width (H) in {64, 128, 256, 512}, n_max == 16, embed_dim == 16, lstm_hidden == 32,
+ * n_model_types in 1..64, n_arch_types in 1..16, type_embed_dim == 8. */
+typedef struct {
+  int32_t hidden_layers;    /* L: hidden ReLU layers of width H after the concatenation */
+  int32_t hidden_width;     /* H */
+  int32_t n_max;            /* worker slots of Table 2's n x 1 vectors (R#7) */
+  int32_t embed_dim;        /* d_e of the per-layer embedding of T (R#4) */
+  int32_t lstm_hidden;      /* h of both LSTM layers (R#5) */
+  int32_t n_model_types;    /* rows of the model-type embedding E_m (R#6) */
+  int32_t n_arch_types;     /* rows of the architecture embedding E_arc (R#6) */
+  int32_t type_embed_dim;   /* columns of E_m / E_arc (R#6) */
+} autobyte_net_desc;
+
+/* Table 2 runtime statistics of J jobs. */
+typedef struct {
+  int32_t J;                 /* number of jobs, >= 1 */
+  int32_t l_max;             /* layer stride of T, >= 1 */
+  const float*   T;          /* [J][l_max][n_max] layer-wise BP time in ms; entries of
+                                layers >= n_layers[j] or workers >= n_workers[j] are ignored */
+  const float*   B_down;     /* [J][n_max] download Gbps (> 0 for valid workers) */
+  const float*   B_up;       /* [J][n_max] upload Gbps (> 0 for valid workers) */
+  const int32_t* n_workers;  /* [J] in 1..n_max */
+  const int32_t* n_layers;   /* [J] in 1..l_max */
+  const int32_t* model_type; /* [J] in 0..n_model_types-1 */
+  const int32_t* arch_type;  /* [J] in 0..n_arch_types-1 (0 = PS, 1 = all-reduce) */
+} autobyte_job_stats;
+
+/* Candidate grid <S_p, S_c>: C = P*Q candidates, global index
+ * c = p*Q + q, so ascending c = smaller partition first, then smaller credit (R#11).
+ * This rank scores c in [shard_begin, shard_end); returned indices are global. */
+typedef struct {
+  int32_t P, Q;                    /* >= 1 each */
+  const int64_t* partition_bytes;  /* [P] strictly ascending, >= 4096 */
+  const float*   credit_mult;      /* [Q] strictly ascending, >= 1 (R#9) */
+  int64_t shard_begin, shard_end;  /* 0 <= begin < end <= P*Q */
+} autobyte_grid;
+
+/* Per-kernel timing collected while profiling is enabled (CUDA events on the ctx stream). */
+typedef struct {
+  double  encode_ms;   int64_t encode_launches;    /* K1 job encoder */
+  double  score_ms;    int64_t score_launches;     /* K2 fused tcgen05 MLP + arg-max */
+  double  finalize_ms; int64_t finalize_launches;  /* K5 key decode */
+  double  exchange_ms; int64_t exchange_calls;     /* K3 NCCL all-reduce(max) of keys */
+  double  adapt_ms;    int64_t adapt_launches;     /* K4 fused forward/backward/SGD */
+  double  pack_ms;     int64_t pack_launches;      /* bf16 weight re-pack after adapt */
+  int64_t other_launches;                          /* every other kernel of this library */
+  double  score_pairs;                             /* (job, candidate) pairs scored by K2 */
+} autobyte_profile;
+
+/* ---- library / host-only helpers (no device needed) ------------------------------- */
+int32_t     autobyte_abi_version(void);
+const char* autobyte_status_string(autobyte_status s);
+/* Validate a net descriptor against the supported set above. */
+autobyte_status autobyte_validate_desc(const autobyte_net_desc* desc);
+/* Size in bytes of the weight blob for desc: 48-byte header + fp32 arrays. */
+autobyte_status autobyte_blob_bytes(const autobyte_net_desc* desc, size_t* out_bytes);
+/* Validate a HOST weight blob: magic "ABYT", version, descriptor equal to desc, length,
+ * finite values (AB_E_NONFINITE otherwise).
+ * Blob layout (little endian): char magic[4]; uint32 version; autobyte_net_desc desc;
+ * uint32 n_arrays; uint32 reserved; then fp32 arrays back to back in the order
+ * E_m[n_model_types][te], E_arc[n_arch_types][te], W_e[de][n_max], b_e[de],
+ * lstm1_Wx[4h][de], lstm1_Wh[4h][h], lstm1_b[4h], lstm2_Wx[4h][h], lstm2_Wh[4h][h],
+ * lstm2_b[4h], W1[H][84], b1[H], {W_k[H][H], b_k[H]} for k = 2..L, W_o[n_max][H], b_o[n_max].
+ * LSTM gate order i, f, g, o (R#5); W1's last two columns multiply u_c (R#8). */
+autobyte_status autobyte_validate_blob(const autobyte_net_desc* desc, const void* blob, size_t blob_bytes);
+
+/* ---- context ---------------------------------------------------------------------- */
+/* Create a ctx on `device` using `cuda_stream` (a cudaStream_t; NULL = legacy default
+ * stream). Copies the HOST blob to device fp32 master weights and builds the bf16
+ * tensor-core shadows. Fails with AB_E_UNSUPPORTED if the device is not sm_100 or the
+ * (desc, precision) pair is not implemented. */
+autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* weight_blob,
+                                size_t blob_bytes, int device, void* cuda_stream,
+                                autobyte_precision precision, autobyte_ctx** out_ctx);
+void            autobyte_destroy(autobyte_ctx* ctx);
+const char*     autobyte_last_error(const autobyte_ctx* ctx);
+autobyte_status autobyte_synchronize(autobyte_ctx* ctx);
+
+/* ---- multi-GPU (candidate-axis sharding) ----------------------------- */
+/* Fill 128 bytes with a fresh NCCL unique id (rank 0 calls it and broadcasts the bytes). */
+autobyte_status autobyte_get_unique_id(void* out_128_bytes);
+/* Join a world of `world` ranks (one per GPU). After this, autobyte_argmax all-reduces the
+ * per-job best keys with ncclAllReduce(max, uint64) so every rank returns the global
+ * result; shards must partition [0, C) across ranks. world == 1 detaches. */
+autobyte_status autobyte_attach_comm(autobyte_ctx* ctx, const void* unique_id_128, int rank, int world);
+
+/* ---- the hot path (DEVICE pointers, asynchronous) ---------------------------------- */
+/* Encoder only: x[J][82] fp32 job feature vectors (P:402 components 1-3; "turn
+ * those metrics to vector inputs"). */
+autobyte_status autobyte_encode(autobyte_ctx* ctx, const autobyte_job_stats* jobs, float* x_out);
+
+/* Predicted speed s[j][c] = mean_{w < n_j} V_hat_w(x_j, u_c) (Eq. 1; R#3) of every job
+ * against this rank's shard: scores is [J][shard_end - shard_begin] fp32, column
+ * c - shard_begin. */
+autobyte_status autobyte_score(autobyte_ctx* ctx, const autobyte_job_stats* jobs,
+                               const autobyte_grid* grid, float* scores);
+
+/* Per-job best candidate: best_idx[j] = the global c maximising s[j][c], ties to the
+ * smallest c (R#11); NaN scores never win; a job whose scores are all NaN gets -1 and a NaN
+ * best_score. cur_idx (nullable) gives each job's current global configuration; cur_score[j]
+ * receives s[j][cur_idx[j]] (NaN when cur_idx is NULL) for the 5% gain trigger.
+ * best_idx, best_score, cur_score are [J] each; cur_score may be NULL. */
+autobyte_status autobyte_argmax(autobyte_ctx* ctx, const autobyte_job_stats* jobs,
+                                const autobyte_grid* grid, const int32_t* cur_idx,
+                                int32_t* best_idx, float* best_score, float* cur_score);
+
+/* Online adaptation (R#12, R#13): `steps` plain-SGD steps with learning
+ * rate lr on the minibatch of B = samples->J observations: sample b has job statistics
+ * samples[b], observed configuration (sp_bytes[b], sc_mult[b]) and observed per-worker speed
+ * v_obs[b][n_max] (Eq. 2's V_bar). Objective (1/B) sum_b 1/2 ||mask_b (V_hat_b - V_bar_b)||^2,
+ * head parameters only (W1, b1, W_k, b_k, W_o, b_o); encoder frozen. loss_before (nullable,
+ * DEVICE [1] fp32) receives (1/B) sum_b ||mask_b (V_hat_b - V_bar_b)||_2 before the first step.
+ * steps == 0 is a no-op apart from loss_before. The bf16 shadows are refreshed in stream
+ * order, so the next score/argmax sees the adapted weights. Deterministic. */
+autobyte_status autobyte_adapt(autobyte_ctx* ctx, const autobyte_job_stats* samples,
+                               const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,
+                               float lr, int32_t steps, float* loss_before);
+
+/* ---- end-to-end entry points (HOST pointers; copies inside; synchronising) ---------- */
+/* Same contracts as above with every array pointer in HOST memory. The library stages the
+ * inputs into its own device workspace with cudaMemcpyAsync, runs the device path, copies
+ * the [J] results back and synchronises the ctx stream. */
+autobyte_status autobyte_argmax_host(autobyte_ctx* ctx, const autobyte_job_stats* jobs,
+                                     const autobyte_grid* grid, const int32_t* cur_idx,
+                                     int32_t* best_idx, float* best_score, float* cur_score);
+autobyte_status autobyte_adapt_host(autobyte_ctx* ctx, const autobyte_job_stats* samples,
+                                    const int64_t* sp_bytes, const float* sc_mult,
+                                    const float* v_obs, float lr, int32_t steps,
+                                    float* loss_before);
+
+/* ---- weights / checkpoint ----------------------------------------------------------- */
+/* Write the current fp32 master weights as a blob (same layout as autobyte_validate_blob)
+ * into HOST memory of exactly autobyte_blob_bytes() bytes. Synchronises the ctx stream.
+ * create(blob) -> get_weights round-trips bit-identically. */
+autobyte_status autobyte_get_weights(autobyte_ctx* ctx, void* host_blob, size_t blob_bytes);
+
+/* ---- profiling ------------------------------------------------------------------------ */
+/* enable != 0: bracket every kernel launch with CUDA events on the ctx stream and
+ * accumulate per-kernel device time (adds a stream-ordered event pair per launch).
+ * autobyte_get_profile synchronises the ctx stream and reads the totals; reset zeroes them. */
+autobyte_status autobyte_set_profiling(autobyte_ctx* ctx, int enable);
+autobyte_status autobyte_get_profile(autobyte_ctx* ctx, autobyte_profile* out);
+autobyte_status autobyte_reset_profile(autobyte_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOBYTE_H_ */

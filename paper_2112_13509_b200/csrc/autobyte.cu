@@ -1,0 +1,643 @@
+// autobyte.cu — the C ABI (include/autobyte.h): argument checks, weight blob, device memory,
+// stream ordering of the kernels K1 (encode), K2 (score/arg-max), K3 (NCCL exchange),
+// K4 (adapt), K5 (finalize), and profiling.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace ab;
+
+namespace {
+
+constexpr uint32_t kBlobHeader = 48;
+
+enum Kind { K_ENCODE = 0, K_SCORE, K_FINALIZE, K_EXCHANGE, K_ADAPT, K_PACK, K_OTHER, K_N };
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= n && ptr) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T) + 256);
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct autobyte_ctx {
+  autobyte_net_desc desc{};
+  ParamOffsets off{};
+  autobyte_precision precision = AB_PREC_BF16;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool check = false;
+  std::string last_error;
+
+  DevBuf<float> params;          // fp32 masters (blob payload order)
+  DevBuf<float> grads;           // same layout, head part used by adapt
+  DevBuf<__nv_bfloat16> wpack;   // packed bf16 W_2..W_L for K2
+  DevBuf<unsigned int> barrier;  // grid barrier of K4 (2 words)
+  DevBuf<int> flag;              // AUTOBYTE_CHECK device flag
+  // per-call workspace
+  DevBuf<float> a, what, beta, x, adapt_ws, loss_tmp;
+  DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
+  // staging for the *_host entry points
+  DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
+  DevBuf<int32_t> sN, sL, sM, sArc, sCur, rIdx;
+  DevBuf<long long> sSp;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // profiling
+  bool profiling = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  double ms[K_N] = {};
+  long long launches[K_N] = {};
+  double score_pairs = 0.0;
+};
+
+namespace {
+
+autobyte_status fail(autobyte_ctx* c, autobyte_status s, const std::string& msg) {
+  if (c) c->last_error = msg;
+  return s;
+}
+autobyte_status cuda_fail(autobyte_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, AB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define AB_CUDA(ctx, expr)                                            \
+  do {                                                                \
+    cudaError_t _e = (expr);                                          \
+    if (_e != cudaSuccess) return cuda_fail((ctx), _e, #expr);        \
+  } while (0)
+
+// Bracket one launch with profiling events (when enabled) and count it.
+template <typename F>
+cudaError_t timed(autobyte_ctx* c, int kind, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profiling) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->stream);
+  }
+  cudaError_t e = launch();
+  if (c->profiling) {
+    cudaEventRecord(b, c->stream);
+    c->pending.push_back({kind, {a, b}});
+  }
+  if (e == cudaSuccess) c->launches[kind] += 1;
+  return e;
+}
+
+autobyte_status check_jobs_host(autobyte_ctx* c, const autobyte_job_stats* j) {
+  if (!j) return fail(c, AB_E_INVALID, "job stats pointer is NULL");
+  if (j->J < 1) return fail(c, AB_E_SHAPE, "J must be >= 1");
+  if (j->l_max < 1) return fail(c, AB_E_SHAPE, "l_max must be >= 1");
+  if (!j->T || !j->B_down || !j->B_up || !j->n_workers || !j->n_layers || !j->model_type || !j->arch_type)
+    return fail(c, AB_E_INVALID, "job stats array pointer is NULL");
+  return AB_OK;
+}
+
+autobyte_status check_grid_host(autobyte_ctx* c, const autobyte_grid* g) {
+  if (!g) return fail(c, AB_E_INVALID, "grid pointer is NULL");
+  if (g->P < 1 || g->Q < 1) return fail(c, AB_E_SHAPE, "grid P and Q must be >= 1");
+  const long long C = (long long)g->P * g->Q;
+  if (C > 0x7FFFFFFFLL) return fail(c, AB_E_SHAPE, "grid has more than 2^31-1 candidates");
+  if (g->shard_begin < 0 || g->shard_end > C || g->shard_begin >= g->shard_end)
+    return fail(c, AB_E_SHAPE, "shard must satisfy 0 <= begin < end <= P*Q");
+  if (!g->partition_bytes || !g->credit_mult) return fail(c, AB_E_INVALID, "grid array pointer is NULL");
+  return AB_OK;
+}
+
+autobyte_status device_checks(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid) {
+  if (!c->check) return AB_OK;
+  AB_CUDA(c, c->flag.ensure(1));
+  AB_CUDA(c, cudaMemsetAsync(c->flag.ptr, 0, sizeof(int), c->stream));
+  if (jobs) AB_CUDA(c, timed(c, K_OTHER, [&] {
+                      return launch_check(*jobs, c->desc.n_max, c->desc.n_model_types, c->desc.n_arch_types,
+                                          c->flag.ptr, c->stream);
+                    }));
+  if (grid) AB_CUDA(c, timed(c, K_OTHER, [&] { return launch_check_grid(*grid, c->flag.ptr, c->stream); }));
+  int h = 0;
+  AB_CUDA(c, cudaMemcpyAsync(&h, c->flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (h) return fail(c, AB_E_INVALID, h & 1 ? "job statistics out of range (AUTOBYTE_CHECK)" : "grid out of range (AUTOBYTE_CHECK)");
+  return AB_OK;
+}
+
+autobyte_status ensure_job_ws(autobyte_ctx* c, int J) {
+  const int H = c->desc.hidden_width;
+  AB_CUDA(c, c->a.ensure((size_t)J * H));
+  AB_CUDA(c, c->what.ensure((size_t)J * H));
+  AB_CUDA(c, c->beta.ensure((size_t)J));
+  AB_CUDA(c, c->keys.ensure((size_t)2 * J));
+  return AB_OK;
+}
+
+EncodeParams encode_params(autobyte_ctx* c, const autobyte_job_stats* j) {
+  EncodeParams p{};
+  p.J = j->J; p.l_max = j->l_max; p.H = c->desc.hidden_width;
+  p.T = j->T; p.B_d = j->B_down; p.B_u = j->B_up;
+  p.n = j->n_workers; p.l = j->n_layers; p.m = j->model_type; p.arc = j->arch_type;
+  p.params = c->params.ptr; p.off = c->off;
+  return p;
+}
+
+autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                                     const int32_t* cur_idx, float* scores) {
+  const int J = jobs->J;
+  autobyte_status st = ensure_job_ws(c, J);
+  if (st != AB_OK) return st;
+  EncodeParams ep = encode_params(c, jobs);
+  ep.a_out = c->a.ptr; ep.what_out = c->what.ptr; ep.beta_out = c->beta.ptr;
+  ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+
+  ScoreParams sp{};
+  sp.J = J; sp.H = c->desc.hidden_width; sp.G = c->desc.hidden_layers - 1;
+  sp.P = grid->P; sp.Q = grid->Q;
+  sp.c_begin = grid->shard_begin; sp.c_end = grid->shard_end;
+  const long long cs = grid->shard_end - grid->shard_begin;
+  sp.tiles_per_job = static_cast<int>((cs + kTileM - 1) / kTileM);
+  sp.n_tiles = (long long)sp.tiles_per_job * J;
+  sp.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); sp.S_c = grid->credit_mult;
+  sp.params = c->params.ptr; sp.off = c->off;
+  sp.a = c->a.ptr; sp.what = c->what.ptr; sp.beta = c->beta.ptr;
+  sp.wpack = c->wpack.ptr;
+  sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
+  sp.cur_idx = cur_idx; sp.scores = scores;
+  AB_CUDA(c, timed(c, K_SCORE, [&] { return launch_score(sp, c->num_sms, c->stream); }));
+  c->score_pairs += (double)J * (double)cs;
+  return AB_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int32_t autobyte_abi_version(void) { return AUTOBYTE_ABI_VERSION; }
+
+const char* autobyte_status_string(autobyte_status s) {
+  switch (s) {
+    case AB_OK: return "ok";
+    case AB_E_INVALID: return "invalid argument";
+    case AB_E_SHAPE: return "shape mismatch";
+    case AB_E_CUDA: return "CUDA error";
+    case AB_E_NCCL: return "NCCL error";
+    case AB_E_NONFINITE: return "non-finite weights";
+    case AB_E_UNSUPPORTED: return "unsupported";
+    case AB_E_NOMEM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+autobyte_status autobyte_validate_desc(const autobyte_net_desc* d) {
+  if (!d) return AB_E_INVALID;
+  if (d->hidden_layers < 1 || d->hidden_layers > kMaxHidden) return AB_E_INVALID;
+  const int H = d->hidden_width;
+  if (H != 64 && H != 128 && H != 256 && H != 512) return AB_E_INVALID;
+  if (d->n_max != kNMax || d->embed_dim != kEmbed || d->lstm_hidden != kLstm || d->type_embed_dim != kTypeEmbed)
+    return AB_E_INVALID;
+  if (d->n_model_types < 1 || d->n_model_types > 64 || d->n_arch_types < 1 || d->n_arch_types > 16)
+    return AB_E_INVALID;
+  return AB_OK;
+}
+
+autobyte_status autobyte_blob_bytes(const autobyte_net_desc* d, size_t* out) {
+  if (!out) return AB_E_INVALID;
+  autobyte_status s = autobyte_validate_desc(d);
+  if (s != AB_OK) return s;
+  *out = kBlobHeader + (size_t)make_offsets(*d).total * sizeof(float);
+  return AB_OK;
+}
+
+autobyte_status autobyte_validate_blob(const autobyte_net_desc* d, const void* blob, size_t bytes) {
+  if (!blob) return AB_E_INVALID;
+  size_t want = 0;
+  autobyte_status s = autobyte_blob_bytes(d, &want);
+  if (s != AB_OK) return s;
+  if (bytes != want) return AB_E_SHAPE;
+  const uint8_t* b = static_cast<const uint8_t*>(blob);
+  if (std::memcmp(b, AUTOBYTE_BLOB_MAGIC, 4) != 0) return AB_E_INVALID;
+  uint32_t ver;
+  std::memcpy(&ver, b + 4, 4);
+  if (ver != AUTOBYTE_BLOB_VERSION) return AB_E_INVALID;
+  autobyte_net_desc bd;
+  std::memcpy(&bd, b + 8, sizeof(bd));
+  if (std::memcmp(&bd, d, sizeof(bd)) != 0) return AB_E_SHAPE;
+  uint32_t n_arrays;
+  std::memcpy(&n_arrays, b + 40, 4);
+  if (n_arrays != static_cast<uint32_t>(12 + 2 * (d->hidden_layers - 1) + 2)) return AB_E_SHAPE;
+  const size_t nf = (bytes - kBlobHeader) / sizeof(float);
+  const float* f = reinterpret_cast<const float*>(b + kBlobHeader);
+  for (size_t i = 0; i < nf; ++i) {
+    float v;
+    std::memcpy(&v, f + i, 4);
+    if (!std::isfinite(v)) return AB_E_NONFINITE;
+  }
+  return AB_OK;
+}
+
+autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob, size_t blob_bytes, int device,
+                                void* cuda_stream, autobyte_precision precision, autobyte_ctx** out) {
+  if (!out) return AB_E_INVALID;
+  *out = nullptr;
+  autobyte_status s = autobyte_validate_desc(desc);
+  if (s != AB_OK) return s;
+  s = autobyte_validate_blob(desc, blob, blob_bytes);
+  if (s != AB_OK) return s;
+  if (precision != AB_PREC_BF16) return AB_E_UNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return AB_E_CUDA;
+  }
+  if (device < 0 || device >= ndev) return AB_E_INVALID;
+  DeviceGuard guard(device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return AB_E_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return AB_E_UNSUPPORTED;  // sm_100a code only
+
+  autobyte_ctx* c = new autobyte_ctx();
+  c->desc = *desc;
+  c->off = make_offsets(*desc);
+  c->precision = precision;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  const char* chk = std::getenv("AUTOBYTE_CHECK");
+  c->check = chk && chk[0] == '1';
+  auto bail = [&](cudaError_t e, const char* what) {
+    std::fprintf(stderr, "autobyte_create: %s: %s\n", what, cudaGetErrorString(e));
+    autobyte_destroy(c);
+    return AB_E_CUDA;
+  };
+  cudaError_t e;
+  if ((e = c->params.ensure(c->off.total)) != cudaSuccess) return bail(e, "alloc params");
+  if ((e = c->grads.ensure(c->off.total)) != cudaSuccess) return bail(e, "alloc grads");
+  if ((e = cudaMemsetAsync(c->grads.ptr, 0, c->off.total * sizeof(float), c->stream)) != cudaSuccess)
+    return bail(e, "memset grads");
+  if ((e = cudaMemcpyAsync(c->params.ptr, static_cast<const uint8_t*>(blob) + kBlobHeader,
+                           c->off.total * sizeof(float), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return bail(e, "copy blob");
+  const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers);
+  if ((e = c->wpack.ensure(wp ? wp : 1)) != cudaSuccess) return bail(e, "alloc wpack");
+  if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
+  if ((e = cudaMemsetAsync(c->barrier.ptr, 0, 2 * sizeof(unsigned int), c->stream)) != cudaSuccess)
+    return bail(e, "memset barrier");
+  if ((e = timed(c, K_PACK, [&] {
+         return launch_pack(c->params.ptr, c->off, desc->hidden_width, desc->hidden_layers, c->wpack.ptr, c->stream);
+       })) != cudaSuccess)
+    return bail(e, "pack weights");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return bail(e, "synchronize");
+  *out = c;
+  return AB_OK;
+}
+
+void autobyte_destroy(autobyte_ctx* c) {
+  if (!c) return;
+  DeviceGuard guard(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
+  c->a.release(); c->what.release(); c->beta.release(); c->x.release(); c->adapt_ws.release();
+  c->loss_tmp.release(); c->keys.release();
+  c->sT.release(); c->sBd.release(); c->sBu.release(); c->sSc.release(); c->sV.release();
+  c->rScore.release(); c->rCur.release();
+  c->sN.release(); c->sL.release(); c->sM.release(); c->sArc.release(); c->sCur.release(); c->rIdx.release();
+  c->sSp.release();
+  delete c;
+}
+
+const char* autobyte_last_error(const autobyte_ctx* c) { return c ? c->last_error.c_str() : "NULL ctx"; }
+
+autobyte_status autobyte_synchronize(autobyte_ctx* c) {
+  if (!c) return AB_E_INVALID;
+  DeviceGuard guard(c->device);
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return AB_OK;
+}
+
+autobyte_status autobyte_get_unique_id(void* out) {
+  if (!out) return AB_E_INVALID;
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AB_E_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return AB_OK;
+}
+
+autobyte_status autobyte_attach_comm(autobyte_ctx* c, const void* uid, int rank, int world) {
+  if (!c) return AB_E_INVALID;
+  if (world < 1 || rank < 0 || rank >= world) return fail(c, AB_E_INVALID, "bad rank/world");
+  DeviceGuard guard(c->device);
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  c->rank = rank;
+  c->world = world;
+  if (world == 1) return AB_OK;
+  if (!uid) return fail(c, AB_E_INVALID, "unique id is NULL");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    return fail(c, AB_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  return AB_OK;
+}
+
+autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs, float* x_out) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if (!x_out) return fail(c, AB_E_INVALID, "x_out is NULL");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, nullptr)) != AB_OK) return s;
+  EncodeParams ep = encode_params(c, jobs);
+  ep.x_out = x_out;
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                               float* scores) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (!scores) return fail(c, AB_E_INVALID, "scores is NULL");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
+  return run_encode_and_score(c, jobs, grid, nullptr, scores);
+}
+
+autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                                const int32_t* cur_idx, int32_t* best_idx, float* best_score, float* cur_score) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (!best_idx || !best_score) return fail(c, AB_E_INVALID, "best_idx / best_score is NULL");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
+  if ((s = run_encode_and_score(c, jobs, grid, cur_idx, nullptr)) != AB_OK) return s;
+  const int J = jobs->J;
+  if (c->comm && c->world > 1) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
+    ncclResult_t r = ncclAllReduce(c->keys.ptr, c->keys.ptr, (size_t)2 * J, ncclUint64, ncclMax, c->comm, c->stream);
+    if (c->profiling) { cudaEventRecord(b, c->stream); c->pending.push_back({K_EXCHANGE, {a, b}}); }
+    if (r != ncclSuccess) return fail(c, AB_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    c->launches[K_EXCHANGE] += 1;
+  }
+  AB_CUDA(c, timed(c, K_FINALIZE, [&] {
+            return launch_finalize(J, c->keys.ptr, c->keys.ptr + J, best_idx, best_score, cur_score, c->stream);
+          }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
+                               const float* sc_mult, const float* v_obs, float lr, int32_t steps,
+                               float* loss_before) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, samples);
+  if (s != AB_OK) return s;
+  if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "adapt input pointer is NULL");
+  if (steps < 0) return fail(c, AB_E_INVALID, "steps must be >= 0");
+  if (!std::isfinite(lr)) return fail(c, AB_E_INVALID, "lr must be finite");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, samples, nullptr)) != AB_OK) return s;
+  if (steps == 0 && !loss_before) return AB_OK;
+  const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
+  AB_CUDA(c, c->x.ensure((size_t)B * kXDim));
+  AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
+  EncodeParams ep = encode_params(c, samples);
+  ep.x_out = c->x.ptr;
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+  AdaptParams ap{};
+  ap.B = B; ap.H = H; ap.L = L; ap.steps = steps; ap.lr = lr;
+  ap.x = c->x.ptr; ap.S_p = reinterpret_cast<const long long*>(sp_bytes); ap.S_c = sc_mult; ap.v_obs = v_obs;
+  ap.n = samples->n_workers;
+  ap.params = c->params.ptr; ap.off = c->off; ap.ws = c->adapt_ws.ptr; ap.grads = c->grads.ptr;
+  ap.loss_before = loss_before; ap.barrier = c->barrier.ptr;
+  int grid_used = 0;
+  AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
+  if (steps > 0)
+    AB_CUDA(c, timed(c, K_PACK, [&] {
+              return launch_pack(c->params.ptr, c->off, H, L, c->wpack.ptr, c->stream);
+            }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                                     const int32_t* cur_idx, int32_t* best_idx, float* best_score,
+                                     float* cur_score) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (!best_idx || !best_score) return fail(c, AB_E_INVALID, "best_idx / best_score is NULL");
+  DeviceGuard guard(c->device);
+  const int J = jobs->J;
+  const size_t nT = (size_t)J * jobs->l_max * kNMax;
+  AB_CUDA(c, c->sT.ensure(nT)); AB_CUDA(c, c->sBd.ensure((size_t)J * kNMax)); AB_CUDA(c, c->sBu.ensure((size_t)J * kNMax));
+  AB_CUDA(c, c->sN.ensure(J)); AB_CUDA(c, c->sL.ensure(J)); AB_CUDA(c, c->sM.ensure(J)); AB_CUDA(c, c->sArc.ensure(J));
+  AB_CUDA(c, c->sSp.ensure(grid->P)); AB_CUDA(c, c->sSc.ensure(grid->Q));
+  AB_CUDA(c, c->rIdx.ensure(J)); AB_CUDA(c, c->rScore.ensure(J)); AB_CUDA(c, c->rCur.ensure(J));
+  if (cur_idx) AB_CUDA(c, c->sCur.ensure(J));
+  auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
+  AB_CUDA(c, h2d(c->sT.ptr, jobs->T, nT * 4));
+  AB_CUDA(c, h2d(c->sBd.ptr, jobs->B_down, (size_t)J * kNMax * 4));
+  AB_CUDA(c, h2d(c->sBu.ptr, jobs->B_up, (size_t)J * kNMax * 4));
+  AB_CUDA(c, h2d(c->sN.ptr, jobs->n_workers, (size_t)J * 4));
+  AB_CUDA(c, h2d(c->sL.ptr, jobs->n_layers, (size_t)J * 4));
+  AB_CUDA(c, h2d(c->sM.ptr, jobs->model_type, (size_t)J * 4));
+  AB_CUDA(c, h2d(c->sArc.ptr, jobs->arch_type, (size_t)J * 4));
+  AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
+  AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
+  if (cur_idx) AB_CUDA(c, h2d(c->sCur.ptr, cur_idx, (size_t)J * 4));
+  autobyte_job_stats dj = *jobs;
+  dj.T = c->sT.ptr; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
+  dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
+  autobyte_grid dg = *grid;
+  dg.partition_bytes = reinterpret_cast<const int64_t*>(c->sSp.ptr); dg.credit_mult = c->sSc.ptr;
+  s = autobyte_argmax(c, &dj, &dg, cur_idx ? c->sCur.ptr : nullptr, c->rIdx.ptr, c->rScore.ptr,
+                      cur_score ? c->rCur.ptr : nullptr);
+  if (s != AB_OK) return s;
+  auto d2h = [&](void* h, const void* d, size_t bytes) { return cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c->stream); };
+  AB_CUDA(c, d2h(best_idx, c->rIdx.ptr, (size_t)J * 4));
+  AB_CUDA(c, d2h(best_score, c->rScore.ptr, (size_t)J * 4));
+  if (cur_score) AB_CUDA(c, d2h(cur_score, c->rCur.ptr, (size_t)J * 4));
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return AB_OK;
+}
+
+autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
+                                    const float* sc_mult, const float* v_obs, float lr, int32_t steps,
+                                    float* loss_before) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, samples);
+  if (s != AB_OK) return s;
+  if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "adapt input pointer is NULL");
+  DeviceGuard guard(c->device);
+  const int B = samples->J;
+  const size_t nT = (size_t)B * samples->l_max * kNMax;
+  AB_CUDA(c, c->sT.ensure(nT)); AB_CUDA(c, c->sBd.ensure((size_t)B * kNMax)); AB_CUDA(c, c->sBu.ensure((size_t)B * kNMax));
+  AB_CUDA(c, c->sN.ensure(B)); AB_CUDA(c, c->sL.ensure(B)); AB_CUDA(c, c->sM.ensure(B)); AB_CUDA(c, c->sArc.ensure(B));
+  AB_CUDA(c, c->sSp.ensure(B)); AB_CUDA(c, c->sSc.ensure(B)); AB_CUDA(c, c->sV.ensure((size_t)B * kNMax));
+  AB_CUDA(c, c->loss_tmp.ensure(1));
+  auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
+  AB_CUDA(c, h2d(c->sT.ptr, samples->T, nT * 4));
+  AB_CUDA(c, h2d(c->sBd.ptr, samples->B_down, (size_t)B * kNMax * 4));
+  AB_CUDA(c, h2d(c->sBu.ptr, samples->B_up, (size_t)B * kNMax * 4));
+  AB_CUDA(c, h2d(c->sN.ptr, samples->n_workers, (size_t)B * 4));
+  AB_CUDA(c, h2d(c->sL.ptr, samples->n_layers, (size_t)B * 4));
+  AB_CUDA(c, h2d(c->sM.ptr, samples->model_type, (size_t)B * 4));
+  AB_CUDA(c, h2d(c->sArc.ptr, samples->arch_type, (size_t)B * 4));
+  AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
+  AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
+  AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));
+  autobyte_job_stats dj = *samples;
+  dj.T = c->sT.ptr; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
+  dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
+  s = autobyte_adapt(c, &dj, reinterpret_cast<const int64_t*>(c->sSp.ptr), c->sSc.ptr, c->sV.ptr, lr, steps,
+                     loss_before ? c->loss_tmp.ptr : nullptr);
+  if (s != AB_OK) return s;
+  if (loss_before)
+    AB_CUDA(c, cudaMemcpyAsync(loss_before, c->loss_tmp.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return AB_OK;
+}
+
+autobyte_status autobyte_get_weights(autobyte_ctx* c, void* host_blob, size_t bytes) {
+  if (!c || !host_blob) return AB_E_INVALID;
+  size_t want = 0;
+  autobyte_blob_bytes(&c->desc, &want);
+  if (bytes != want) return fail(c, AB_E_SHAPE, "blob size mismatch");
+  DeviceGuard guard(c->device);
+  uint8_t* b = static_cast<uint8_t*>(host_blob);
+  std::memcpy(b, AUTOBYTE_BLOB_MAGIC, 4);
+  const uint32_t ver = AUTOBYTE_BLOB_VERSION;
+  std::memcpy(b + 4, &ver, 4);
+  std::memcpy(b + 8, &c->desc, sizeof(c->desc));
+  const uint32_t n_arrays = 12 + 2 * (c->desc.hidden_layers - 1) + 2, zero = 0;
+  std::memcpy(b + 40, &n_arrays, 4);
+  std::memcpy(b + 44, &zero, 4);
+  AB_CUDA(c, cudaMemcpyAsync(b + kBlobHeader, c->params.ptr, c->off.total * sizeof(float), cudaMemcpyDeviceToHost,
+                             c->stream));
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  return AB_OK;
+}
+
+autobyte_status autobyte_set_profiling(autobyte_ctx* c, int enable) {
+  if (!c) return AB_E_INVALID;
+  c->profiling = enable != 0;
+  return AB_OK;
+}
+
+autobyte_status autobyte_get_profile(autobyte_ctx* c, autobyte_profile* out) {
+  if (!c || !out) return AB_E_INVALID;
+  DeviceGuard guard(c->device);
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) c->ms[p.first] += ms;
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  c->pending.clear();
+  out->encode_ms = c->ms[K_ENCODE]; out->encode_launches = c->launches[K_ENCODE];
+  out->score_ms = c->ms[K_SCORE]; out->score_launches = c->launches[K_SCORE];
+  out->finalize_ms = c->ms[K_FINALIZE]; out->finalize_launches = c->launches[K_FINALIZE];
+  out->exchange_ms = c->ms[K_EXCHANGE]; out->exchange_calls = c->launches[K_EXCHANGE];
+  out->adapt_ms = c->ms[K_ADAPT]; out->adapt_launches = c->launches[K_ADAPT];
+  out->pack_ms = c->ms[K_PACK]; out->pack_launches = c->launches[K_PACK];
+  out->other_launches = c->launches[K_OTHER];
+  out->score_pairs = c->score_pairs;
+  return AB_OK;
+}
+
+autobyte_status autobyte_reset_profile(autobyte_ctx* c) {
+  if (!c) return AB_E_INVALID;
+  autobyte_profile tmp;
+  autobyte_status s = autobyte_get_profile(c, &tmp);   // drains pending events
+  if (s != AB_OK) return s;
+  for (int k = 0; k < K_N; ++k) { c->ms[k] = 0.0; c->launches[k] = 0; }
+  c->score_pairs = 0.0;
+  return AB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------
+namespace ab {
+ParamOffsets make_offsets(const autobyte_net_desc& d) {
+  ParamOffsets o{};
+  int64_t p = 0;
+  auto take = [&](int64_t n) { int64_t r = p; p += n; return r; };
+  const int64_t te = d.type_embed_dim, de = d.embed_dim, h = d.lstm_hidden, H = d.hidden_width, nm = d.n_max;
+  o.E_m = take((int64_t)d.n_model_types * te);
+  o.E_arc = take((int64_t)d.n_arch_types * te);
+  o.W_e = take(de * nm);
+  o.b_e = take(de);
+  o.l1Wx = take(4 * h * de);
+  o.l1Wh = take(4 * h * h);
+  o.l1b = take(4 * h);
+  o.l2Wx = take(4 * h * h);
+  o.l2Wh = take(4 * h * h);
+  o.l2b = take(4 * h);
+  o.W[1] = take(H * kZDim);
+  o.b[1] = take(H);
+  for (int k = 2; k <= d.hidden_layers; ++k) {
+    o.W[k] = take(H * H);
+    o.b[k] = take(H);
+  }
+  o.W_o = take(nm * H);
+  o.b_o = take(nm);
+  o.total = p;
+  return o;
+}
+}  // namespace ab

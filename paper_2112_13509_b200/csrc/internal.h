@@ -1,0 +1,98 @@
+// internal.h — library-private declarations shared by the .cu files of libautobyte.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/autobyte.h"
+
+namespace ab {
+
+constexpr int kNMax = 16;
+constexpr int kEmbed = 16;
+constexpr int kLstm = 32;
+constexpr int kTypeEmbed = 8;
+constexpr int kXDim = AUTOBYTE_X_DIM;          // 82
+constexpr int kZDim = AUTOBYTE_X_DIM + 2;      // 84 = [x | u]
+constexpr int kMaxHidden = 8;
+constexpr int kTileM = 128;                    // candidates per tcgen05 tile (TMEM lanes)
+
+// Offsets (in floats) of every parameter inside the fp32 master buffer (= blob payload order).
+struct ParamOffsets {
+  int64_t E_m, E_arc, W_e, b_e;
+  int64_t l1Wx, l1Wh, l1b, l2Wx, l2Wh, l2b;
+  int64_t W[kMaxHidden + 1];   // W[1] = W1 [H][84]; W[k] = W_k [H][H], k = 2..L
+  int64_t b[kMaxHidden + 1];
+  int64_t W_o, b_o;
+  int64_t total;
+};
+ParamOffsets make_offsets(const autobyte_net_desc& d);
+
+// ---------------------------------------------------------------- kernel parameter blocks
+struct EncodeParams {
+  int J, l_max, H;
+  const float* T; const float* B_d; const float* B_u;
+  const int32_t* n; const int32_t* l; const int32_t* m; const int32_t* arc;
+  const float* params; ParamOffsets off;
+  float* x_out;        // [J][82] or null
+  float* a_out;        // [J][H] = W1x x + b1, or null
+  float* what_out;     // [J][H] = mean of the first n rows of W_o, or null
+  float* beta_out;     // [J]    = mean of the first n entries of b_o, or null
+  unsigned long long* keys;      // [J] reset to 0, or null
+  unsigned long long* cur_keys;  // [J] reset to 0, or null
+};
+
+struct ScoreParams {
+  int J, H, G;                  // G = L - 1 tensor-core layers
+  int P, Q;
+  long long c_begin, c_end;     // shard [begin, end)
+  int tiles_per_job;
+  long long n_tiles;
+  const long long* S_p;         // [P]
+  const float* S_c;             // [Q]
+  const float* params;          // fp32 masters (W1's u-columns, biases)
+  ParamOffsets off;
+  const float* a;               // [J][H]
+  const float* what;            // [J][H]
+  const float* beta;            // [J]
+  const __nv_bfloat16* wpack;   // packed bf16 W_2..W_L (see pack_weights)
+  unsigned long long* keys;     // [J]
+  unsigned long long* cur_keys; // [J]
+  const int32_t* cur_idx;       // [J] or null
+  float* scores;                // [J][c_end - c_begin] or null
+};
+
+struct AdaptParams {
+  int B, H, L, steps;
+  float lr;
+  const float* x;          // [B][82] frozen encoder output
+  const long long* S_p;    // [B]
+  const float* S_c;        // [B]
+  const float* v_obs;      // [B][16]
+  const int32_t* n;        // [B]
+  float* params;           // fp32 masters (updated in place)
+  ParamOffsets off;
+  float* ws;               // workspace (see adapt.cu)
+  float* grads;            // [head params] gradient buffer
+  float* loss_before;      // [1] or null
+  unsigned int* barrier;   // grid barrier counter (2 words)
+};
+
+// ---------------------------------------------------------------- launches (return cudaError_t)
+cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s);
+cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigned long long* cur_keys,
+                            int32_t* best_idx, float* best_score, float* cur_score, cudaStream_t s);
+cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, __nv_bfloat16* wpack,
+                        cudaStream_t s);
+__host__ __device__ size_t packed_weight_elems(int H, int L);
+cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
+size_t adapt_ws_floats(int B, int H, int L);
+cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,
+                         int* flag, cudaStream_t s);
+cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
+size_t score_smem_bytes(int H);
+
+}  // namespace ab

@@ -1,0 +1,346 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same seeded
+inputs. Tolerances: bf16 scores within 2e-2 of the per-job max |s|; arg-max
+exact when the oracle's top-2 gap exceeds the tolerance, regret within it otherwise; exact
+equality on the dyadic constructions; fp32 SIMT adaptation within 1e-3 relative."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.helpers import check_argmax, check_scores, hand_net
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_13509_b200 import autobyte
+    autobyte.load_library()
+
+
+def make(L, H, W):
+    from paper_2112_13509_b200.autobyte import AutoByte
+    return AutoByte(L, H, W, device=0)
+
+
+def dev(jobs, grid=None):
+    from paper_2112_13509_b200.autobyte import DeviceGrid, DeviceJobs
+    dj = DeviceJobs.from_host(jobs)
+    return (dj, DeviceGrid.from_host(grid)) if grid is not None else dj
+
+
+def gpu_scores(net, jobs, grid, begin=0, end=None):
+    dj, dg = dev(jobs, grid)
+    s = net.score(dj, dg, begin, end)
+    torch.cuda.synchronize()
+    return s.cpu().numpy()
+
+
+def gpu_argmax(net, jobs, grid, cur=None, begin=0, end=None):
+    dj, dg = dev(jobs, grid)
+    cur_t = torch.as_tensor(cur, dtype=torch.int32, device="cuda") if cur is not None else None
+    bi, bs, cs = net.argmax(dj, dg, cur_t, begin, end)
+    torch.cuda.synchronize()
+    return bi.cpu().numpy(), bs.cpu().numpy(), cs.cpu().numpy()
+
+
+# ------------------------------------------------------------------------------------- K1 encoder
+def test_encoder_matches_oracle():
+    desc = synth.NetDesc(2, 128)
+    W = synth.make_weights(desc)
+    jobs = synth.small_fleet(24, 5)
+    net = make(2, 128, W)
+    x = net.encode(dev(jobs)).cpu().numpy()
+    ref = oracle.encode_jobs(W, jobs)
+    np.testing.assert_allclose(x, ref, rtol=1e-4, atol=2e-5)
+
+
+# ------------------------------------------------------------------------------------- exact cases
+def _pad_hand_net(L):
+    """The hand-computed H=2 net of tests/golden/hand_net.json embedded in H=64 with zeros."""
+    desc, W2, jobs, grid, expected, best = hand_net(L)
+    d64 = synth.NetDesc(L, 64)
+    W = {k: np.zeros(s, np.float32) for k, s in synth.param_shapes(d64).items()}
+    for k, v in W2.items():
+        sl = tuple(slice(0, n) for n in v.shape)
+        W[k][sl] = v
+    return W, jobs, grid, expected, best
+
+
+@pytest.mark.parametrize("L", [1, 2])
+def test_hand_computed_net_exact(L):
+    W, jobs, grid, expected, best = _pad_hand_net(L)
+    net = make(L, 64, W)
+    s = gpu_scores(net, jobs, grid)
+    assert np.array_equal(s[0].astype(np.float64), expected), (s, expected)
+    bi, bs, _ = gpu_argmax(net, jobs, grid)
+    assert bi[0] == best and bs[0] == expected[best]
+
+
+def _bf16(a):
+    t = torch.as_tensor(np.asarray(a, np.float32))
+    return t.to(torch.bfloat16).to(torch.float32).numpy().astype(np.float64)
+
+
+def dyadic_net(L, H, seed):
+    """Sparse weights in {0, +-1/2, +-1}, biases in quarters; neurons whose oracle activations
+    are not exactly representable in bf16 are zeroed, so every product and sum on the GPU is
+    exact and the GPU must reproduce the float64 oracle bit for bit (SURVEY §8(c) pin)."""
+    rng = np.random.default_rng(seed)
+    desc = synth.NetDesc(L, H)
+    W = {k: np.zeros(s, np.float32) for k, s in synth.param_shapes(desc).items()}
+    W["E_m"][:] = rng.choice([-0.5, -0.25, 0, 0.25, 0.5], size=W["E_m"].shape)
+    W["E_arc"][:] = rng.choice([-0.5, 0, 0.5], size=W["E_arc"].shape)
+    vals = np.array([-1, -0.5, 0.5, 1], np.float32)
+    useful_x = list(range(32, 36)) + list(range(48, 52)) + [64, 65] + list(range(66, 82))
+    for r in range(H):
+        for c in rng.choice(useful_x, size=2, replace=False):
+            W["W1"][r, c] = rng.choice(vals)
+        W["W1"][r, 82] = rng.choice(vals)
+        W["W1"][r, 83] = rng.choice(vals)
+    W["b1"][:] = rng.integers(-4, 5, size=H) / 4
+    for k in range(2, L + 1):
+        for r in range(H):
+            for c in rng.choice(H, size=2, replace=False):
+                W[f"W{k}"][r, c] = rng.choice(vals)
+        W[f"b{k}"][:] = rng.integers(-4, 5, size=H) / 4
+    W["W_o"][:] = rng.choice([-1, -0.5, 0, 0.5, 1], size=W["W_o"].shape)
+    W["b_o"][:] = rng.integers(-4, 5, size=16) / 4
+    jobs, grid = synth.toy_job(dyadic=True), synth.toy_grid(dyadic=True)
+    # repair: zero neurons whose activations are not bf16-exact, layer by layer
+    X = oracle.encode_jobs(W, jobs)
+    Z = np.concatenate([np.repeat(X, grid.C, 0), oracle.encode_grid(grid.S_p, grid.S_c)], 1)
+    for k in range(1, L + 1):
+        _, hs, _ = oracle.head_forward(W, Z, stash=True)
+        h = hs[k]
+        bad = np.any(_bf16(h) != h, axis=0) | np.any(np.abs(h) > 2 ** 14, axis=0)
+        W[f"W{k}"][bad] = 0
+        W[f"b{k}"][bad] = 0
+    _, hs, _ = oracle.head_forward(W, Z, stash=True)
+    alive = [float(np.mean(np.any(hs[k] != 0, axis=0))) for k in range(1, L + 1)]
+    return W, jobs, grid, alive
+
+
+@pytest.mark.parametrize("L,H", [(1, 64), (2, 64), (3, 64), (2, 128), (3, 256), (4, 512), (2, 512)])
+def test_exact_dyadic_bit_for_bit(L, H):
+    W, jobs, grid, alive = dyadic_net(L, H, seed=L * 1000 + H)
+    assert min(alive) > 0.2, alive
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    net = make(L, H, W)
+    s = gpu_scores(net, jobs, grid).astype(np.float64)
+    mism = np.flatnonzero(s[0] != s_ora[0])
+    assert mism.size == 0, f"{mism.size} mismatches, first {mism[:5]}: gpu {s[0, mism[:5]]} oracle {s_ora[0, mism[:5]]}"
+
+
+# ------------------------------------------------------------------------------------- random nets
+CASES = [(1, 64, 7, 9), (2, 64, 8, 8), (2, 128, 7, 13), (3, 128, 5, 31), (3, 256, 31, 9), (4, 256, 16, 16),
+         (2, 512, 9, 11), (4, 512, 33, 7)]
+
+
+@pytest.mark.parametrize("L,H,P,Q", CASES)
+def test_scores_and_argmax_vs_oracle(L, H, P, Q):
+    desc = synth.NetDesc(L, H)
+    W = synth.make_weights(desc, seed=L * 31 + H)
+    jobs = synth.small_fleet(5, L + H)
+    grid = synth.log_grid(P, Q)
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    net = make(L, H, W)
+    s = gpu_scores(net, jobs, grid)
+    err = check_scores(s, s_ora, RTOL)
+    bi, bs, _ = gpu_argmax(net, jobs, grid)
+    check_argmax(bi, s_ora, RTOL)
+    # self-consistency: the arg-max path and the score path are the same arithmetic
+    assert np.array_equal(bs, s[np.arange(5), bi])
+    assert np.all(bs[:, None] >= s)
+    print(f"L={L} H={H} C={grid.C}: max err {err.max():.2e} mean {err.mean():.2e}")
+
+
+def test_c1_config():
+    c = synth.config("C1")
+    W = synth.make_weights(c.desc)
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    check_scores(gpu_scores(net, c.jobs, c.grid), s_ora, RTOL)
+    bi, _, _ = gpu_argmax(net, c.jobs, c.grid)
+    check_argmax(bi, s_ora, RTOL)
+
+
+def test_c2_config_full():
+    c = synth.config("C2")
+    W = synth.make_weights(c.desc)
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    check_scores(gpu_scores(net, c.jobs, c.grid), s_ora, RTOL)
+    bi, _, _ = gpu_argmax(net, c.jobs, c.grid)
+    check_argmax(bi, s_ora, RTOL)
+
+
+def test_shards_combine_to_full_and_determinism():
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H))
+    jobs = synth.small_fleet(9, 3)
+    grid = synth.log_grid(20, 17)
+    net = make(L, H, W)
+    full = gpu_scores(net, jobs, grid)
+    again = gpu_scores(net, jobs, grid)
+    assert np.array_equal(full, again)
+    C = grid.C
+    cuts = [0, 77, 200, 201, C]
+    parts = [gpu_scores(net, jobs, grid, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    assert np.array_equal(np.concatenate(parts, 1), full)
+    keys = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        bi, bs, _ = gpu_argmax(net, jobs, grid, None, a, b)
+        assert np.all((bi >= a) & (bi < b))
+        keys.append((bs, bi))
+    bi_full, bs_full, _ = gpu_argmax(net, jobs, grid)
+    best = np.stack([k[0] for k in keys])          # combine like the NCCL max: score, then smaller c
+    idx = np.stack([k[1] for k in keys])
+    for j in range(jobs.J):
+        cand = [(best[s, j], -idx[s, j]) for s in range(len(keys))]
+        bsc, nidx = max(cand)
+        assert bsc == bs_full[j] and -nidx == bi_full[j]
+
+
+def test_current_config_score():
+    L, H = 2, 128
+    W = synth.make_weights(synth.NetDesc(L, H))
+    jobs = synth.small_fleet(6, 4)
+    grid = synth.log_grid(10, 10)
+    cur = synth.current_configs(6, grid.C, 1)
+    net = make(L, H, W)
+    s = gpu_scores(net, jobs, grid)
+    _, _, cs = gpu_argmax(net, jobs, grid, cur)
+    assert np.array_equal(cs, s[np.arange(6), cur])
+    _, _, cs_none = gpu_argmax(net, jobs, grid, None)
+    assert np.all(np.isnan(cs_none))
+
+
+def test_nan_job_returns_minus_one():
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H))
+    jobs = synth.small_fleet(3, 8)
+    jobs.T[1, 0, 0] = np.nan
+    grid = synth.log_grid(4, 4)
+    net = make(L, H, W)
+    bi, bs, _ = gpu_argmax(net, jobs, grid)
+    assert bi[1] == -1 and np.isnan(bs[1])
+    assert bi[0] >= 0 and bi[2] >= 0
+
+
+def test_zero_network_tie_goes_to_first_candidate():
+    L, H = 3, 128
+    W = {k: np.zeros(s, np.float32) for k, s in synth.param_shapes(synth.NetDesc(L, H)).items()}
+    W["b_o"][:] = 0.5
+    jobs = synth.small_fleet(4, 2)
+    grid = synth.log_grid(8, 9)
+    net = make(L, H, W)
+    bi, bs, _ = gpu_argmax(net, jobs, grid, None, 13, 60)
+    assert np.all(bi == 13) and np.all(bs == 0.5)
+
+
+def test_c4_full_launch_sampled_jobs():
+    c = synth.config("C4")
+    W = synth.make_weights(c.desc)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    s = gpu_scores(net, c.jobs, c.grid)
+    bi, bs, _ = gpu_argmax(net, c.jobs, c.grid)
+    assert np.array_equal(bs, s[np.arange(c.jobs.J), bi])
+    sample = [0, 1, 1023, 2048, 4095]
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample)
+    check_scores(s[sample], s_ora, RTOL)
+    check_argmax(bi[sample], s_ora, RTOL)
+
+
+def test_c5_full_launch_sampled():
+    c = synth.config("C5")
+    W = synth.make_weights(c.desc)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    bi, bs, _ = gpu_argmax(net, c.jobs, c.grid)
+    assert np.all(bi >= 0) and np.all(np.isfinite(bs))
+    # a window of the grid scored for all jobs, checked against the oracle on sampled jobs
+    a, b = 524288 - 700, 524288 + 1348
+    s = gpu_scores(net, c.jobs, c.grid, a, b)
+    sample = [0, 777]
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample, c_begin=a, c_end=b)
+    check_scores(s[sample], s_ora, RTOL)
+    assert np.all(bs[:, None] >= s)
+    # the best score of sampled jobs equals the oracle's score of the returned candidate
+    for j in sample:
+        u = oracle.encode_grid(c.grid.S_p, c.grid.S_c)[bi[j]][None]
+        x = oracle.encode_jobs(W, c.jobs, [j])[0]
+        ref = oracle.score_pairs(W, x, c.jobs.n[j], u)[0]
+        assert abs(bs[j] - ref) <= RTOL * abs(ref)
+
+
+# ------------------------------------------------------------------------------------- K4 adapt
+def test_weights_roundtrip_and_noop_adapt():
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H))
+    net = make(L, H, W)
+    back = net.get_weights()
+    for k in W:
+        assert np.array_equal(back[k], W[k]), k
+    batch = synth.make_adapt_batch(synth.small_fleet(8, 1), synth.log_grid(8, 8), 3)
+    loss = net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=0.1, steps=0)
+    _, ref = oracle.adapt(W, batch, lr=0.1, steps=0)
+    assert abs(loss - ref) <= 1e-4 * ref
+    back = net.get_weights()
+    for k in W:
+        assert np.array_equal(back[k], W[k]), k
+
+
+@pytest.mark.parametrize("L,H,B,steps", [(1, 64, 7, 1), (2, 128, 33, 2), (3, 256, 256, 1), (4, 512, 100, 3)])
+def test_adapt_matches_oracle(L, H, B, steps):
+    W = synth.make_weights(synth.NetDesc(L, H), seed=L + H)
+    jobs = synth.small_fleet(B, 17 + L)
+    grid = synth.log_grid(64, 64)
+    batch = synth.make_adapt_batch(jobs, grid, 5)
+    lr = 1e-2
+    W_ora, loss_ora = oracle.adapt(W, batch, lr=lr, steps=steps)
+    net = make(L, H, W)
+    loss = net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=lr, steps=steps)
+    assert abs(loss - loss_ora) <= 1e-4 * loss_ora, (loss, loss_ora)
+    W_gpu = net.get_weights()
+    for k in oracle.HEAD_PARAMS(W_ora):
+        d_ora = W_ora[k] - W[k].astype(np.float64)
+        d_gpu = W_gpu[k].astype(np.float64) - W[k].astype(np.float64)
+        rel = np.linalg.norm(d_gpu - d_ora) / max(np.linalg.norm(d_ora), 1e-30)
+        assert rel <= 1e-3, (k, rel)
+    for k in ["E_m", "W_e", "lstm1_Wx", "lstm2_Wh"]:
+        assert np.array_equal(W_gpu[k], W[k])
+    # scoring after adaptation uses the adapted weights
+    g2 = synth.log_grid(9, 7)
+    s_ora = oracle.score_matrix(W_ora, jobs.subset(np.arange(3)), g2)
+    check_scores(gpu_scores(net, jobs.subset(np.arange(3)), g2), s_ora, RTOL)
+
+
+def test_adapt_is_deterministic():
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H))
+    batch = synth.make_adapt_batch(synth.small_fleet(64, 9), synth.log_grid(16, 16), 2)
+    outs = []
+    for _ in range(2):
+        net = make(L, H, W)
+        net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=1e-2, steps=2)
+        outs.append(net.get_weights_blob())
+        net.close()
+    assert outs[0] == outs[1]
+
+
+def test_host_entry_point_matches_device():
+    c = synth.config("C3")
+    W = synth.make_weights(c.desc)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    cur = synth.current_configs(c.jobs.J, c.grid.C, 4)
+    bi_h, bs_h, cs_h = net.argmax_host(c.jobs, c.grid, cur)
+    bi_d, bs_d, cs_d = gpu_argmax(net, c.jobs, c.grid, cur)
+    assert np.array_equal(bi_h, bi_d) and np.array_equal(bs_h, bs_d) and np.array_equal(cs_h, cs_d)
+    sample = [0, 127, 128, 255]
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample)
+    check_argmax(bi_h[sample], s_ora, RTOL)
