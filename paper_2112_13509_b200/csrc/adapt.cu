@@ -70,7 +70,7 @@ __device__ void gemm_tile(const Gemm& g, int tile, float (*As)[kTM + 4], float (
       const int n = n0 + tx * 4 + jj;
       if (n >= g.N) continue;
       float v = acc[i][jj];
-      if (g.mode == 0) v = fmaxf(v + g.bias[n], 0.f);
+      if (g.mode == 0) v = relu(v + g.bias[n]);
       else if (g.mode == 1) v = g.mask[m * g.ldmask + n] > 0.f ? v : 0.f;
       else if (g.mode == 3) v = (n < g.nvalid[m]) ? (v + g.bias[n] - g.vbar[m * 16 + n]) * g.scale : 0.f;
       g.C[m * g.ldc + n] = v;

@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         for (int i = 0; i < 16; ++i) {
           const int k = c0 + 2 * i;
           const float2 w0 = sW1c[k], w1 = sW1c[k + 1];
-          const float v0 = fmaxf(fmaf(w0.y, uc, fmaf(w0.x, up, vec[k].x)), 0.f);
-          const float v1 = fmaxf(fmaf(w1.y, uc, fmaf(w1.x, up, vec[k + 1].x)), 0.f);
+          const float v0 = relu(fmaf(w0.y, uc, fmaf(w0.x, up, vec[k].x)));
+          const float v1 = relu(fmaf(w1.y, uc, fmaf(w1.x, up, vec[k + 1].x)));
           pk[i] = pack_bf16x2(v0, v1);
         }
         store32(dst, c0, pk);
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         if (it > 0) { load_vecs(slot, t); named_bar_sync(kEpiBar, kEpiThreads); }
         const float2* vec = sVec + slot * H;
         for (int k = half * (H / 2); k < (half + 1) * (H / 2); ++k) {
-          const float v = fmaxf(fmaf(sW1c[k].y, uc, fmaf(sW1c[k].x, up, vec[k].x)), 0.f);
+          const float v = relu(fmaf(sW1c[k].y, uc, fmaf(sW1c[k].x, up, vec[k].x)));
           dot = fmaf(v, vec[k].y, dot);
         }
       }
@@ -262,10 +262,10 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 bb = __ldg(bias4 + (n0 >> 2) + i);
-              v[4 * i + 0] = fmaxf(__uint_as_float(acc[hpart][4 * i + 0]) + bb.x, 0.f);
-              v[4 * i + 1] = fmaxf(__uint_as_float(acc[hpart][4 * i + 1]) + bb.y, 0.f);
-              v[4 * i + 2] = fmaxf(__uint_as_float(acc[hpart][4 * i + 2]) + bb.z, 0.f);
-              v[4 * i + 3] = fmaxf(__uint_as_float(acc[hpart][4 * i + 3]) + bb.w, 0.f);
+              v[4 * i + 0] = relu(__uint_as_float(acc[hpart][4 * i + 0]) + bb.x);
+              v[4 * i + 1] = relu(__uint_as_float(acc[hpart][4 * i + 1]) + bb.y);
+              v[4 * i + 2] = relu(__uint_as_float(acc[hpart][4 * i + 2]) + bb.z);
+              v[4 * i + 3] = relu(__uint_as_float(acc[hpart][4 * i + 3]) + bb.w);
             }
             if (!last) {
               uint32_t pk[16];
