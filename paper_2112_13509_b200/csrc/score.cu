@@ -53,6 +53,32 @@ constexpr int kScoreThreads = 320;
 constexpr int kEpiThreads = 256;
 constexpr uint32_t kEpiBar = 1;
 
+// One output chunk of one layer: NKB weight stages x 4 MMAs (K = 16 each) into accumulator d_t.
+// A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address).
+template <typename C, bool TS>
+__device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32_t a_tmem0, uint64_t b_desc0,
+                                          uint64_t* full, uint64_t* empty, int& s, uint32_t& ph) {
+#pragma unroll 1
+  for (int b = 0; b < C::NKB; ++b) {
+    mbar_wait(&full[s], ph);
+    tc_fence_after();
+    if (elect_one()) {
+      const uint64_t bd = b_desc0 + static_cast<uint64_t>(s * (C::STAGE_BYTES >> 4));
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = (b | kk) != 0;
+        if (TS)
+          umma_ts(d_t, a_tmem0 + (b * 4 + kk) * 8, bd + 2 * kk, C::IDESC, acc);
+        else
+          umma_ss(d_t, a_desc0 + static_cast<uint64_t>(b * 1024 + 2 * kk), bd + 2 * kk, C::IDESC, acc);
+      }
+      umma_commit(&empty[s]);
+    }
+    __syncwarp();
+    if (++s == C::NS) { s = 0; ph ^= 1; }
+  }
+}
+
 template <int H>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
   using C = ScoreCfg<H>;
@@ -97,7 +123,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 
   if (warp == 0) {
     // ================================================================ TMA producer
-    if (lane == 0 && G > 0) {
+    if (G > 0) {
       const uint64_t pol = l2_policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
@@ -106,19 +132,24 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           for (int q = 0; q < C::NQ; ++q)
             for (int b = 0; b < C::NKB; ++b) {
               mbar_wait(&empty[s], ph ^ 1);
-              mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-              const __nv_bfloat16* src = p.wpack + ((size_t)(g * C::NQ + q) * C::NKB + b) * (C::NCH * 64);
-              bulk_g2s(sStage + s * C::STAGE_BYTES, src, C::STAGE_BYTES, &full[s], pol);
+              if (elect_one()) {
+                mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+                const __nv_bfloat16* src = p.wpack + ((size_t)(g * C::NQ + q) * C::NKB + b) * (C::NCH * 64);
+                bulk_g2s(sStage + s * C::STAGE_BYTES, src, C::STAGE_BYTES, &full[s], pol);
+              }
+              __syncwarp();
               if (++s == C::NS) { s = 0; ph ^= 1; }
             }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer
-    if (lane == 0 && G > 0) {
+    // ================================================================ MMA issuer (warp-converged;
+    // one elected lane issues, so every operand is warp-uniform and lives in uniform registers)
+    if (G > 0) {
       int s = 0;
       uint32_t ph = 0, aph = 0, dbits = 0;
       int dq = 0, b0 = 0;
-      const uint32_t a_smem = smem_u32(sA);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sStage));
       for (long long t = first; t < p.n_tiles; t += stride) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
@@ -130,31 +161,18 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             dbits ^= 1u << dq;
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
-            for (int b = 0; b < C::NKB; ++b) {
-              mbar_wait(&full[s], ph);
-              tc_fence_after();
-              const uint32_t st = smem_u32(sStage + s * C::STAGE_BYTES);
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const int ks = b * 4 + kk;
-                const uint64_t bdesc = umma_desc_sw128(st + kk * 32);
-                const uint32_t acc = (b | kk) != 0;
-                if (src == 0)
-                  umma_ss(d_t, umma_desc_sw128(a_smem + (ks >> 2) * 16384 + (ks & 3) * 32), bdesc, C::IDESC, acc);
-                else
-                  umma_ts(d_t, tmem + C::Y_COL + ks * 8, bdesc, C::IDESC, acc);
-              }
-              umma_commit(&empty[s]);
-              if (++s == C::NS) { s = 0; ph ^= 1; }
-            }
-            umma_commit(&dfull[dq]);
+            if (src == 0)
+              mma_chunk<C, false>(d_t, a_desc0, 0u, b_desc0, full, empty, s, ph);
+            else
+              mma_chunk<C, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, s, ph);
+            if (elect_one()) umma_commit(&dfull[dq]);
+            __syncwarp();
             dq ^= 1;
           }
         }
         b0 = ((b0 + G - 1) & 1) ^ 1;
       }
     }
-    __syncwarp();
   } else {
     // ================================================================ epilogue (256 threads)
     const int etid = threadIdx.x - 64;
