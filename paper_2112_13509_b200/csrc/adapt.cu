@@ -40,14 +40,19 @@ __device__ void gemm_tile(const Gemm& g, int tile, float (*As)[kTM + 4], float (
   float acc[4][4] = {};
   for (int k0 = 0; k0 < g.K; k0 += kTK) {
     __syncthreads();
+    // stage a 16 x 64 slice of each operand; consecutive threads walk the operand's contiguous
+    // dimension (k when the row stride is not 1) so every warp load is coalesced
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int e = tid + r * kAdaptThreads;
-      const int ml = e % kTM, kl = e / kTM;
+      int ml, kl;
+      if (g.lak == 1) { kl = e % kTK; ml = e / kTK; } else { ml = e % kTM; kl = e / kTM; }
       const int m = m0 + ml, k = k0 + kl;
       As[kl][ml] = (m < g.M && k < g.K) ? g.A[m * g.lam + k * g.lak] : 0.f;
-      const int n = n0 + ml;
-      Bs[kl][ml] = (n < g.N && k < g.K) ? g.Bm[k * g.lbk + n * g.lbn] : 0.f;
+      int nl, kb;
+      if (g.lbk == 1) { kb = e % kTK; nl = e / kTK; } else { nl = e % kTN; kb = e / kTN; }
+      const int n = n0 + nl, kk = k0 + kb;
+      Bs[kb][nl] = (n < g.N && kk < g.K) ? g.Bm[kk * g.lbk + n * g.lbn] : 0.f;
     }
     __syncthreads();
 #pragma unroll

@@ -166,6 +166,7 @@ autobyte_status ensure_job_ws(autobyte_ctx* c, int J) {
   AB_CUDA(c, c->what.ensure((size_t)J * H));
   AB_CUDA(c, c->beta.ensure((size_t)J));
   AB_CUDA(c, c->keys.ensure((size_t)2 * J));
+  AB_CUDA(c, c->x.ensure((size_t)J * kXDim));
   return AB_OK;
 }
 
@@ -184,9 +185,10 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   autobyte_status st = ensure_job_ws(c, J);
   if (st != AB_OK) return st;
   EncodeParams ep = encode_params(c, jobs);
-  ep.a_out = c->a.ptr; ep.what_out = c->what.ptr; ep.beta_out = c->beta.ptr;
+  ep.x_out = c->x.ptr; ep.a_out = c->a.ptr; ep.what_out = c->what.ptr; ep.beta_out = c->beta.ptr;
   ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
   AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+  c->launches[K_ENCODE] += 1;   // launch_encode issued K1a + K1b (projections)
 
   ScoreParams sp{};
   sp.J = J; sp.H = c->desc.hidden_width; sp.G = c->desc.hidden_layers - 1;

@@ -1,49 +1,73 @@
 // encode.cu — K1: per-job prologue of the scoring path.
 //
-// For every job j (one 128-thread CTA per job):
+// K1a, one 256-thread CTA per job:
 //   t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers (R#7, R#8); e_i = W_e t'_i + b_e (R#4)
 //   two-layer LSTM over i = 0..l_j-1, gates i,f,g,o, h0 = c0 = 0 ("two-layer LSTM", R#5);
-//     thread g owns gate row g of both layers with its weights held in registers
+//     thread g owns gate row g of one layer with its weights held in registers
 //   x_j = [h | log2 B_d | log2 B_u | n/16 | l/64 | E_m[m] | E_arc[arc]]   (Table 2)
+//   beta_j = (1/n) sum_{w<n} b_o[w], and resets the job's arg-max keys.
+// K1b, 32 jobs per CTA:
 //   a_j = W1[:, :82] x_j + b1     (layer-1 projection of the job half of the concatenation)
-//   w_j = (1/n) sum_{w<n} W_o[w],  beta_j = (1/n) sum_{w<n} b_o[w]   (worker-mean fold, R#3)
-// and resets the job's arg-max keys. This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
+//   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3) This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace ab {
 
-constexpr int kEncThreads = 128;
-constexpr int kChunk = 64;   // layers whose embeddings are staged in shared memory at a time
+constexpr int kEncThreads = 256;   // threads 0..127: LSTM layer 1 gate rows; 128..255: layer 2
+constexpr int kChunk = 64;         // layers whose embeddings are staged in shared memory at a time
 
 __device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
+// dot of a register-resident weight row with a shared-memory vector, 4 independent partial sums
+template <int N>
+__device__ __forceinline__ float dot_row(const float (&w)[N], const float* v) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int d = 0; d < N; d += 4) {
+    a0 = fmaf(w[d], v[d], a0);
+    a1 = fmaf(w[d + 1], v[d + 1], a1);
+    a2 = fmaf(w[d + 2], v[d + 2], a2);
+    a3 = fmaf(w[d + 3], v[d + 3], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// K1a: one CTA per job. The two LSTM layers run as a wavefront: in iteration i layer 1 takes
+// step i while layer 2 takes step i-1 (both read h1 of step i-1 before it is overwritten).
 __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_constant__ EncodeParams p) {
   __shared__ float sT[kChunk][kNMax];
   __shared__ float sE[kChunk][kEmbed];
-  __shared__ float sGate[4 * kLstm];
+  __shared__ float sG1[4 * kLstm], sG2[4 * kLstm];
   __shared__ float sH1[kLstm], sH2[kLstm];
   __shared__ float sX[kXDim + 2];
   const int j = blockIdx.x, tid = threadIdx.x;
   const int n = p.n[j], l = p.l[j], m = p.m[j], arc = p.arc[j];
   const float* P = p.params;
+  const bool layer1 = tid < 4 * kLstm;
+  const int row = layer1 ? tid : tid - 4 * kLstm;
 
-  // gate row `tid` of both LSTM layers, in registers
-  float wx1[kEmbed], wh1[kLstm], wx2[kLstm], wh2[kLstm];
+  float wx[kLstm], wh[kLstm];   // layer 1 uses wx[0..15] only
+  if (layer1) {
 #pragma unroll
-  for (int d = 0; d < kEmbed; ++d) wx1[d] = P[p.off.l1Wx + tid * kEmbed + d];
+    for (int d = 0; d < kEmbed; ++d) wx[d] = P[p.off.l1Wx + row * kEmbed + d];
 #pragma unroll
-  for (int d = 0; d < kLstm; ++d) {
-    wh1[d] = P[p.off.l1Wh + tid * kLstm + d];
-    wx2[d] = P[p.off.l2Wx + tid * kLstm + d];
-    wh2[d] = P[p.off.l2Wh + tid * kLstm + d];
+    for (int d = kEmbed; d < kLstm; ++d) wx[d] = 0.f;
+#pragma unroll
+    for (int d = 0; d < kLstm; ++d) wh[d] = P[p.off.l1Wh + row * kLstm + d];
+  } else {
+#pragma unroll
+    for (int d = 0; d < kLstm; ++d) {
+      wx[d] = P[p.off.l2Wx + row * kLstm + d];
+      wh[d] = P[p.off.l2Wh + row * kLstm + d];
+    }
   }
-  const float bb1 = P[p.off.l1b + tid], bb2 = P[p.off.l2b + tid];
-  float c1 = 0.f, c2 = 0.f;  // cell state, owned by threads 0..31
+  const float bias = layer1 ? P[p.off.l1b + row] : P[p.off.l2b + row];
+  float c = 0.f;  // cell state: threads 0..31 (layer 1) and 128..159 (layer 2)
   if (tid < kLstm) { sH1[tid] = 0.f; sH2[tid] = 0.f; }
 
   const float* T = p.T + (size_t)j * p.l_max * kNMax;
-  for (int i0 = 0; i0 < l; i0 += kChunk) {
+  for (int i0 = 0; i0 <= l; i0 += kChunk) {
     const int len = min(kChunk, l - i0);
     __syncthreads();
     for (int e = tid; e < len * kNMax; e += kEncThreads) {
@@ -59,40 +83,40 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
       sE[i][d] = acc;
     }
     __syncthreads();
-    for (int i = 0; i < len; ++i) {
-      // layer 1
-      float z = bb1;
+    const int iend = min(i0 + kChunk, l + 1);   // the wavefront runs one extra iteration
+    for (int i = i0; i < iend; ++i) {
+      if (layer1) {
+        if (i < l) {
+          float z = bias;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          const float* e = sE[i - i0];
 #pragma unroll
-      for (int d = 0; d < kEmbed; ++d) z = fmaf(wx1[d], sE[i][d], z);
-#pragma unroll
-      for (int d = 0; d < kLstm; ++d) z = fmaf(wh1[d], sH1[d], z);
-      sGate[tid] = z;
-      __syncthreads();
-      if (tid < kLstm) {
-        const float ig = sigmoidf_acc(sGate[tid]), fg = sigmoidf_acc(sGate[kLstm + tid]);
-        const float gg = tanhf(sGate[2 * kLstm + tid]), og = sigmoidf_acc(sGate[3 * kLstm + tid]);
-        c1 = fg * c1 + ig * gg;
-        sH1[tid] = og * tanhf(c1);
+          for (int d = 0; d < kEmbed; d += 4) {
+            a0 = fmaf(wx[d], e[d], a0); a1 = fmaf(wx[d + 1], e[d + 1], a1);
+            a2 = fmaf(wx[d + 2], e[d + 2], a2); a3 = fmaf(wx[d + 3], e[d + 3], a3);
+          }
+          z += ((a0 + a1) + (a2 + a3)) + dot_row<kLstm>(wh, sH1);
+          sG1[row] = z;
+        }
+      } else if (i >= 1) {
+        sG2[row] = bias + dot_row<kLstm>(wx, sH1) + dot_row<kLstm>(wh, sH2);
       }
       __syncthreads();
-      // layer 2
-      z = bb2;
-#pragma unroll
-      for (int d = 0; d < kLstm; ++d) z = fmaf(wx2[d], sH1[d], z);
-#pragma unroll
-      for (int d = 0; d < kLstm; ++d) z = fmaf(wh2[d], sH2[d], z);
-      sGate[tid] = z;
-      __syncthreads();
-      if (tid < kLstm) {
-        const float ig = sigmoidf_acc(sGate[tid]), fg = sigmoidf_acc(sGate[kLstm + tid]);
-        const float gg = tanhf(sGate[2 * kLstm + tid]), og = sigmoidf_acc(sGate[3 * kLstm + tid]);
-        c2 = fg * c2 + ig * gg;
-        sH2[tid] = og * tanhf(c2);
+      if (tid < kLstm && i < l) {
+        const float ig = sigmoidf_acc(sG1[tid]), fg = sigmoidf_acc(sG1[kLstm + tid]);
+        const float gg = tanhf(sG1[2 * kLstm + tid]), og = sigmoidf_acc(sG1[3 * kLstm + tid]);
+        c = fg * c + ig * gg;
+        sH1[tid] = og * tanhf(c);
+      } else if (tid >= 4 * kLstm && tid < 5 * kLstm && i >= 1) {
+        const int t = tid - 4 * kLstm;
+        const float ig = sigmoidf_acc(sG2[t]), fg = sigmoidf_acc(sG2[kLstm + t]);
+        const float gg = tanhf(sG2[2 * kLstm + t]), og = sigmoidf_acc(sG2[3 * kLstm + t]);
+        c = fg * c + ig * gg;
+        sH2[t] = og * tanhf(c);
       }
       __syncthreads();
     }
   }
-  __syncthreads();
   // feature vector x_j
   if (tid < kLstm) sX[tid] = sH2[tid];
   if (tid < kNMax) {
@@ -110,28 +134,6 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   __syncthreads();
   if (p.x_out)
     for (int i = tid; i < kXDim; i += kEncThreads) p.x_out[(size_t)j * kXDim + i] = sX[i];
-
-  const int H = p.H;
-  if (p.a_out) {
-    // a_j[k] = b1[k] + sum_i W1[k][i] x[i]: one warp per row, lanes over i (coalesced rows)
-    const int warp = tid >> 5, lane = tid & 31;
-    const float* W1 = P + p.off.W[1];
-    for (int k = warp; k < H; k += kEncThreads / 32) {
-      float acc = 0.f;
-      for (int i = lane; i < kXDim; i += 32) acc = fmaf(W1[(size_t)k * kZDim + i], sX[i], acc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) p.a_out[(size_t)j * H + k] = acc + P[p.off.b[1] + k];
-    }
-  }
-  if (p.what_out) {
-    const float inv_n = 1.0f / static_cast<float>(n);
-    for (int k = tid; k < H; k += kEncThreads) {
-      float acc = 0.f;
-      for (int w = 0; w < n; ++w) acc += P[p.off.W_o + (size_t)w * H + k];
-      p.what_out[(size_t)j * H + k] = acc * inv_n;
-    }
-  }
   if (tid == 0) {
     if (p.beta_out) {
       float acc = 0.f;
@@ -143,9 +145,73 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   }
 }
 
+// K1b: per-job projections for K2, 32 jobs per CTA, one output column per thread per pass:
+//   a[j][c]    = b1[c] + sum_i W1[c][i] x[j][i]            (job half of layer 1)
+//   what[j][c] = sum_{w < n_j} W_o[w][c] / n_j             (worker-mean fold of the output layer)
+constexpr int kProjJobs = 32;
+constexpr int kProjThreads = 256;
+
+__global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ EncodeParams p) {
+  __shared__ __align__(16) float sXt[kXDim][kProjJobs];    // transposed: 4 jobs per LDS.128
+  __shared__ __align__(16) float sM[kNMax][kProjJobs];     // mask / n
+  const int j0 = blockIdx.x * kProjJobs, tid = threadIdx.x;
+  const float* P = p.params;
+  for (int e = tid; e < kXDim * kProjJobs; e += kProjThreads) {
+    const int jj = e / kXDim, i = e % kXDim;
+    sXt[i][jj] = (j0 + jj < p.J) ? p.x_out[(size_t)(j0 + jj) * kXDim + i] : 0.f;
+  }
+  for (int e = tid; e < kNMax * kProjJobs; e += kProjThreads) {
+    const int w = e / kProjJobs, jj = e % kProjJobs;
+    const int nj = (j0 + jj < p.J) ? p.n[j0 + jj] : 1;
+    sM[w][jj] = w < nj ? 1.0f / static_cast<float>(nj) : 0.f;
+  }
+  __syncthreads();
+  const int H = p.H;
+  const int jn = min(kProjJobs, p.J - j0);
+  for (int col = tid; col < H; col += kProjThreads) {
+    float acc[kProjJobs];
+#pragma unroll
+    for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
+    const float* wrow = P + p.off.W[1] + (size_t)col * kZDim;
+    for (int i = 0; i < kXDim; ++i) {
+      const float w = wrow[i];
+      const float4* xv = reinterpret_cast<const float4*>(sXt[i]);
+#pragma unroll
+      for (int q = 0; q < kProjJobs / 4; ++q) {
+        const float4 v = xv[q];
+        acc[4 * q] = fmaf(w, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(w, v.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(w, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(w, v.w, acc[4 * q + 3]);
+      }
+    }
+    const float b1 = P[p.off.b[1] + col];
+#pragma unroll
+    for (int jj = 0; jj < kProjJobs; ++jj)
+      if (jj < jn) p.a_out[(size_t)(j0 + jj) * H + col] = acc[jj] + b1;
+#pragma unroll
+    for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
+    for (int w = 0; w < kNMax; ++w) {
+      const float wo = P[p.off.W_o + (size_t)w * H + col];
+      const float4* mv = reinterpret_cast<const float4*>(sM[w]);
+#pragma unroll
+      for (int q = 0; q < kProjJobs / 4; ++q) {
+        const float4 v = mv[q];
+        acc[4 * q] = fmaf(wo, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(wo, v.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(wo, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(wo, v.w, acc[4 * q + 3]);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < kProjJobs; ++jj)
+      if (jj < jn) p.what_out[(size_t)(j0 + jj) * H + col] = acc[jj];
+  }
+}
+
+// K1 = K1a (+ K1b when the projections are requested; they need x, so x_out must be set).
 cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s) {
   if (p.J <= 0) return cudaSuccess;
   encode_kernel<<<p.J, kEncThreads, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !p.a_out) return e;
+  project_kernel<<<(p.J + kProjJobs - 1) / kProjJobs, kProjThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

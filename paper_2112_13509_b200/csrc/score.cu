@@ -30,36 +30,48 @@ struct ScoreCfg {
   static constexpr int NCH = H >= 128 ? 128 : H;  // N of one MMA / one TMEM accumulator chunk
   static constexpr int NQ = H / NCH;              // chunks per layer
   static constexpr int NKB = H / 64;              // 64-element K blocks per layer
+  static constexpr int KB_PER_Q = NCH / 64;       // K blocks of the next layer produced by one chunk
   static constexpr int STAGE_BYTES = NCH * 128;   // one (chunk, K block) weight tile
   static constexpr int A_BYTES = kTileM * H * 2;  // bf16 activation tile, buffer X
   static constexpr int HALF = NCH / 2;            // columns per epilogue warp per chunk
-  static constexpr int W1C_BYTES = H * 8;
-  static constexpr int VEC_BYTES = 2 * H * 8;
+  static constexpr int G_CAP = H == 512 ? 3 : 7;  // hidden-layer biases kept in shared memory
+  static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
+  static constexpr int WHAT_BYTES = 2 * H * 4;    // w_j, two tile slots
+  static constexpr int BIAS_BYTES = G_CAP * H * 4;
   static constexpr int PART_BYTES = 2 * kTileM * 4;
   static constexpr int MISC_BYTES = 512;
-  static constexpr int FIXED = A_BYTES + W1C_BYTES + VEC_BYTES + PART_BYTES + MISC_BYTES;
-  static constexpr int BUDGET = 227 * 1024 - 1024;
+  static constexpr int FIXED = A_BYTES + AW_BYTES + WHAT_BYTES + BIAS_BYTES + PART_BYTES + MISC_BYTES;
+  static constexpr int BUDGET = 232448 - 1024;    // opt-in maximum minus the 1 KB alignment slack
   static constexpr int NS_FIT = (BUDGET - FIXED) / STAGE_BYTES;
   static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;
   static constexpr int SMEM = 1024 + FIXED + NS * STAGE_BYTES;
   static constexpr uint32_t IDESC = umma_idesc_bf16(128, NCH);
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t Y_COL = 256;          // TMEM column of activation buffer Y
-  static_assert(NS >= 3, "not enough shared memory for the weight pipeline");
+  static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
+  static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
 };
 
 constexpr int kScoreThreads = 320;
 constexpr int kEpiThreads = 256;
+constexpr int kEpiWarps = 8;
 constexpr uint32_t kEpiBar = 1;
 
 // One output chunk of one layer: NKB weight stages x 4 MMAs (K = 16 each) into accumulator d_t.
-// A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address).
+// A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address). For the first
+// chunk of a layer, K block b is only consumed once the epilogue has published the matching
+// 128-column piece of A (afull[b / KB_PER_Q]), so a layer starts before its input is complete.
 template <typename C, bool TS>
 __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32_t a_tmem0, uint64_t b_desc0,
-                                          uint64_t* full, uint64_t* empty, int& s, uint32_t& ph) {
+                                          uint64_t* full, uint64_t* empty, uint64_t* afull, uint32_t aph,
+                                          int& s, uint32_t& ph) {
 #pragma unroll 1
   for (int b = 0; b < C::NKB; ++b) {
+    if (afull != nullptr && (b % C::KB_PER_Q) == 0) {
+      mbar_wait(&afull[b / C::KB_PER_Q], aph);
+      tc_fence_after();
+    }
     mbar_wait(&full[s], ph);
     tc_fence_after();
     if (elect_one()) {
@@ -86,16 +98,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
   uint8_t* sStage = sA + C::A_BYTES;
-  float2* sW1c = reinterpret_cast<float2*>(sStage + C::NS * C::STAGE_BYTES);
-  float2* sVec = sW1c + H;                                   // [2][H] {a_j, w_j}
-  float* sPart = reinterpret_cast<float*>(sVec + 2 * H);     // [2][128]
+  float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::STAGE_BYTES);   // [3][H]: a_j | W1c0 | W1c1
+  float* sWhat = sAw + 3 * H;                                             // [2][H]
+  float* sBias = sWhat + 2 * H;                                           // [G_CAP][H]
+  float* sPart = sBias + C::G_CAP * H;                                    // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + 2 * kTileM);
   uint64_t* full = bars;
   uint64_t* empty = full + C::NS;
   uint64_t* dfull = empty + C::NS;
   uint64_t* dempty = dfull + 2;
-  uint64_t* afull = dempty + 2;
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(afull + 1);
+  uint64_t* afull = dempty + 2;                                           // [NQ]
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(afull + C::NQ);
   unsigned long long* sWkey = reinterpret_cast<unsigned long long*>(sTmem + 2);
   float* sBeta = reinterpret_cast<float*>(sWkey + 4);
 
@@ -105,15 +118,19 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kEpiThreads); }
-    mbar_init(afull, kEpiThreads);
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kEpiWarps); }
+    for (int q = 0; q < C::NQ; ++q) mbar_init(&afull[q], kEpiWarps);
     fence_barrier_init();
   }
   if (warp == 1) { tmem_alloc(sTmem, C::TMEM_COLS); tmem_relinquish(); }
   if (warp >= 2) {
     const float* W1 = p.params + p.off.W[1];
-    for (int k = threadIdx.x - 64; k < H; k += kEpiThreads)
-      sW1c[k] = make_float2(W1[(size_t)k * kZDim + kXDim], W1[(size_t)k * kZDim + kXDim + 1]);
+    for (int k = threadIdx.x - 64; k < H; k += kEpiThreads) {
+      sAw[H + k] = W1[(size_t)k * kZDim + kXDim];
+      sAw[2 * H + k] = W1[(size_t)k * kZDim + kXDim + 1];
+    }
+    const int gs = G < C::G_CAP ? G : C::G_CAP;
+    for (int e = threadIdx.x - 64; e < gs * H; e += kEpiThreads) sBias[e] = p.params[p.off.b[e / H + 2] + e % H];
   }
   tc_fence_before();
   __syncthreads();
@@ -153,22 +170,21 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       for (long long t = first; t < p.n_tiles; t += stride) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
-          mbar_wait(afull, aph);
-          aph ^= 1;
-          tc_fence_after();
           for (int q = 0; q < C::NQ; ++q) {
             mbar_wait(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
             dbits ^= 1u << dq;
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
+            uint64_t* aw = q == 0 ? afull : nullptr;
             if (src == 0)
-              mma_chunk<C, false>(d_t, a_desc0, 0u, b_desc0, full, empty, s, ph);
+              mma_chunk<C, false>(d_t, a_desc0, 0u, b_desc0, full, empty, aw, aph, s, ph);
             else
-              mma_chunk<C, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, s, ph);
+              mma_chunk<C, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph);
             if (elect_one()) umma_commit(&dfull[dq]);
             __syncwarp();
             dq ^= 1;
           }
+          aph ^= 1;
         }
         b0 = ((b0 + G - 1) & 1) ^ 1;
       }
@@ -180,12 +196,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16);
     const long long cshard = p.c_end - p.c_begin;
+    const float* w0s = sAw + H;
+    const float* w1s = sAw + 2 * H;
 
     auto load_vecs = [&](int slot, long long tile) {
       const int j = static_cast<int>(tile / tpj);
       const float* a = p.a + (size_t)j * H;
       const float* w = p.what + (size_t)j * H;
-      for (int k = etid; k < H; k += kEpiThreads) sVec[slot * H + k] = make_float2(a[k], w[k]);
+      for (int k = etid; k < H; k += kEpiThreads) {
+        sAw[k] = a[k];
+        sWhat[slot * H + k] = w[k];
+      }
       if (etid == 0) sBeta[slot] = p.beta[j];
     };
     auto row_u = [&](long long tile, float& up, float& uc, long long& c) {
@@ -207,25 +228,33 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         tmem_st16(lane_base + C::Y_COL + (c0 >> 1), pk);
       }
     };
-    auto publish = [&](int dst) {
+    // make this warp's part of A-chunk q visible to the tensor core and count the warp in
+    auto publish = [&](int dst, int q) {
       if (dst == 0) fence_proxy_async_smem();
       else { tmem_st_wait(); tc_fence_before(); }
-      mbar_arrive(afull);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[q]);
     };
-    auto build_h1 = [&](int slot, float up, float uc, int dst) {
-      const float2* vec = sVec + slot * H;
+    auto build_h1 = [&](float up, float uc, int dst) {
 #pragma unroll 1
-      for (int c0 = half * (H / 2); c0 < (half + 1) * (H / 2); c0 += 32) {
-        uint32_t pk[16];
+      for (int q = 0; q < C::NQ; ++q) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int k = c0 + 2 * i;
-          const float2 w0 = sW1c[k], w1 = sW1c[k + 1];
-          const float v0 = relu(fmaf(w0.y, uc, fmaf(w0.x, up, vec[k].x)));
-          const float v1 = relu(fmaf(w1.y, uc, fmaf(w1.x, up, vec[k + 1].x)));
-          pk[i] = pack_bf16x2(v0, v1);
+        for (int hp = 0; hp < C::HALF / 32; ++hp) {
+          const int c0 = q * C::NCH + half * C::HALF + hp * 32;
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+            const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
+            const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+            pk[2 * i] = pack_bf16x2(relu(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x))),
+                                    relu(fmaf(v4.y, uc, fmaf(u4.y, up, a4.y))));
+            pk[2 * i + 1] = pack_bf16x2(relu(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z))),
+                                        relu(fmaf(v4.w, uc, fmaf(u4.w, up, a4.w))));
+          }
+          store32(dst, c0, pk);
         }
-        store32(dst, c0, pk);
+        publish(dst, q);
       }
     };
 
@@ -238,8 +267,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       float up, uc;
       long long c;
       row_u(t, up, uc, c);
-      build_h1(0, up, uc, 0);
-      publish(0);
+      build_h1(up, uc, 0);
     }
     for (; t < p.n_tiles; t += stride, ++it) {
       const int slot = it & 1;
@@ -251,16 +279,14 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       float dot = 0.f;
       if (G == 0) {
         if (it > 0) { load_vecs(slot, t); named_bar_sync(kEpiBar, kEpiThreads); }
-        const float2* vec = sVec + slot * H;
-        for (int k = half * (H / 2); k < (half + 1) * (H / 2); ++k) {
-          const float v = relu(fmaf(sW1c[k].y, uc, fmaf(sW1c[k].x, up, vec[k].x)));
-          dot = fmaf(v, vec[k].y, dot);
-        }
+        const float* wv = sWhat + slot * H;
+        for (int k = half * (H / 2); k < (half + 1) * (H / 2); ++k)
+          dot = fmaf(relu(fmaf(w1s[k], uc, fmaf(w0s[k], up, sAw[k]))), wv[k], dot);
       }
       for (int g = 0; g < G; ++g) {
         const int src = (b0 + g) & 1, dst = src ^ 1;
         const bool last = (g == G - 1);
-        const float4* bias4 = reinterpret_cast<const float4*>(p.params + p.off.b[g + 2]);
+        const float* bias = g < C::G_CAP ? sBias + g * H : p.params + p.off.b[g + 2];
         for (int q = 0; q < C::NQ; ++q) {
           mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
           dbits ^= 1u << dq;
@@ -271,19 +297,21 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           if (C::HALF == 64) tmem_ld32(lane_base + dcol + 32, acc[1]);
           tmem_ld_wait();
           tc_fence_before();
-          mbar_arrive(&dempty[dq]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[dq]);
           dq ^= 1;
 #pragma unroll
-          for (int hpart = 0; hpart < C::HALF / 32; ++hpart) {
-            const int n0 = q * C::NCH + half * C::HALF + hpart * 32;
+          for (int hp = 0; hp < C::HALF / 32; ++hp) {
+            const int n0 = q * C::NCH + half * C::HALF + hp * 32;
+            const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
             float v[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const float4 bb = __ldg(bias4 + (n0 >> 2) + i);
-              v[4 * i + 0] = relu(__uint_as_float(acc[hpart][4 * i + 0]) + bb.x);
-              v[4 * i + 1] = relu(__uint_as_float(acc[hpart][4 * i + 1]) + bb.y);
-              v[4 * i + 2] = relu(__uint_as_float(acc[hpart][4 * i + 2]) + bb.z);
-              v[4 * i + 3] = relu(__uint_as_float(acc[hpart][4 * i + 3]) + bb.w);
+              const float4 bb = b4[i];
+              v[4 * i + 0] = relu(__uint_as_float(acc[hp][4 * i + 0]) + bb.x);
+              v[4 * i + 1] = relu(__uint_as_float(acc[hp][4 * i + 1]) + bb.y);
+              v[4 * i + 2] = relu(__uint_as_float(acc[hp][4 * i + 2]) + bb.z);
+              v[4 * i + 3] = relu(__uint_as_float(acc[hp][4 * i + 3]) + bb.w);
             }
             if (!last) {
               uint32_t pk[16];
@@ -291,11 +319,18 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
               for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
               store32(dst, n0, pk);
             } else {
-              const float2* vec = sVec + slot * H + n0;
+              const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * H + n0);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) dot = fmaf(v[i], vec[i].y, dot);
+              for (int i = 0; i < 8; ++i) {
+                const float4 ww = w4[i];
+                dot = fmaf(v[4 * i], ww.x, dot);
+                dot = fmaf(v[4 * i + 1], ww.y, dot);
+                dot = fmaf(v[4 * i + 2], ww.z, dot);
+                dot = fmaf(v[4 * i + 3], ww.w, dot);
+              }
             }
           }
+          if (!last) publish(dst, q);
           if (last && q == 0 && tn < p.n_tiles) {
             // next tile's h1 goes into the buffer the last layer does not read
             load_vecs(slot ^ 1, tn);
@@ -303,11 +338,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             float up2, uc2;
             long long c2;
             row_u(tn, up2, uc2, c2);
-            build_h1(slot ^ 1, up2, uc2, src ^ 1);
-            publish(src ^ 1);
+            build_h1(up2, uc2, src ^ 1);
           }
         }
-        if (!last) publish(dst);
       }
       if (G > 0) b0 = ((b0 + G - 1) & 1) ^ 1;
 
