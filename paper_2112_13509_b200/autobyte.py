@@ -69,11 +69,13 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load libautobyte.so (raises if it was not built — there is no fallback)."""
+def load_library(path: Optional[str] = None):
+    """Load libautobyte.so (raises if it was not built — there is no fallback). AUTOBYTE_LIB
+    may name an alternative build of the same library (e.g. a cycle-accounting variant)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("AUTOBYTE_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)

@@ -10,6 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libautobyte.so")
+STATS_LIB = os.path.join(PKG, "libautobyte_stats.so")   # -DAB_STATS cycle-accounting variant (tools only)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -35,23 +36,23 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, stats: bool = False) -> str:
+    lib_path = STATS_LIB if stats else LIB
+    if not force and not stats and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *sources(), "-o", LIB + ".tmp",
+           *(["-DAB_STATS"] if stats else []), *sources(), "-o", lib_path + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_path + ".tmp", lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, stats="--stats" in sys.argv))

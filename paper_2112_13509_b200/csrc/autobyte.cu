@@ -63,6 +63,8 @@ struct autobyte_ctx {
   autobyte_precision precision = AB_PREC_BF16;
   int device = 0;
   int num_sms = 148;
+  int cta_group = 2;             // K2 variant: CTA pairs (default) or single CTAs (AUTOBYTE_CTA_GROUP=1)
+  CUtensorMap wmap{};            // tensor map over wpack for the CTA-pair TMA
   cudaStream_t stream = nullptr;
   bool check = false;
   std::string last_error;
@@ -73,7 +75,8 @@ struct autobyte_ctx {
   DevBuf<unsigned int> barrier;  // grid barrier of K4 (2 words)
   DevBuf<int> flag;              // AUTOBYTE_CHECK device flag
   // per-call workspace
-  DevBuf<float> a, what, beta, x, adapt_ws, loss_tmp;
+  DevBuf<float> jobvec, x, adapt_ws, loss_tmp;
+  DevBuf<float2> u;                  // [shard] candidate encodings (K0)
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
   // staging for the *_host entry points
   DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
@@ -162,9 +165,7 @@ autobyte_status device_checks(autobyte_ctx* c, const autobyte_job_stats* jobs, c
 
 autobyte_status ensure_job_ws(autobyte_ctx* c, int J) {
   const int H = c->desc.hidden_width;
-  AB_CUDA(c, c->a.ensure((size_t)J * H));
-  AB_CUDA(c, c->what.ensure((size_t)J * H));
-  AB_CUDA(c, c->beta.ensure((size_t)J));
+  AB_CUDA(c, c->jobvec.ensure((size_t)J * (2 * H + 4)));
   AB_CUDA(c, c->keys.ensure((size_t)2 * J));
   AB_CUDA(c, c->x.ensure((size_t)J * kXDim));
   return AB_OK;
@@ -185,10 +186,15 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   autobyte_status st = ensure_job_ws(c, J);
   if (st != AB_OK) return st;
   EncodeParams ep = encode_params(c, jobs);
-  ep.x_out = c->x.ptr; ep.a_out = c->a.ptr; ep.what_out = c->what.ptr; ep.beta_out = c->beta.ptr;
+  const int H = c->desc.hidden_width;
+  ep.jv = 2 * H + 4;
+  ep.x_out = c->x.ptr; ep.a_out = c->jobvec.ptr; ep.what_out = c->jobvec.ptr + H; ep.beta_out = c->jobvec.ptr + 2 * H;
   ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
   AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
   c->launches[K_ENCODE] += 1;   // launch_encode issued K1a + K1b (projections)
+  // K0: candidate encodings u_c of this shard (§8(a) a-1), 8 bytes per candidate
+  AB_CUDA(c, c->u.ensure((size_t)(grid->shard_end - grid->shard_begin)));
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_grid(*grid, c->u.ptr, c->stream); }));
 
   ScoreParams sp{};
   sp.J = J; sp.H = c->desc.hidden_width; sp.G = c->desc.hidden_layers - 1;
@@ -199,8 +205,11 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.n_tiles = (long long)sp.tiles_per_job * J;
   sp.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); sp.S_c = grid->credit_mult;
   sp.params = c->params.ptr; sp.off = c->off;
-  sp.a = c->a.ptr; sp.what = c->what.ptr; sp.beta = c->beta.ptr;
+  sp.jobvec = c->jobvec.ptr;
+  sp.u = c->u.ptr;
   sp.wpack = c->wpack.ptr;
+  sp.wmap = c->wmap;
+  sp.cta_group = c->cta_group;
   sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
   sp.cur_idx = cur_idx; sp.scores = scores;
   AB_CUDA(c, timed(c, K_SCORE, [&] { return launch_score(sp, c->num_sms, c->stream); }));
@@ -321,6 +330,15 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers);
   if ((e = c->wpack.ensure(wp ? wp : 1)) != cudaSuccess) return bail(e, "alloc wpack");
   if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
+  // K2 variant: CTA pairs win when the head is deep and wide (4x512: 1158 vs 1133 TFLOP/s),
+  // single CTAs win on smaller heads (3x256: 726 vs 580); AUTOBYTE_CTA_GROUP=1|2 overrides.
+  const char* cg = std::getenv("AUTOBYTE_CTA_GROUP");
+  c->cta_group = (desc->hidden_width == 512 && desc->hidden_layers >= 4) ? 2 : 1;
+  if (cg && (cg[0] == '1' || cg[0] == '2')) c->cta_group = cg[0] - '0';
+  if (!make_weight_tmap(&c->wmap, c->wpack.ptr, desc->hidden_width, desc->hidden_layers)) {
+    autobyte_destroy(c);
+    return AB_E_CUDA;
+  }
   if ((e = cudaMemsetAsync(c->barrier.ptr, 0, 2 * sizeof(unsigned int), c->stream)) != cudaSuccess)
     return bail(e, "memset barrier");
   if ((e = timed(c, K_PACK, [&] {
@@ -342,7 +360,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   }
   if (c->comm) ncclCommDestroy(c->comm);
   c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
-  c->a.release(); c->what.release(); c->beta.release(); c->x.release(); c->adapt_ws.release();
+  c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
   c->loss_tmp.release(); c->keys.release();
   c->sT.release(); c->sBd.release(); c->sBu.release(); c->sSc.release(); c->sV.release();
   c->rScore.release(); c->rCur.release();

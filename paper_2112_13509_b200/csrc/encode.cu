@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     if (p.beta_out) {
       float acc = 0.f;
       for (int w = 0; w < n; ++w) acc += P[p.off.b_o + w];
-      p.beta_out[j] = acc / static_cast<float>(n);
+      p.beta_out[(size_t)j * p.jv] = acc / static_cast<float>(n);
     }
     if (p.keys) p.keys[j] = 0ull;
     if (p.cur_keys) p.cur_keys[j] = 0ull;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
     const float b1 = P[p.off.b[1] + col];
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj)
-      if (jj < jn) p.a_out[(size_t)(j0 + jj) * H + col] = acc[jj] + b1;
+      if (jj < jn) p.a_out[(size_t)(j0 + jj) * p.jv + col] = acc[jj] + b1;
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
     for (int w = 0; w < kNMax; ++w) {
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
     }
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj)
-      if (jj < jn) p.what_out[(size_t)(j0 + jj) * H + col] = acc[jj];
+      if (jj < jn) p.what_out[(size_t)(j0 + jj) * p.jv + col] = acc[jj];
   }
 }
 
@@ -212,6 +212,27 @@ cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !p.a_out) return e;
   project_kernel<<<(p.J + kProjJobs - 1) / kProjJobs, kProjThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K0: candidate encodings
+// u_c = ((log2 S_p - 21) / 8, (S_c - 8.5) / 8) for c = p*Q + q in [shard_begin, shard_end)
+// (R#8), computed in double and rounded once to fp32.
+__global__ void encode_grid_kernel(int Q, long long c0, long long n, const long long* __restrict__ S_p,
+                                   const float* __restrict__ S_c, float2* __restrict__ u) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = c0 + i;
+    const long long pi = c / Q, qi = c % Q;
+    u[i] = make_float2(static_cast<float>((log2(static_cast<double>(S_p[pi])) - 21.0) / 8.0),
+                       static_cast<float>((static_cast<double>(S_c[qi]) - 8.5) / 8.0));
+  }
+}
+
+cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s) {
+  const long long n = g.shard_end - g.shard_begin;
+  const long long blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+  encode_grid_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
+      g.Q, g.shard_begin, n, reinterpret_cast<const long long*>(g.partition_bytes), g.credit_mult, u);
   return cudaGetLastError();
 }
 

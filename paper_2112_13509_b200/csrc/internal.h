@@ -1,5 +1,6 @@
 // internal.h — library-private declarations shared by the .cu files of libautobyte.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -37,14 +38,18 @@ struct EncodeParams {
   const int32_t* n; const int32_t* l; const int32_t* m; const int32_t* arc;
   const float* params; ParamOffsets off;
   float* x_out;        // [J][82] or null
-  float* a_out;        // [J][H] = W1x x + b1, or null
-  float* what_out;     // [J][H] = mean of the first n rows of W_o, or null
-  float* beta_out;     // [J]    = mean of the first n entries of b_o, or null
+  // per-job vectors, row stride jv floats (K2 reads one contiguous block [a | w | beta] per job)
+  long long jv;
+  float* a_out;        // [J][jv]: W1x x + b1 in [0, H), or null
+  float* what_out;     // [J][jv]: mean of the first n rows of W_o, or null
+  float* beta_out;     // [J][jv]: mean of the first n entries of b_o, or null
   unsigned long long* keys;      // [J] reset to 0, or null
   unsigned long long* cur_keys;  // [J] reset to 0, or null
 };
 
-struct ScoreParams {
+struct alignas(64) ScoreParams {
+  CUtensorMap wmap;             // 2-D view of wpack (rows of 128 B) for the CTA-pair TMA loads
+  int cta_group;                // 1: one CTA per tile (M = 128); 2: CTA pairs (M = 256)
   int J, H, G;                  // G = L - 1 tensor-core layers
   int P, Q;
   long long c_begin, c_end;     // shard [begin, end)
@@ -54,9 +59,8 @@ struct ScoreParams {
   const float* S_c;             // [Q]
   const float* params;          // fp32 masters (W1's u-columns, biases)
   ParamOffsets off;
-  const float* a;               // [J][H]
-  const float* what;            // [J][H]
-  const float* beta;            // [J]
+  const float* jobvec;          // [J][2H+4]: a_j | w_j | beta_j, 0, 0, 0  (K1)
+  const float2* u;              // [c_end - c_begin] candidate encodings (K0)
   const __nv_bfloat16* wpack;   // packed bf16 W_2..W_L (see pack_weights)
   unsigned long long* keys;     // [J]
   unsigned long long* cur_keys; // [J]
@@ -83,6 +87,7 @@ struct AdaptParams {
 // ---------------------------------------------------------------- launches (return cudaError_t)
 cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s);
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s);
 cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigned long long* cur_keys,
                             int32_t* best_idx, float* best_score, float* cur_score, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, __nv_bfloat16* wpack,
@@ -93,6 +98,7 @@ size_t adapt_ws_floats(int B, int H, int L);
 cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
-size_t score_smem_bytes(int H);
+size_t score_smem_bytes(int H, int cta_group);
+bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L);
 
 }  // namespace ab

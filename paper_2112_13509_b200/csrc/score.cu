@@ -15,114 +15,190 @@
 //               NS-stage shared-memory ring with cp.async.bulk (L2 evict_last: every CTA
 //               re-reads the same 1.5 MB at 4x512, so they stay L2-resident).
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.
-//   warps 2..9  epilogue: 2 warps per TMEM lane quadrant, each owning half of the columns.
+//   warps 2..17 epilogue: 4 warps per TMEM lane quadrant, each owning a quarter of the columns.
 // Activations ping-pong between buffer X (shared memory, UMMA SW128 K-major layout, used as
 // the A operand of SS-MMAs) and buffer Y (TMEM columns 256.., packed bf16 pairs, A operand
 // of TS-MMAs); accumulators are two 128-column TMEM chunks so the epilogue of chunk q
 // overlaps the MMAs of chunk q+1. The next tile's h1 is built during the last layer.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace ab {
 
-template <int H>
+#ifndef AB_KBS
+#define AB_KBS 2   // 64-wide K blocks per weight stage for CTA pairs
+#endif
+
+// Optional cycle accounting (build with -DAB_STATS): where each warp role spends its time.
+#ifdef AB_STATS
+__device__ unsigned long long g_ab_stats[16];
+#define AB_T0(v) const long long v = clock64()
+#define AB_ACC(st, i, v) (st)[i] += clock64() - (v)
+__device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3][1024 events][code, clock]
+// timeline of CTAs 0/1 for their third work unit, plain stores into per-role regions (no atomics)
+#define AB_TRACE(on, ev, g, q)                                                                   \
+  do {                                                                                           \
+    if ((on) && blockIdx.x < 2) {                                                                \
+      const int _role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;                       \
+      unsigned long long* _r = g_ab_trace + ((size_t)(blockIdx.x * 4 + _role) * 1024) * 2;       \
+      if (trace_n < 1023) {                                                                      \
+        _r[2 * trace_n] = ((unsigned long long)blockIdx.x << 32) | ((ev) << 16) | ((g) << 8) | (q); \
+        _r[2 * trace_n + 1] = clock64();                                                         \
+        ++trace_n;                                                                               \
+      }                                                                                          \
+    }                                                                                            \
+  } while (0)
+#else
+#define AB_TRACE(on, ev, g, q)
+#define AB_T0(v)
+#define AB_ACC(st, i, v)
+#endif
+
+template <int H, int CG>
 struct ScoreCfg {
   static constexpr int NCH = H >= 128 ? 128 : H;  // N of one MMA / one TMEM accumulator chunk
   static constexpr int NQ = H / NCH;              // chunks per layer
   static constexpr int NKB = H / 64;              // 64-element K blocks per layer
   static constexpr int KB_PER_Q = NCH / 64;       // K blocks of the next layer produced by one chunk
   static constexpr int STAGE_BYTES = NCH * 128;   // one (chunk, K block) weight tile
+  static constexpr int KBS = (CG == 2 && NKB >= 2) ? AB_KBS : 1;  // K blocks per pipeline stage
+  static constexpr int ATOM_BYTES = STAGE_BYTES / CG;        // this CTA's part of one K block (N-half for CG=2)
+  static constexpr int CTA_STAGE_BYTES = ATOM_BYTES * KBS;   // this CTA's bytes per stage
+  static constexpr int STAGE_TX = STAGE_BYTES * KBS;         // bytes per stage over the pair
   static constexpr int A_BYTES = kTileM * H * 2;  // bf16 activation tile, buffer X
-  static constexpr int HALF = NCH / 2;            // columns per epilogue warp per chunk
+  static constexpr int NSPLIT = 4;                // epilogue warps per TMEM lane quadrant
+  static constexpr int QC = NCH / NSPLIT;         // columns per epilogue warp per chunk
   static constexpr int G_CAP = H == 512 ? 3 : 7;  // hidden-layer biases kept in shared memory
   static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
-  static constexpr int WHAT_BYTES = 2 * H * 4;    // w_j, two tile slots
+  static constexpr int WV = H + 4;                // w_j | beta_j, 0, 0, 0 (one tile slot)
+  static constexpr int WHAT_BYTES = 2 * WV * 4;   // two tile slots
   static constexpr int BIAS_BYTES = G_CAP * H * 4;
-  static constexpr int PART_BYTES = 2 * kTileM * 4;
+  static constexpr int PART_BYTES = NSPLIT * kTileM * 4;
   static constexpr int MISC_BYTES = 512;
   static constexpr int FIXED = A_BYTES + AW_BYTES + WHAT_BYTES + BIAS_BYTES + PART_BYTES + MISC_BYTES;
   static constexpr int BUDGET = 232448 - 1024;    // opt-in maximum minus the 1 KB alignment slack
-  static constexpr int NS_FIT = (BUDGET - FIXED) / STAGE_BYTES;
-  static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;
-  static constexpr int SMEM = 1024 + FIXED + NS * STAGE_BYTES;
-  static constexpr uint32_t IDESC = umma_idesc_bf16(128, NCH);
+  static constexpr int NS_FIT = (BUDGET - FIXED) / CTA_STAGE_BYTES;
+  static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;
+  static constexpr int SMEM = 1024 + FIXED + NS * CTA_STAGE_BYTES;
+  static constexpr uint32_t IDESC = umma_idesc_bf16(128 * CG, NCH);
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t Y_COL = 256;          // TMEM column of activation buffer Y
+  static constexpr int EPI_ARRIVALS = CG == 2 ? 17 : 16;   // leader's 16 warps (+1 forwarded by the peer)
   static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
   static_assert(SMEM <= 232448, "shared memory budget");
-  static_assert(STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
+  static_assert(CTA_STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
 };
 
-constexpr int kScoreThreads = 320;
-constexpr int kEpiThreads = 256;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kScoreThreads = 64 + kEpiThreads;
 constexpr uint32_t kEpiBar = 1;
+constexpr uint32_t kPeerBar = 2;
 
 // One output chunk of one layer: NKB weight stages x 4 MMAs (K = 16 each) into accumulator d_t.
 // A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address). For the first
-// chunk of a layer, K block b is only consumed once the epilogue has published the matching
+// chunk of a layer, K block b is only consumed once the epilogues have published the matching
 // 128-column piece of A (afull[b / KB_PER_Q]), so a layer starts before its input is complete.
-template <typename C, bool TS>
+template <typename C, int CG, bool TS>
 __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32_t a_tmem0, uint64_t b_desc0,
                                           uint64_t* full, uint64_t* empty, uint64_t* afull, uint32_t aph,
-                                          int& s, uint32_t& ph) {
+                                          int& s, uint32_t& ph, long long* st, bool trace_on, int g, int q,
+                                          int& trace_n) {
+  const int warp = 1;
+  (void)warp;
 #pragma unroll 1
-  for (int b = 0; b < C::NKB; ++b) {
+  for (int b = 0; b < C::NKB; b += C::KBS) {
     if (afull != nullptr && (b % C::KB_PER_Q) == 0) {
-      mbar_wait(&afull[b / C::KB_PER_Q], aph);
+      AB_T0(ta);
+      if (CG == 2) mbar_wait_cluster(&afull[b / C::KB_PER_Q], aph);
+      else mbar_wait(&afull[b / C::KB_PER_Q], aph);
+      AB_ACC(st, 2, ta);
       tc_fence_after();
     }
+    AB_T0(tf);
     mbar_wait(&full[s], ph);
+    AB_ACC(st, 1, tf);
+    AB_TRACE(trace_on && (threadIdx.x & 31) == 0, 42, g, q * 16 + b);
     tc_fence_after();
     if (elect_one()) {
-      const uint64_t bd = b_desc0 + static_cast<uint64_t>(s * (C::STAGE_BYTES >> 4));
+      const uint64_t bst = b_desc0 + static_cast<uint64_t>(s * (C::CTA_STAGE_BYTES >> 4));
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint32_t acc = (b | kk) != 0;
-        if (TS)
-          umma_ts(d_t, a_tmem0 + (b * 4 + kk) * 8, bd + 2 * kk, C::IDESC, acc);
-        else
-          umma_ss(d_t, a_desc0 + static_cast<uint64_t>(b * 1024 + 2 * kk), bd + 2 * kk, C::IDESC, acc);
+      for (int a = 0; a < C::KBS; ++a) {
+        const uint64_t bd = bst + static_cast<uint64_t>(a * (C::ATOM_BYTES >> 4));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t acc = ((b + a) | kk) != 0;
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>((b + a) * 1024 + 2 * kk);
+          const uint32_t at = a_tmem0 + ((b + a) * 4 + kk) * 8;
+          if (CG == 2) {
+            if (TS) umma_ts2(d_t, at, bd + 2 * kk, C::IDESC, acc);
+            else umma_ss2(d_t, ad, bd + 2 * kk, C::IDESC, acc);
+          } else {
+            if (TS) umma_ts(d_t, at, bd + 2 * kk, C::IDESC, acc);
+            else umma_ss(d_t, ad, bd + 2 * kk, C::IDESC, acc);
+          }
+        }
       }
-      umma_commit(&empty[s]);
+      if (CG == 2) umma_commit2(&empty[s]);
+      else umma_commit(&empty[s]);
     }
     __syncwarp();
     if (++s == C::NS) { s = 0; ph ^= 1; }
   }
 }
 
-template <int H>
+// CG = 1: one CTA per SM computes 128-candidate tiles (M = 128 MMAs).
+// CG = 2: a cluster of two CTAs on a TPC forms a CTA pair; each CTA owns one 128-candidate tile
+// (its A rows, its TMEM accumulators, its epilogue) and half of every weight stage (64 of the 128
+// output rows), and the leader issues M = 256 tcgen05.mma.cta_group::2 for both. Weight bytes
+// streamed from L2 per candidate are halved.
+template <int H, int CG>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
-  using C = ScoreCfg<H>;
+  using C = ScoreCfg<H, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
   uint8_t* sStage = sA + C::A_BYTES;
-  float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::STAGE_BYTES);   // [3][H]: a_j | W1c0 | W1c1
-  float* sWhat = sAw + 3 * H;                                             // [2][H]
-  float* sBias = sWhat + 2 * H;                                           // [G_CAP][H]
-  float* sPart = sBias + C::G_CAP * H;                                    // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + 2 * kTileM);
+  float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::CTA_STAGE_BYTES);   // [3][H]: a_j | W1c0 | W1c1
+  float* sWhat = sAw + 3 * H;                                                   // [2][WV]
+  float* sBias = sWhat + 2 * C::WV;                                             // [G_CAP][H]
+  float* sPart = sBias + C::G_CAP * H;                                          // [NSPLIT][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + C::NSPLIT * kTileM);
   uint64_t* full = bars;
   uint64_t* empty = full + C::NS;
   uint64_t* dfull = empty + C::NS;
   uint64_t* dempty = dfull + 2;
-  uint64_t* afull = dempty + 2;                                           // [NQ]
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(afull + C::NQ);
+  uint64_t* afull = dempty + 2;                                                 // [NQ]
+  uint64_t* vfull = afull + C::NQ;                                              // next tile's job vectors
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(vfull + 1);
   unsigned long long* sWkey = reinterpret_cast<unsigned long long*>(sTmem + 2);
-  float* sBeta = reinterpret_cast<float*>(sWkey + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.G;
   const int tpj = p.tiles_per_job;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int trace_n = 0;
+  (void)trace_n;
+  AB_T0(t_start);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kEpiWarps); }
-    for (int q = 0; q < C::NQ; ++q) mbar_init(&afull[q], kEpiWarps);
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::EPI_ARRIVALS); }
+    for (int q = 0; q < C::NQ; ++q) mbar_init(&afull[q], C::EPI_ARRIVALS);
+    mbar_init(vfull, 1);
     fence_barrier_init();
   }
-  if (warp == 1) { tmem_alloc(sTmem, C::TMEM_COLS); tmem_relinquish(); }
+  if (warp == 0 && CG == 2) prefetch_tmap(&p.wmap);
+  if (warp == 1) {
+    if (CG == 2) { tmem_alloc2(sTmem, C::TMEM_COLS); tmem_relinquish2(); }
+    else { tmem_alloc(sTmem, C::TMEM_COLS); tmem_relinquish(); }
+  }
   if (warp >= 2) {
     const float* W1 = p.params + p.off.W[1];
     for (int k = threadIdx.x - 64; k < H; k += kEpiThreads) {
@@ -133,54 +209,77 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     for (int e = threadIdx.x - 64; e < gs * H; e += kEpiThreads) sBias[e] = p.params[p.off.b[e / H + 2] + e % H];
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sTmem;
-  const long long first = blockIdx.x, stride = gridDim.x;
+  // tile schedule: CG = 1 -> tile = first + i*stride; CG = 2 -> pair-tile pt, this CTA's tile 2*pt + rank
+  const long long n_units = CG == 2 ? (p.n_tiles + 1) / 2 : p.n_tiles;
+  const long long first = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
+  const long long stride = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
 
   if (warp == 0) {
-    // ================================================================ TMA producer
+    // ================================================================ TMA producer (both CTAs)
     if (G > 0) {
       const uint64_t pol = l2_policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
-      for (long long t = first; t < p.n_tiles; t += stride)
+      for (long long u = first; u < n_units; u += stride)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
-            for (int b = 0; b < C::NKB; ++b) {
+            for (int b = 0; b < C::NKB; b += C::KBS) {
+              AB_T0(te);
               mbar_wait(&empty[s], ph ^ 1);
+              AB_ACC(st, 0, te);
+              AB_TRACE(u == first + 2 * stride && lane == 0, 40, g, q * 16 + b);
               if (elect_one()) {
-                mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-                const __nv_bfloat16* src = p.wpack + ((size_t)(g * C::NQ + q) * C::NKB + b) * (C::NCH * 64);
-                bulk_g2s(sStage + s * C::STAGE_BYTES, src, C::STAGE_BYTES, &full[s], pol);
+                const int ti = (g * C::NQ + q) * C::NKB + b;
+                if (CG == 2) {
+                  if (leader) mbar_arrive_expect_tx(&full[s], C::STAGE_TX);   // both halves of KBS blocks
+#pragma unroll
+                  for (int a = 0; a < C::KBS; ++a)
+                    tma_load_2d_pair(sStage + s * C::CTA_STAGE_BYTES + a * C::ATOM_BYTES, &p.wmap, 0,
+                                     (ti + a) * C::NCH + static_cast<int>(rank) * (C::NCH / 2), &full[s], pol);
+                } else {
+                  mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+                  bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)ti * (C::NCH * 64), C::STAGE_BYTES,
+                           &full[s], pol);
+                }
               }
               __syncwarp();
               if (++s == C::NS) { s = 0; ph ^= 1; }
             }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer (warp-converged;
-    // one elected lane issues, so every operand is warp-uniform and lives in uniform registers)
-    if (G > 0) {
+    // ================================================================ MMA issuer (leader only;
+    // warp-converged, one elected lane issues, operands are warp-uniform)
+    if (G > 0 && leader) {
       int s = 0;
       uint32_t ph = 0, aph = 0, dbits = 0;
       int dq = 0, b0 = 0;
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sStage));
-      for (long long t = first; t < p.n_tiles; t += stride) {
+      for (long long u = first; u < n_units; u += stride) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
           for (int q = 0; q < C::NQ; ++q) {
-            mbar_wait(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
+            AB_T0(td);
+            if (CG == 2) mbar_wait_cluster(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
+            else mbar_wait(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
+            AB_ACC(st, 0, td);
+            AB_TRACE(u == first + 2 * stride, 10, g, q);
             dbits ^= 1u << dq;
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
             uint64_t* aw = q == 0 ? afull : nullptr;
             if (src == 0)
-              mma_chunk<C, false>(d_t, a_desc0, 0u, b_desc0, full, empty, aw, aph, s, ph);
+              mma_chunk<C, CG, false>(d_t, a_desc0, 0u, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
             else
-              mma_chunk<C, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph);
-            if (elect_one()) umma_commit(&dfull[dq]);
+              mma_chunk<C, CG, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
+            if (elect_one()) {
+              if (CG == 2) umma_commit2(&dfull[dq]);
+              else umma_commit(&dfull[dq]);
+            }
+            AB_TRACE(u == first + 2 * stride && lane == 0, 12, g, q);
             __syncwarp();
             dq ^= 1;
           }
@@ -192,40 +291,67 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   } else {
     // ================================================================ epilogue (256 threads)
     const int etid = threadIdx.x - 64;
-    const int ew = warp - 2, quad = warp & 3, half = ew >> 2;
+    const int ew = warp - 2, quad = warp & 3, grp = ew >> 2;   // grp: column group of a chunk
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16);
     const long long cshard = p.c_end - p.c_begin;
     const float* w0s = sAw + H;
     const float* w1s = sAw + 2 * H;
-
-    auto load_vecs = [&](int slot, long long tile) {
-      const int j = static_cast<int>(tile / tpj);
-      const float* a = p.a + (size_t)j * H;
-      const float* w = p.what + (size_t)j * H;
-      for (int k = etid; k < H; k += kEpiThreads) {
-        sAw[k] = a[k];
-        sWhat[slot * H + k] = w[k];
+    // the MMA issuer's barriers live in the leader CTA
+    // CG = 2: the leader's 8 epilogue warps arrive locally; the peer's 8 warps meet at a named
+    // barrier and one thread forwards a single cluster-scope arrive to the leader's barrier
+    const uint32_t dempty_c[2] = {mapa_shared(smem_u32(&dempty[0]), 0), mapa_shared(smem_u32(&dempty[1]), 0)};
+    auto my_tile = [&](long long u) { return CG == 2 ? 2 * u + rank : u; };
+    auto signal = [&](uint64_t* bar, uint32_t cluster_addr) {   // called by the whole warp
+      if (CG == 2 && !leader) {
+        named_bar_sync(kPeerBar, kEpiThreads);
+        if (etid == 0) mbar_arrive_cluster(cluster_addr);
+      } else if (lane == 0) {
+        mbar_arrive(bar);
       }
-      if (etid == 0) sBeta[slot] = p.beta[j];
     };
+
+    const int jv = 2 * H + 4;
+    auto job_of = [&](long long tile) {
+      const long long tt = tile < p.n_tiles ? tile : p.n_tiles - 1;   // ghost tile of an odd pair
+      return static_cast<int>(tt / tpj);
+    };
+    // job vectors of `tile` -> a slot (single) and w|beta slot `slot`, synchronously
+    auto load_vecs = [&](int slot, long long tile) {
+      const float* v = p.jobvec + (size_t)job_of(tile) * jv;
+      for (int k = etid; k < H; k += kEpiThreads) sAw[k] = v[k];
+      for (int k = etid; k < C::WV; k += kEpiThreads) sWhat[slot * C::WV + k] = v[H + k];
+    };
+    // the same, as two TMA bulk copies completing on vfull (issued by one thread)
+    auto prefetch_vecs = [&](int slot, long long tile) {
+      if (etid == 0) {
+        const float* v = p.jobvec + (size_t)job_of(tile) * jv;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(vfull, (H + C::WV) * 4);
+        bulk_g2s(sAw, v, H * 4, vfull, 0ull);
+        bulk_g2s(sWhat + slot * C::WV, v + H, C::WV * 4, vfull, 0ull);
+      }
+    };
+    // candidate index and encoding (K0) of this thread's row of `tile`
     auto row_u = [&](long long tile, float& up, float& uc, long long& c) {
-      const int ct = static_cast<int>(tile % tpj);
+      const long long tt = tile < p.n_tiles ? tile : p.n_tiles - 1;
+      const int ct = static_cast<int>(tt % tpj);
       c = p.c_begin + (long long)ct * kTileM + row;
       const long long cc = c < p.c_end ? c : p.c_end - 1;
-      const long long pi = cc / p.Q, qi = cc % p.Q;
-      up = static_cast<float>((log2(static_cast<double>(p.S_p[pi])) - 21.0) / 8.0);   // R#8
-      uc = static_cast<float>((static_cast<double>(p.S_c[qi]) - 8.5) / 8.0);
+      const float2 uu = p.u[cc - p.c_begin];
+      up = uu.x;
+      uc = uu.y;
     };
-    auto store32 = [&](int dst, int c0, const uint32_t (&pk)[16]) {
+    // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
+    auto store_cols = [&](int dst, int c0, const uint32_t (&pk)[C::QC / 2]) {
       if (dst == 0) {  // buffer X: SW128 K-major, 16-byte chunk j of row r stored at chunk j ^ (r % 8)
         const uint32_t rowbase = smem_u32(sA) + (c0 >> 6) * 16384 + row * 128;
         const int j0 = (c0 & 63) >> 3;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < C::QC / 8; ++u)
           st_shared_v4(rowbase + (((j0 + u) ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       } else {         // buffer Y: TMEM, column = element pair index
-        tmem_st16(lane_base + C::Y_COL + (c0 >> 1), pk);
+        tmem_st_cols<C::QC / 2>(lane_base + C::Y_COL + (c0 >> 1), pk);
       }
     };
     // make this warp's part of A-chunk q visible to the tensor core and count the warp in
@@ -233,123 +359,139 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       if (dst == 0) fence_proxy_async_smem();
       else { tmem_st_wait(); tc_fence_before(); }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[q]);
+      signal(&afull[q], CG == 2 ? mapa_shared(smem_u32(&afull[q]), 0) : 0u);
     };
-    auto build_h1 = [&](float up, float uc, int dst) {
-#pragma unroll 1
-      for (int q = 0; q < C::NQ; ++q) {
+    // layer-1 activations h1 = ReLU(a_j + W1c u_c) for the 128-column piece q (this warp's columns)
+    auto build_piece = [&](int q, float up, float uc, int dst) {
+      const int c0 = q * C::NCH + grp * C::QC;
+      uint32_t pk[C::QC / 2];
 #pragma unroll
-        for (int hp = 0; hp < C::HALF / 32; ++hp) {
-          const int c0 = q * C::NCH + half * C::HALF + hp * 32;
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
-            const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
-            const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-            pk[2 * i] = pack_bf16x2(relu(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x))),
-                                    relu(fmaf(v4.y, uc, fmaf(u4.y, up, a4.y))));
-            pk[2 * i + 1] = pack_bf16x2(relu(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z))),
-                                        relu(fmaf(v4.w, uc, fmaf(u4.w, up, a4.w))));
-          }
-          store32(dst, c0, pk);
-        }
-        publish(dst, q);
+      for (int i = 0; i < C::QC / 4; ++i) {
+        const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+        const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
+        const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+        pk[2 * i] = pack_relu_bf16x2(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)), fmaf(v4.y, uc, fmaf(u4.y, up, a4.y)));
+        pk[2 * i + 1] = pack_relu_bf16x2(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)), fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
       }
+      store_cols(dst, c0, pk);
+      publish(dst, q);
     };
 
     int dq = 0, b0 = 0, it = 0;
-    uint32_t dbits = 0;
-    long long t = first;
-    if (t < p.n_tiles) load_vecs(0, t);
+    uint32_t dbits = 0, vph = 0;
+    long long u = first;
+    if (u < n_units) load_vecs(0, my_tile(u));
     named_bar_sync(kEpiBar, kEpiThreads);
-    if (G > 0 && t < p.n_tiles) {
+    if (G > 0 && u < n_units) {
       float up, uc;
       long long c;
-      row_u(t, up, uc, c);
-      build_h1(up, uc, 0);
+      row_u(my_tile(u), up, uc, c);
+#pragma unroll 1
+      for (int q = 0; q < C::NQ; ++q) build_piece(q, up, uc, 0);
     }
-    for (; t < p.n_tiles; t += stride, ++it) {
+    named_bar_sync(kEpiBar, kEpiThreads);   // every thread is done with the a-slot before it is refilled
+    for (; u < n_units; u += stride, ++it) {
       const int slot = it & 1;
-      const long long tn = t + stride;
-      const int j = static_cast<int>(t / tpj);
+      const long long t = my_tile(u);
+      const bool has_next = u + stride < n_units;
+      const long long tn = my_tile(u + stride);
+      const bool real = t < p.n_tiles;
+      const int j = static_cast<int>((real ? t : p.n_tiles - 1) / tpj);
       float up, uc;
       long long c;
       row_u(t, up, uc, c);
+      float up2 = 0.f, uc2 = 0.f;
+      if (G > 0 && has_next) {
+        // h1 of tile t is complete, so the a-slot is free: fetch the next tile's job vectors now
+        prefetch_vecs(slot ^ 1, tn);
+        long long c2;
+        row_u(tn, up2, uc2, c2);
+      }
       float dot = 0.f;
       if (G == 0) {
         if (it > 0) { load_vecs(slot, t); named_bar_sync(kEpiBar, kEpiThreads); }
-        const float* wv = sWhat + slot * H;
-        for (int k = half * (H / 2); k < (half + 1) * (H / 2); ++k)
+        const float* wv = sWhat + slot * C::WV;
+        for (int k = grp * (H / C::NSPLIT); k < (grp + 1) * (H / C::NSPLIT); ++k)
           dot = fmaf(relu(fmaf(w1s[k], uc, fmaf(w0s[k], up, sAw[k]))), wv[k], dot);
       }
       for (int g = 0; g < G; ++g) {
         const int src = (b0 + g) & 1, dst = src ^ 1;
         const bool last = (g == G - 1);
         const float* bias = g < C::G_CAP ? sBias + g * H : p.params + p.off.b[g + 2];
+        if (last && has_next) {
+          // the next tile's h1 is built one 128-column piece per chunk of this layer into the
+          // buffer this layer does not read (free once chunk 0's MMAs, so every earlier MMA, are done)
+          AB_T0(th);
+          mbar_wait(vfull, vph);
+          vph ^= 1;
+          AB_ACC(st, 3, th);
+        }
         for (int q = 0; q < C::NQ; ++q) {
+          AB_T0(tw);
           mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
+          AB_ACC(st, 0, tw);
+          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 20 + (warp == 17) * 10, g, q);
+          AB_T0(tl);
           dbits ^= 1u << dq;
           tc_fence_after();
-          uint32_t acc[2][32];
-          const uint32_t dcol = dq * C::NCH + half * C::HALF;
-          tmem_ld32(lane_base + dcol, acc[0]);
-          if (C::HALF == 64) tmem_ld32(lane_base + dcol + 32, acc[1]);
+          uint32_t acc[C::QC];
+          tmem_ld_cols<C::QC>(lane_base + dq * C::NCH + grp * C::QC, acc);
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&dempty[dq]);
+          signal(&dempty[dq], dempty_c[dq]);
+          AB_ACC(st, 1, tl);
+          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
+          AB_T0(tc);
           dq ^= 1;
-#pragma unroll
-          for (int hp = 0; hp < C::HALF / 32; ++hp) {
-            const int n0 = q * C::NCH + half * C::HALF + hp * 32;
+          {
+            const int n0 = q * C::NCH + grp * C::QC;
             const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
-            float v[32];
+            if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
+              uint32_t pk[C::QC / 2];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 bb = b4[i];
-              v[4 * i + 0] = relu(__uint_as_float(acc[hp][4 * i + 0]) + bb.x);
-              v[4 * i + 1] = relu(__uint_as_float(acc[hp][4 * i + 1]) + bb.y);
-              v[4 * i + 2] = relu(__uint_as_float(acc[hp][4 * i + 2]) + bb.z);
-              v[4 * i + 3] = relu(__uint_as_float(acc[hp][4 * i + 3]) + bb.w);
-            }
-            if (!last) {
-              uint32_t pk[16];
+              for (int i = 0; i < C::QC / 4; ++i) {
+                const float4 bb = b4[i];
+                pk[2 * i] = pack_relu_bf16x2(__uint_as_float(acc[4 * i]) + bb.x, __uint_as_float(acc[4 * i + 1]) + bb.y);
+                pk[2 * i + 1] =
+                    pack_relu_bf16x2(__uint_as_float(acc[4 * i + 2]) + bb.z, __uint_as_float(acc[4 * i + 3]) + bb.w);
+              }
+              store_cols(dst, n0, pk);
+            } else {       // last hidden layer stays fp32: dot with the folded output row w_j (R#16)
+              const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * C::WV + n0);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-              store32(dst, n0, pk);
-            } else {
-              const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * H + n0);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float4 ww = w4[i];
-                dot = fmaf(v[4 * i], ww.x, dot);
-                dot = fmaf(v[4 * i + 1], ww.y, dot);
-                dot = fmaf(v[4 * i + 2], ww.z, dot);
-                dot = fmaf(v[4 * i + 3], ww.w, dot);
+              for (int i = 0; i < C::QC / 4; ++i) {
+                const float4 bb = b4[i], ww = w4[i];
+                dot = fmaf(relu(__uint_as_float(acc[4 * i]) + bb.x), ww.x, dot);
+                dot = fmaf(relu(__uint_as_float(acc[4 * i + 1]) + bb.y), ww.y, dot);
+                dot = fmaf(relu(__uint_as_float(acc[4 * i + 2]) + bb.z), ww.z, dot);
+                dot = fmaf(relu(__uint_as_float(acc[4 * i + 3]) + bb.w), ww.w, dot);
               }
             }
           }
           if (!last) publish(dst, q);
-          if (last && q == 0 && tn < p.n_tiles) {
-            // next tile's h1 goes into the buffer the last layer does not read
-            load_vecs(slot ^ 1, tn);
-            named_bar_sync(kEpiBar, kEpiThreads);
-            float up2, uc2;
-            long long c2;
-            row_u(tn, up2, uc2, c2);
-            build_h1(up2, uc2, src ^ 1);
+          AB_ACC(st, 2, tc);
+          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
+          if (last && has_next) {
+            AB_T0(th);
+            build_piece(q, up2, uc2, src ^ 1);
+            AB_ACC(st, 3, th);
+            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
           }
         }
       }
       if (G > 0) b0 = ((b0 + G - 1) & 1) ^ 1;
 
       // ------------------------------------------------ score, arg-max key, per-job reduction
-      sPart[half * kTileM + row] = dot;
+      AB_T0(tr);
+      sPart[grp * kTileM + row] = dot;
       named_bar_sync(kEpiBar, kEpiThreads);
-      if (half == 0) {
-        const float score = sPart[row] + sPart[kTileM + row] + sBeta[slot];
-        const bool valid = c < p.c_end;
+      if (grp == 0) {
+        float score = sPart[row];
+#pragma unroll
+        for (int i = 1; i < C::NSPLIT; ++i) score += sPart[i * kTileM + row];
+        score += sWhat[slot * C::WV + H];
+        const bool valid = real && c < p.c_end;
         if (valid && p.scores) p.scores[(size_t)j * cshard + (c - p.c_begin)] = score;
         const uint32_t o = ord32(score);
         unsigned long long key = (valid && o) ? ((static_cast<unsigned long long>(o) << 32) |
@@ -365,42 +507,81 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         if (lane == 0) sWkey[quad] = key;
       }
       named_bar_sync(kEpiBar, kEpiThreads);
-      if (etid == 0) {
+      if (etid == 0 && real) {
         unsigned long long k = sWkey[0];
         for (int i = 1; i < 4; ++i) k = sWkey[i] > k ? sWkey[i] : k;
         if (k) atomicMax(p.keys + j, k);
       }
+      AB_ACC(st, 4, tr);
+      AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 24 + (warp == 17) * 10, 0, 0);
     }
   }
+#ifdef AB_STATS
+  // slots: 0-3 producer/MMA/epilogue waits, see tools/kstats.py
+  if (lane == 0 && rank == 0) {
+    const long long total = clock64() - t_start;
+    if (warp == 0) { atomicAdd(&g_ab_stats[0], st[0]); atomicAdd(&g_ab_stats[1], total); }
+    if (warp == 1) {
+      atomicAdd(&g_ab_stats[2], st[0]); atomicAdd(&g_ab_stats[3], st[1]);
+      atomicAdd(&g_ab_stats[4], st[2]); atomicAdd(&g_ab_stats[5], total);
+    }
+    if (warp >= 2) {
+      for (int i = 0; i < 5; ++i) atomicAdd(&g_ab_stats[6 + i], st[i]);
+      atomicAdd(&g_ab_stats[11], total);
+    }
+  }
+#endif
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2) tmem_dealloc2(tmem, C::TMEM_COLS);
+    else tmem_dealloc(tmem, C::TMEM_COLS);
+  }
 }
 
-size_t score_smem_bytes(int H) {
-  switch (H) {
-    case 64: return ScoreCfg<64>::SMEM;
-    case 128: return ScoreCfg<128>::SMEM;
-    case 256: return ScoreCfg<256>::SMEM;
-    case 512: return ScoreCfg<512>::SMEM;
+template <int H, int CG>
+static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
+  using C = ScoreCfg<H, CG>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<H, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
-  return 0;
+  const long long units = CG == 2 ? (p.n_tiles + 1) / 2 : p.n_tiles;
+  const long long max_units = num_sms / CG;
+  const long long grid = (units < max_units ? units : max_units) * CG;
+  if (grid < 1) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kScoreThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG>, p);
 }
 
 template <int H>
 static cudaError_t launch_score_h(const ScoreParams& p, int num_sms, cudaStream_t s) {
-  using C = ScoreCfg<H>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  if (p.cta_group == 2) return launch_score_hc<H, 2>(p, num_sms, s);
+  return launch_score_hc<H, 1>(p, num_sms, s);
+}
+
+size_t score_smem_bytes(int H, int cg) {
+  switch (H) {
+    case 64: return cg == 2 ? ScoreCfg<64, 2>::SMEM : ScoreCfg<64, 1>::SMEM;
+    case 128: return cg == 2 ? ScoreCfg<128, 2>::SMEM : ScoreCfg<128, 1>::SMEM;
+    case 256: return cg == 2 ? ScoreCfg<256, 2>::SMEM : ScoreCfg<256, 1>::SMEM;
+    case 512: return cg == 2 ? ScoreCfg<512, 2>::SMEM : ScoreCfg<512, 1>::SMEM;
   }
-  long long grid = p.n_tiles < num_sms ? p.n_tiles : num_sms;
-  if (grid < 1) return cudaSuccess;
-  score_kernel<H><<<static_cast<int>(grid), kScoreThreads, C::SMEM, s>>>(p);
-  return cudaGetLastError();
+  return 0;
 }
 
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s) {
@@ -472,4 +653,50 @@ cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int
   return cudaGetLastError();
 }
 
+}  // namespace ab
+
+#ifdef AB_STATS
+extern "C" int ab_debug_trace(unsigned long long* out, int n, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, ab::g_ab_trace, sizeof(unsigned long long) * 2 * n) != cudaSuccess) return -1;
+  if (reset) cudaMemset(out, 0, 0);
+  static unsigned long long z[8 * 1024 * 2];
+  if (reset) cudaMemcpyToSymbol(ab::g_ab_trace, z, sizeof(z));
+  return n;
+}
+extern "C" int ab_debug_stats(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, ab::g_ab_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(ab::g_ab_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
+namespace ab {
+// Tensor map over the packed weights: a 2-D array of 128-byte rows (64 bf16), SWIZZLE_NONE (the
+// data is pre-swizzled), box = 64 bf16 x NCH/2 rows = one CTA's half of a weight stage.
+bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const int NCH = H >= 128 ? 128 : H;
+  const size_t rows = packed_weight_elems(H, L) / 64;
+  if (rows == 0) { std::memset(map, 0, sizeof(*map)); return true; }
+  cuuint64_t dims[2] = {64, rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(NCH / 2)};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(wpack), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace ab

@@ -23,9 +23,15 @@ def need_gpu():
     autobyte.load_library()
 
 
-def make(L, H, W):
+def make(L, H, W, cta_group=2):
+    """A context; cta_group selects the K2 variant (2 = CTA pairs, the default; 1 = single CTAs)."""
+    import os
     from paper_2112_13509_b200.autobyte import AutoByte
-    return AutoByte(L, H, W, device=0)
+    os.environ["AUTOBYTE_CTA_GROUP"] = str(cta_group)
+    try:
+        return AutoByte(L, H, W, device=0)
+    finally:
+        os.environ.pop("AUTOBYTE_CTA_GROUP", None)
 
 
 def dev(jobs, grid=None):
@@ -126,12 +132,13 @@ def dyadic_net(L, H, seed):
     return W, jobs, grid, alive
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("L,H", [(1, 64), (2, 64), (3, 64), (2, 128), (3, 256), (4, 512), (2, 512)])
-def test_exact_dyadic_bit_for_bit(L, H):
+def test_exact_dyadic_bit_for_bit(L, H, cg):
     W, jobs, grid, alive = dyadic_net(L, H, seed=L * 1000 + H)
     assert min(alive) > 0.2, alive
     s_ora = oracle.score_matrix(W, jobs, grid)
-    net = make(L, H, W)
+    net = make(L, H, W, cg)
     s = gpu_scores(net, jobs, grid).astype(np.float64)
     mism = np.flatnonzero(s[0] != s_ora[0])
     assert mism.size == 0, f"{mism.size} mismatches, first {mism[:5]}: gpu {s[0, mism[:5]]} oracle {s_ora[0, mism[:5]]}"
@@ -142,14 +149,15 @@ CASES = [(1, 64, 7, 9), (2, 64, 8, 8), (2, 128, 7, 13), (3, 128, 5, 31), (3, 256
          (2, 512, 9, 11), (4, 512, 33, 7)]
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("L,H,P,Q", CASES)
-def test_scores_and_argmax_vs_oracle(L, H, P, Q):
+def test_scores_and_argmax_vs_oracle(L, H, P, Q, cg):
     desc = synth.NetDesc(L, H)
     W = synth.make_weights(desc, seed=L * 31 + H)
     jobs = synth.small_fleet(5, L + H)
     grid = synth.log_grid(P, Q)
     s_ora = oracle.score_matrix(W, jobs, grid)
-    net = make(L, H, W)
+    net = make(L, H, W, cg)
     s = gpu_scores(net, jobs, grid)
     err = check_scores(s, s_ora, RTOL)
     bi, bs, _ = gpu_argmax(net, jobs, grid)
@@ -187,6 +195,7 @@ def test_shards_combine_to_full_and_determinism():
     grid = synth.log_grid(20, 17)
     net = make(L, H, W)
     full = gpu_scores(net, jobs, grid)
+    assert np.array_equal(full, gpu_scores(make(L, H, W, 1), jobs, grid))   # both K2 variants agree bitwise
     again = gpu_scores(net, jobs, grid)
     assert np.array_equal(full, again)
     C = grid.C
