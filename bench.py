@@ -175,7 +175,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2112_13509_b200.autobyte import AutoByte, DeviceGrid, DeviceJobs, get_unique_id, shard_bounds
+    from paper_2112_13509_b200 import dist as abd
+    from paper_2112_13509_b200.autobyte import AutoByte, DeviceGrid, DeviceJobs, shard_bounds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -190,10 +191,7 @@ def run_ours(args):
     begin, end = shard_bounds(C, rank, world)
     stream = torch.cuda.current_stream(dev)
     net = AutoByte(L, H, W, device=local, stream=stream)
-    if world > 1:
-        uid = [get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        net.attach_comm(uid[0], rank, world)
+    abd.attach(net)
 
     jobs, grid = DeviceJobs.from_host(c.jobs, dev), DeviceGrid.from_host(c.grid, dev)
     cur_t = torch.as_tensor(cur, dtype=torch.int32, device=dev)

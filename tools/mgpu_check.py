@@ -1,0 +1,79 @@
+"""Multi-GPU parity (run under torchrun, one rank per GPU): candidate-sharded arg-max with the NCCL
+key exchange must be bit-identical on every rank and to the single-GPU result (G-invariance), and
+agree with the float64 oracle on sampled jobs. Prints one JSON line per config on rank 0."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2112_13509_b200 import dist as abd  # noqa: E402
+from paper_2112_13509_b200.autobyte import AutoByte, DeviceGrid, DeviceJobs  # noqa: E402
+from tests.helpers import check_argmax  # noqa: E402
+
+
+def run(name, desc, jobs, grid, cg, dev, rank, world):
+    W = synth.make_weights(desc)
+    os.environ["AUTOBYTE_CTA_GROUP"] = str(cg)
+    net = AutoByte(desc.hidden_layers, desc.hidden_width, W, device=dev.index)
+    abd.attach(net)
+    dj, dg = DeviceJobs.from_host(jobs, dev), DeviceGrid.from_host(grid, dev)
+    cur = torch.as_tensor(synth.current_configs(jobs.J, grid.C, 9), dtype=torch.int32, device=dev)
+    b, e = abd.my_shard(grid.C)
+    bi, bs, cs = net.argmax(dj, dg, cur, b, e)
+    torch.cuda.synchronize(dev)
+    packed = torch.cat([bi.view(torch.int32), bs.view(torch.int32), cs.view(torch.int32)])
+    allp = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(allp, packed)
+    same_all_ranks = all(torch.equal(allp[0], x) for x in allp)
+    res = {"config": name, "world": world, "cta_group": cg, "same_on_all_ranks": same_all_ranks}
+    if rank == 0:
+        single = AutoByte(desc.hidden_layers, desc.hidden_width, W, device=dev.index)
+        bi1, bs1, cs1 = single.argmax(dj, dg, cur)
+        torch.cuda.synchronize(dev)
+        res["g_invariant"] = bool(torch.equal(bi, bi1) and torch.equal(bs.view(torch.int32), bs1.view(torch.int32))
+                                  and torch.equal(torch.nan_to_num(cs), torch.nan_to_num(cs1)))
+        sample = [0, jobs.J // 2, jobs.J - 1]
+        s_ora = oracle.score_matrix(W, jobs, grid, job_idx=sample)
+        check_argmax(bi.cpu().numpy()[sample], s_ora, 2e-2)
+        res["oracle_sampled_ok"] = True
+        single.close()
+    net.close()
+    return res
+
+
+def main():
+    dist.init_process_group("nccl")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    ok = True
+    c3 = synth.config("C3")
+    ragged = synth.log_grid(37, 29)
+    cases = [("C3", c3.desc, c3.jobs, c3.grid, 1), ("C3-ragged", c3.desc, c3.jobs.subset(np.arange(40)), ragged, 1),
+             ("C4-subset-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(300)),
+              synth.log_grid(64, 64), 2),
+             ("C4-subset-ragged-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(33)),
+              synth.log_grid(45, 23), 2)]
+    for name, desc, jobs, grid, cg in cases:
+        r = run(name, desc, jobs, grid, cg, dev, rank, world)
+        if rank == 0:
+            print(json.dumps(r), flush=True)
+            ok &= r["same_on_all_ranks"] and r["g_invariant"]
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_OK" if ok else "MGPU_FAIL", flush=True)
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
