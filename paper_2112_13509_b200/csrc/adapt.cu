@@ -19,6 +19,7 @@ namespace ab {
 
 constexpr int kAdaptThreads = 256;
 constexpr int kTM = 64, kTN = 64, kTK = 16;
+constexpr int kSplitK = kAdaptSplitK;   // K = B splits of the weight-gradient GEMMs (partials in grads[kSplitK][total])
 
 struct Gemm {
   int M, N, K;
@@ -30,42 +31,64 @@ struct Gemm {
   const float* bias;
   const float* mask; long long ldmask;
   const float* vbar; const int32_t* nvalid; float scale;
-  __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN); }
+  int ksplit;                            // split-K count (mode 2 only): partial s -> C + s*cpart
+  long long cpart;
+  __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
 };
 
-__device__ void gemm_tile(const Gemm& g, int tile, float (*As)[kTM + 4], float (*Bs)[kTN + 4]) {
+// One 64 x 64 output tile (or one K-slice of it for split-K). Each thread owns 4 x 4 outputs;
+// the next 16-wide K slice is fetched into registers while the current one is multiplied.
+__device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (*Bs)[kTN + 4]) {
   const int tiles_n = (g.N + kTN - 1) / kTN;
+  const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
+  const int split = g.ksplit > 1 ? work / tiles_mn : 0;
+  const int tile = work % tiles_mn;
   const int m0 = (tile / tiles_n) * kTM, n0 = (tile % tiles_n) * kTN;
+  int kbeg = 0, kend = g.K;
+  if (g.ksplit > 1) {
+    const int chunk = ((g.K + g.ksplit - 1) / g.ksplit + kTK - 1) / kTK * kTK;
+    kbeg = split * chunk;
+    kend = min(g.K, kbeg + chunk);
+  }
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < g.K; k0 += kTK) {
-    __syncthreads();
-    // stage a 16 x 64 slice of each operand; consecutive threads walk the operand's contiguous
-    // dimension (k when the row stride is not 1) so every warp load is coalesced
+  // per-thread staging coordinates (coalesced along each operand's contiguous dimension)
+  int aml[4], akl[4], bnl[4], bkl[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = tid + r * kAdaptThreads;
+    if (g.lak == 1) { akl[r] = e % kTK; aml[r] = e / kTK; } else { aml[r] = e % kTM; akl[r] = e / kTM; }
+    if (g.lbk == 1) { bkl[r] = e % kTK; bnl[r] = e / kTK; } else { bnl[r] = e % kTN; bkl[r] = e / kTN; }
+  }
+  float ra[4], rb[4];
+  auto fetch = [&](int k0) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const int e = tid + r * kAdaptThreads;
-      int ml, kl;
-      if (g.lak == 1) { kl = e % kTK; ml = e / kTK; } else { ml = e % kTM; kl = e / kTM; }
-      const int m = m0 + ml, k = k0 + kl;
-      As[kl][ml] = (m < g.M && k < g.K) ? g.A[m * g.lam + k * g.lak] : 0.f;
-      int nl, kb;
-      if (g.lbk == 1) { kb = e % kTK; nl = e / kTK; } else { nl = e % kTN; kb = e / kTN; }
-      const int n = n0 + nl, kk = k0 + kb;
-      Bs[kb][nl] = (n < g.N && kk < g.K) ? g.Bm[kk * g.lbk + n * g.lbn] : 0.f;
+      const int m = m0 + aml[r], k = k0 + akl[r];
+      ra[r] = (m < g.M && k < kend) ? g.A[m * g.lam + k * g.lak] : 0.f;
+      const int n = n0 + bnl[r], kk = k0 + bkl[r];
+      rb[r] = (n < g.N && kk < kend) ? g.Bm[kk * g.lbk + n * g.lbn] : 0.f;
     }
+  };
+  float acc[4][4] = {};
+  if (kbeg < kend) fetch(kbeg);
+  for (int k0 = kbeg; k0 < kend; k0 += kTK) {
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < kTK; ++kk) {
-      float a[4], b[4];
+    for (int r = 0; r < 4; ++r) { As[akl[r]][aml[r]] = ra[r]; Bs[bkl[r]][bnl[r]] = rb[r]; }
+    __syncthreads();
+    if (k0 + kTK < kend) fetch(k0 + kTK);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+    for (int kk = 0; kk < kTK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(a[i], b[jj], acc[i][jj]);
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(av[i], bv[jj], acc[i][jj]);
     }
   }
+  float* C = g.C + (g.ksplit > 1 ? split * g.cpart : 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;
@@ -78,7 +101,7 @@ __device__ void gemm_tile(const Gemm& g, int tile, float (*As)[kTM + 4], float (
       if (g.mode == 0) v = relu(v + g.bias[n]);
       else if (g.mode == 1) v = g.mask[m * g.ldmask + n] > 0.f ? v : 0.f;
       else if (g.mode == 3) v = (n < g.nvalid[m]) ? (v + g.bias[n] - g.vbar[m * 16 + n]) * g.scale : 0.f;
-      g.C[m * g.ldc + n] = v;
+      C[m * g.ldc + n] = v;
     }
   }
 }
@@ -183,7 +206,8 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
     if (fwd_only) break;
     // ---------------- backward: output layer
     {
-      Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f};
+      Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f,
+              kSplitK, p.off.total};
       Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H, nullptr, nullptr, 0.f};
       const int t1 = gw.tiles(), t2 = gd.tiles();
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
@@ -198,7 +222,8 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
       const int Kin = k == 1 ? kZDim : H;
       const float* in = k == 1 ? Z : Hk(k - 1);
       const float* Dk = D[k & 1];
-      Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f};
+      Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f,
+              kSplitK, p.off.total};
       const int t1 = gw.tiles();
       int t2 = 0;
       Gemm gd{};
@@ -216,7 +241,13 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
     }
     // ---------------- SGD on the head parameters (contiguous from W1 to b_o in the blob order)
     const float lr = p.lr;
-    for (long long i = p.off.W[1] + gtid; i < p.off.total; i += gthreads) P[i] = P[i] - lr * Gr[i];
+    // (the weight gradients arrive as kSplitK partial sums over B; summed here in fixed order)
+    for (long long i = p.off.W[1] + gtid; i < p.off.total; i += gthreads) {
+      float gsum = Gr[i];
+#pragma unroll
+      for (int sk = 1; sk < kSplitK; ++sk) gsum += Gr[sk * p.off.total + i];
+      P[i] = P[i] - lr * gsum;
+    }
     grid_sync(p.barrier, gen);
   }
 }

@@ -321,8 +321,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   };
   cudaError_t e;
   if ((e = c->params.ensure(c->off.total)) != cudaSuccess) return bail(e, "alloc params");
-  if ((e = c->grads.ensure(c->off.total)) != cudaSuccess) return bail(e, "alloc grads");
-  if ((e = cudaMemsetAsync(c->grads.ptr, 0, c->off.total * sizeof(float), c->stream)) != cudaSuccess)
+  if ((e = c->grads.ensure(c->off.total * kAdaptSplitK)) != cudaSuccess) return bail(e, "alloc grads");
+  if ((e = cudaMemsetAsync(c->grads.ptr, 0, c->off.total * kAdaptSplitK * sizeof(float), c->stream)) != cudaSuccess)
     return bail(e, "memset grads");
   if ((e = cudaMemcpyAsync(c->params.ptr, static_cast<const uint8_t*>(blob) + kBlobHeader,
                            c->off.total * sizeof(float), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)

@@ -1,140 +1,180 @@
 // encode.cu — K1: per-job prologue of the scoring path.
 //
-// K1a, one 256-thread CTA per job:
+// K1a, 16 jobs per 256-thread CTA:
 //   t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers (R#7, R#8); e_i = W_e t'_i + b_e (R#4)
 //   two-layer LSTM over i = 0..l_j-1, gates i,f,g,o, h0 = c0 = 0 ("two-layer LSTM", R#5);
-//     thread g owns gate row g of one layer with its weights held in registers
+//     thread (g, half) owns gate row g of both layers, weights in registers, for 8 jobs
 //   x_j = [h | log2 B_d | log2 B_u | n/16 | l/64 | E_m[m] | E_arc[arc]]   (Table 2)
 //   beta_j = (1/n) sum_{w<n} b_o[w], and resets the job's arg-max keys.
 // K1b, 32 jobs per CTA:
 //   a_j = W1[:, :82] x_j + b1     (layer-1 projection of the job half of the concatenation)
-//   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3) This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
+//   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3)
+// This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace ab {
 
-constexpr int kEncThreads = 256;   // threads 0..127: LSTM layer 1 gate rows; 128..255: layer 2
-constexpr int kChunk = 64;         // layers whose embeddings are staged in shared memory at a time
+constexpr int kEncThreads = 256;   // 128 LSTM gate rows x 2 job halves
+constexpr int kEncJobs = 16;       // jobs per CTA (8 per half)
+constexpr int kHalfJobs = kEncJobs / 2;
+constexpr int kChunk = 16;         // layers whose embeddings are staged in shared memory at a time
 
-__device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
+// logistic and tanh from the ex2 unit: |error| ~ 1e-7 absolute, well inside the 1e-4 / 2e-5
+// tolerance the encoder is held to against the float64 oracle (tests/test_gpu_parity.py)
+__device__ __forceinline__ float sigmoidf_acc(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
+__device__ __forceinline__ float tanh_acc(float z) { return 2.0f * sigmoidf_acc(2.0f * z) - 1.0f; }
 
-// dot of a register-resident weight row with a shared-memory vector, 4 independent partial sums
-template <int N>
-__device__ __forceinline__ float dot_row(const float (&w)[N], const float* v) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-  for (int d = 0; d < N; d += 4) {
-    a0 = fmaf(w[d], v[d], a0);
-    a1 = fmaf(w[d + 1], v[d + 1], a1);
-    a2 = fmaf(w[d + 2], v[d + 2], a2);
-    a3 = fmaf(w[d + 3], v[d + 3], a3);
-  }
-  return (a0 + a1) + (a2 + a3);
-}
-
-// K1a: one CTA per job. The two LSTM layers run as a wavefront: in iteration i layer 1 takes
-// step i while layer 2 takes step i-1 (both read h1 of step i-1 before it is overwritten).
+// K1a: 16 jobs per CTA. Thread (g, half) owns LSTM gate row g of both layers (weights in
+// registers) and evaluates it for the 8 jobs of its half, so each step is an FMA-rich
+// [8 jobs x 48|64] x [48|64] product per thread instead of a latency-bound matvec. Jobs with fewer
+// layers freeze after their last step (h, c kept), so the final h is the state at step l_j - 1.
 __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_constant__ EncodeParams p) {
-  __shared__ float sT[kChunk][kNMax];
-  __shared__ float sE[kChunk][kEmbed];
-  __shared__ float sG1[4 * kLstm], sG2[4 * kLstm];
-  __shared__ float sH1[kLstm], sH2[kLstm];
-  __shared__ float sX[kXDim + 2];
-  const int j = blockIdx.x, tid = threadIdx.x;
-  const int n = p.n[j], l = p.l[j], m = p.m[j], arc = p.arc[j];
+  __shared__ __align__(16) float sE[kEncJobs][kChunk][kEmbed];   // layer embeddings e_i of the chunk
+  __shared__ float sTl[kEncJobs][kChunk][kNMax];                  // log2(1 + T) of the chunk
+  __shared__ __align__(16) float sH1[kEncJobs][kLstm], sH2[kEncJobs][kLstm];
+  __shared__ float sG[kEncJobs][4 * kLstm];
+  float (*sX)[kXDim + 2] = reinterpret_cast<float (*)[kXDim + 2]>(&sTl[0][0][0]);   // reused after the LSTM
+  __shared__ int sN[kEncJobs], sL[kEncJobs];
+  const int tid = threadIdx.x;
+  const int g = tid & (4 * kLstm - 1), half = tid >> 7;
+  const int j0 = blockIdx.x * kEncJobs;
+  const int nj = min(kEncJobs, p.J - j0);
   const float* P = p.params;
-  const bool layer1 = tid < 4 * kLstm;
-  const int row = layer1 ? tid : tid - 4 * kLstm;
-
-  float wx[kLstm], wh[kLstm];   // layer 1 uses wx[0..15] only
-  if (layer1) {
-#pragma unroll
-    for (int d = 0; d < kEmbed; ++d) wx[d] = P[p.off.l1Wx + row * kEmbed + d];
-#pragma unroll
-    for (int d = kEmbed; d < kLstm; ++d) wx[d] = 0.f;
-#pragma unroll
-    for (int d = 0; d < kLstm; ++d) wh[d] = P[p.off.l1Wh + row * kLstm + d];
-  } else {
-#pragma unroll
-    for (int d = 0; d < kLstm; ++d) {
-      wx[d] = P[p.off.l2Wx + row * kLstm + d];
-      wh[d] = P[p.off.l2Wh + row * kLstm + d];
-    }
+  if (tid < kEncJobs) {
+    sN[tid] = tid < nj ? p.n[j0 + tid] : 1;
+    sL[tid] = tid < nj ? p.l[j0 + tid] : 0;
   }
-  const float bias = layer1 ? P[p.off.l1b + row] : P[p.off.l2b + row];
-  float c = 0.f;  // cell state: threads 0..31 (layer 1) and 128..159 (layer 2)
-  if (tid < kLstm) { sH1[tid] = 0.f; sH2[tid] = 0.f; }
+  for (int e = tid; e < kEncJobs * kLstm; e += kEncThreads) {
+    (&sH1[0][0])[e] = 0.f;
+    (&sH2[0][0])[e] = 0.f;
+  }
+  float wx1[kEmbed], wh1[kLstm], wx2[kLstm], wh2[kLstm];
+#pragma unroll
+  for (int d = 0; d < kEmbed; ++d) wx1[d] = P[p.off.l1Wx + g * kEmbed + d];
+#pragma unroll
+  for (int d = 0; d < kLstm; ++d) {
+    wh1[d] = P[p.off.l1Wh + g * kLstm + d];
+    wx2[d] = P[p.off.l2Wx + g * kLstm + d];
+    wh2[d] = P[p.off.l2Wh + g * kLstm + d];
+  }
+  const float bg1 = P[p.off.l1b + g], bg2 = P[p.off.l2b + g];
+  // cell states: thread owns (job = tid / 16, cells 2*(tid % 16), +1) of each layer
+  const int cj = tid >> 4, cc = (tid & 15) * 2;
+  float c1[2] = {0.f, 0.f}, c2[2] = {0.f, 0.f};
+  __syncthreads();
+  int lmax = 0;
+  for (int k = 0; k < kEncJobs; ++k) lmax = max(lmax, sL[k]);
 
-  const float* T = p.T + (size_t)j * p.l_max * kNMax;
-  for (int i0 = 0; i0 <= l; i0 += kChunk) {
-    const int len = min(kChunk, l - i0);
+  for (int i0 = 0; i0 < lmax; i0 += kChunk) {
+    const int len = min(kChunk, lmax - i0);
     __syncthreads();
-    for (int e = tid; e < len * kNMax; e += kEncThreads) {
-      const int i = e / kNMax, w = e % kNMax;
-      sT[i][w] = (w < n) ? log2f(1.0f + T[(size_t)(i0 + i) * kNMax + w]) : 0.f;
+    // t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers, 0 on padding (R#7, R#8)
+    for (int e = tid; e < kEncJobs * len * kNMax; e += kEncThreads) {
+      const int jj = e / (len * kNMax), r = e % (len * kNMax), i = r / kNMax, w = r % kNMax;
+      float v = 0.f;
+      if (jj < nj && i0 + i < sL[jj] && w < sN[jj]) v = log2f(1.0f + p.T[((size_t)(j0 + jj) * p.l_max + i0 + i) * kNMax + w]);
+      sTl[jj][i][w] = v;
     }
     __syncthreads();
-    for (int e = tid; e < len * kEmbed; e += kEncThreads) {
-      const int i = e / kEmbed, d = e % kEmbed;
+    // e_i = W_e t'_i + b_e (R#4)
+    for (int e = tid; e < kEncJobs * len * kEmbed; e += kEncThreads) {
+      const int jj = e / (len * kEmbed), r = e % (len * kEmbed), i = r / kEmbed, d = r % kEmbed;
       float acc = P[p.off.b_e + d];
 #pragma unroll
-      for (int w = 0; w < kNMax; ++w) acc = fmaf(P[p.off.W_e + d * kNMax + w], sT[i][w], acc);
-      sE[i][d] = acc;
+      for (int w = 0; w < kNMax; ++w) acc = fmaf(P[p.off.W_e + d * kNMax + w], sTl[jj][i][w], acc);
+      sE[jj][i][d] = acc;
     }
     __syncthreads();
-    const int iend = min(i0 + kChunk, l + 1);   // the wavefront runs one extra iteration
-    for (int i = i0; i < iend; ++i) {
-      if (layer1) {
-        if (i < l) {
-          float z = bias;
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-          const float* e = sE[i - i0];
+    for (int i = 0; i < len; ++i) {
+      // ---- layer 1 gates for the 8 jobs of this half
+      float z[kHalfJobs];
 #pragma unroll
-          for (int d = 0; d < kEmbed; d += 4) {
-            a0 = fmaf(wx[d], e[d], a0); a1 = fmaf(wx[d + 1], e[d + 1], a1);
-            a2 = fmaf(wx[d + 2], e[d + 2], a2); a3 = fmaf(wx[d + 3], e[d + 3], a3);
-          }
-          z += ((a0 + a1) + (a2 + a3)) + dot_row<kLstm>(wh, sH1);
-          sG1[row] = z;
+      for (int k = 0; k < kHalfJobs; ++k) {
+        const int jj = half * kHalfJobs + k;
+        const float4* e4 = reinterpret_cast<const float4*>(sE[jj][i]);
+        const float4* h4 = reinterpret_cast<const float4*>(sH1[jj]);
+        float a0 = bg1, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kEmbed / 4; ++q) {
+          const float4 v = e4[q];
+          a0 = fmaf(wx1[4 * q], v.x, a0); a1 = fmaf(wx1[4 * q + 1], v.y, a1);
+          a2 = fmaf(wx1[4 * q + 2], v.z, a2); a3 = fmaf(wx1[4 * q + 3], v.w, a3);
         }
-      } else if (i >= 1) {
-        sG2[row] = bias + dot_row<kLstm>(wx, sH1) + dot_row<kLstm>(wh, sH2);
+#pragma unroll
+        for (int q = 0; q < kLstm / 4; ++q) {
+          const float4 v = h4[q];
+          a0 = fmaf(wh1[4 * q], v.x, a0); a1 = fmaf(wh1[4 * q + 1], v.y, a1);
+          a2 = fmaf(wh1[4 * q + 2], v.z, a2); a3 = fmaf(wh1[4 * q + 3], v.w, a3);
+        }
+        z[k] = (a0 + a1) + (a2 + a3);
+      }
+#pragma unroll
+      for (int k = 0; k < kHalfJobs; ++k) sG[half * kHalfJobs + k][g] = z[k];
+      __syncthreads();
+      if (i0 + i < sL[cj]) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = cc + u;
+          const float ig = sigmoidf_acc(sG[cj][c]), fg = sigmoidf_acc(sG[cj][kLstm + c]);
+          const float gg = tanh_acc(sG[cj][2 * kLstm + c]), og = sigmoidf_acc(sG[cj][3 * kLstm + c]);
+          c1[u] = fg * c1[u] + ig * gg;
+          sH1[cj][c] = og * tanh_acc(c1[u]);
+        }
       }
       __syncthreads();
-      if (tid < kLstm && i < l) {
-        const float ig = sigmoidf_acc(sG1[tid]), fg = sigmoidf_acc(sG1[kLstm + tid]);
-        const float gg = tanhf(sG1[2 * kLstm + tid]), og = sigmoidf_acc(sG1[3 * kLstm + tid]);
-        c = fg * c + ig * gg;
-        sH1[tid] = og * tanhf(c);
-      } else if (tid >= 4 * kLstm && tid < 5 * kLstm && i >= 1) {
-        const int t = tid - 4 * kLstm;
-        const float ig = sigmoidf_acc(sG2[t]), fg = sigmoidf_acc(sG2[kLstm + t]);
-        const float gg = tanhf(sG2[2 * kLstm + t]), og = sigmoidf_acc(sG2[3 * kLstm + t]);
-        c = fg * c + ig * gg;
-        sH2[t] = og * tanhf(c);
+      // ---- layer 2 gates
+#pragma unroll
+      for (int k = 0; k < kHalfJobs; ++k) {
+        const int jj = half * kHalfJobs + k;
+        const float4* x4 = reinterpret_cast<const float4*>(sH1[jj]);
+        const float4* h4 = reinterpret_cast<const float4*>(sH2[jj]);
+        float a0 = bg2, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kLstm / 4; ++q) {
+          const float4 v = x4[q], w = h4[q];
+          a0 = fmaf(wx2[4 * q], v.x, a0); a1 = fmaf(wx2[4 * q + 1], v.y, a1);
+          a2 = fmaf(wx2[4 * q + 2], v.z, a2); a3 = fmaf(wx2[4 * q + 3], v.w, a3);
+          a0 = fmaf(wh2[4 * q], w.x, a0); a1 = fmaf(wh2[4 * q + 1], w.y, a1);
+          a2 = fmaf(wh2[4 * q + 2], w.z, a2); a3 = fmaf(wh2[4 * q + 3], w.w, a3);
+        }
+        z[k] = (a0 + a1) + (a2 + a3);
+      }
+#pragma unroll
+      for (int k = 0; k < kHalfJobs; ++k) sG[half * kHalfJobs + k][g] = z[k];
+      __syncthreads();
+      if (i0 + i < sL[cj]) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = cc + u;
+          const float ig = sigmoidf_acc(sG[cj][c]), fg = sigmoidf_acc(sG[cj][kLstm + c]);
+          const float gg = tanh_acc(sG[cj][2 * kLstm + c]), og = sigmoidf_acc(sG[cj][3 * kLstm + c]);
+          c2[u] = fg * c2[u] + ig * gg;
+          sH2[cj][c] = og * tanh_acc(c2[u]);
+        }
       }
       __syncthreads();
     }
   }
-  // feature vector x_j
-  if (tid < kLstm) sX[tid] = sH2[tid];
-  if (tid < kNMax) {
-    sX[kLstm + tid] = tid < n ? log2f(p.B_d[(size_t)j * kNMax + tid]) : 0.f;
-    sX[kLstm + kNMax + tid] = tid < n ? log2f(p.B_u[(size_t)j * kNMax + tid]) : 0.f;
-  }
-  if (tid == 0) {
-    sX[kLstm + 2 * kNMax] = static_cast<float>(n) / 16.0f;
-    sX[kLstm + 2 * kNMax + 1] = static_cast<float>(l) / 64.0f;
-  }
-  if (tid < kTypeEmbed) {
-    sX[kLstm + 2 * kNMax + 2 + tid] = P[p.off.E_m + m * kTypeEmbed + tid];
-    sX[kLstm + 2 * kNMax + 2 + kTypeEmbed + tid] = P[p.off.E_arc + arc * kTypeEmbed + tid];
+  // ---- feature vectors x_j (Table 2; R#6-R#8)
+  for (int e = tid; e < nj * kXDim; e += kEncThreads) {
+    const int jj = e / kXDim, i = e % kXDim, j = j0 + jj, n = sN[jj];
+    float v;
+    if (i < kLstm) v = sH2[jj][i];
+    else if (i < kLstm + kNMax) v = (i - kLstm) < n ? log2f(p.B_d[(size_t)j * kNMax + i - kLstm]) : 0.f;
+    else if (i < kLstm + 2 * kNMax) v = (i - kLstm - kNMax) < n ? log2f(p.B_u[(size_t)j * kNMax + i - kLstm - kNMax]) : 0.f;
+    else if (i == kLstm + 2 * kNMax) v = static_cast<float>(n) / 16.0f;
+    else if (i == kLstm + 2 * kNMax + 1) v = static_cast<float>(sL[jj]) / 64.0f;
+    else if (i < kLstm + 2 * kNMax + 2 + kTypeEmbed) v = P[p.off.E_m + p.m[j] * kTypeEmbed + (i - kLstm - 2 * kNMax - 2)];
+    else v = P[p.off.E_arc + p.arc[j] * kTypeEmbed + (i - kLstm - 2 * kNMax - 2 - kTypeEmbed)];
+    sX[jj][i] = v;
   }
   __syncthreads();
   if (p.x_out)
-    for (int i = tid; i < kXDim; i += kEncThreads) p.x_out[(size_t)j * kXDim + i] = sX[i];
-  if (tid == 0) {
+    for (int e = tid; e < nj * kXDim; e += kEncThreads)
+      p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
+  if (tid < nj) {
+    const int j = j0 + tid, n = sN[tid];
     if (p.beta_out) {
       float acc = 0.f;
       for (int w = 0; w < n; ++w) acc += P[p.off.b_o + w];
@@ -208,7 +248,7 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
 // K1 = K1a (+ K1b when the projections are requested; they need x, so x_out must be set).
 cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s) {
   if (p.J <= 0) return cudaSuccess;
-  encode_kernel<<<p.J, kEncThreads, 0, s>>>(p);
+  encode_kernel<<<(p.J + kEncJobs - 1) / kEncJobs, kEncThreads, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !p.a_out) return e;
   project_kernel<<<(p.J + kProjJobs - 1) / kProjJobs, kProjThreads, 0, s>>>(p);

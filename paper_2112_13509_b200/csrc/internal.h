@@ -95,6 +95,7 @@ cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int
 __host__ __device__ size_t packed_weight_elems(int H, int L);
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
 size_t adapt_ws_floats(int B, int H, int L);
+constexpr int kAdaptSplitK = 4;   // must match adapt.cu kSplitK (gradient partial buffers)
 cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
