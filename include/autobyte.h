@@ -186,6 +186,20 @@ autobyte_status autobyte_adapt(autobyte_ctx* ctx, const autobyte_job_stats* samp
                                const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,
                                float lr, int32_t steps, float* loss_before);
 
+/* Optimization Trigger, per job j, DEVICE pointers, [J] each:
+ *   1. drift first: v_observed[j] > 0 and |cur_score - v_observed| / v_observed > drift
+ *      -> action 2 (adapt, then decide again)
+ *   2. gain: best_idx != cur_idx, best_idx >= 0 and
+ *      best_score - cur_score > gain * |cur_score|                  -> action 1 (reconfigure)
+ *   3. otherwise                                                      -> action 0 (keep)
+ * Gain is predicted-vs-predicted (both scores from one autobyte_argmax call). v_observed (the
+ * measured mean speed of the current configuration over the last 10-iteration group)
+ * may be NULL (no drift check). NaN inputs never trigger an action. Paper defaults: gain = 0.05,
+ * drift = 0.10. */
+autobyte_status autobyte_trigger(autobyte_ctx* ctx, int32_t J, const int32_t* best_idx, const float* best_score,
+                                 const int32_t* cur_idx, const float* cur_score, const float* v_observed,
+                                 float gain, float drift, int32_t* action);
+
 /* ---- end-to-end entry points (HOST pointers; copies inside; synchronising) ---------- */
 /* Same contracts as above with every array pointer in HOST memory. The library stages the
  * inputs into its own device workspace with cudaMemcpyAsync, runs the device path, copies

@@ -18,3 +18,4 @@ from .metanet import (  # noqa: F401
     speed, score_matrix, score_pairs, argmax_rows, loss_norm, adapt, head_loss_and_grad,
     HEAD_PARAMS,
 )
+from .trigger import trigger_decide, KEEP, RECONFIGURE, ADAPT  # noqa: F401,E402

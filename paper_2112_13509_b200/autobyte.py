@@ -63,7 +63,8 @@ class Profile(ctypes.Structure):
 EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_desc", "autobyte_blob_bytes",
            "autobyte_validate_blob", "autobyte_create", "autobyte_destroy", "autobyte_last_error",
            "autobyte_synchronize", "autobyte_get_unique_id", "autobyte_attach_comm", "autobyte_encode",
-           "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_argmax_host", "autobyte_adapt_host",
+           "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
+           "autobyte_adapt_host",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile"]
 
 _lib = None
@@ -96,6 +97,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_score": (I32, [P, P, P, P]),
         "autobyte_argmax": (I32, [P, P, P, P, P, P, P]),
         "autobyte_adapt": (I32, [P, P, P, P, P, F32, I32, P]),
+        "autobyte_trigger": (I32, [P, I32, P, P, P, P, P, F32, F32, P]),
         "autobyte_argmax_host": (I32, [P, P, P, P, P, P, P]),
         "autobyte_adapt_host": (I32, [P, P, P, P, P, F32, I32, P]),
         "autobyte_get_weights": (I32, [P, P, SZ]),
@@ -305,6 +307,18 @@ class AutoByte:
                                             V_bar.data_ptr(), float(lr), int(steps),
                                             loss.data_ptr() if loss is not None else None), "adapt")
         return loss
+
+    def trigger(self, best_idx, best_score, cur_idx, cur_score, v_observed=None, gain: float = 0.05,
+                drift: float = 0.10):
+        """Per-job Optimization Trigger action: 0 keep, 1 reconfigure, 2 adapt (device tensors)."""
+        import torch
+        J = int(best_idx.shape[0])
+        action = torch.empty(J, dtype=torch.int32, device=self.torch_device)
+        self._check(self.lib.autobyte_trigger(self.ctx, J, best_idx.data_ptr(), best_score.data_ptr(),
+                                              cur_idx.data_ptr(), cur_score.data_ptr(),
+                                              v_observed.data_ptr() if v_observed is not None else None,
+                                              float(gain), float(drift), action.data_ptr()), "trigger")
+        return action
 
     # ---------------------------------------------------------------- host (end-to-end) API
     def argmax_host(self, jobs, grid, cur_idx=None, begin: int = 0, end: Optional[int] = None, out=None):

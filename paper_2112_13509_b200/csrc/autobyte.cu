@@ -63,7 +63,8 @@ struct autobyte_ctx {
   autobyte_precision precision = AB_PREC_BF16;
   int device = 0;
   int num_sms = 148;
-  int cta_group = 2;             // K2 variant: CTA pairs (default) or single CTAs (AUTOBYTE_CTA_GROUP=1)
+  int cta_group = 2;             // K2 variant: CTA pairs or single CTAs (AUTOBYTE_CTA_GROUP=1|2)
+  int planes = 1;                // 2 for the fp32-accuracy path (bf16 hi + lo weight planes)
   CUtensorMap wmap{};            // tensor map over wpack for the CTA-pair TMA
   cudaStream_t stream = nullptr;
   bool check = false;
@@ -209,7 +210,8 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.u = c->u.ptr;
   sp.wpack = c->wpack.ptr;
   sp.wmap = c->wmap;
-  sp.cta_group = c->cta_group;
+  sp.cta_group = c->planes == 2 ? 1 : c->cta_group;
+  sp.precision3 = c->planes == 2 ? 1 : 0;
   sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
   sp.cur_idx = cur_idx; sp.scores = scores;
   AB_CUDA(c, timed(c, K_SCORE, [&] { return launch_score(sp, c->num_sms, c->stream); }));
@@ -293,7 +295,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   if (s != AB_OK) return s;
   s = autobyte_validate_blob(desc, blob, blob_bytes);
   if (s != AB_OK) return s;
-  if (precision != AB_PREC_BF16) return AB_E_UNSUPPORTED;
+  if (precision != AB_PREC_BF16 && precision != AB_PREC_FP32) return AB_E_INVALID;
+  if (precision == AB_PREC_FP32 && desc->hidden_width > 256) return AB_E_UNSUPPORTED;   // hi+lo activations exceed smem
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -327,7 +330,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   if ((e = cudaMemcpyAsync(c->params.ptr, static_cast<const uint8_t*>(blob) + kBlobHeader,
                            c->off.total * sizeof(float), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
     return bail(e, "copy blob");
-  const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers);
+  c->planes = precision == AB_PREC_FP32 ? 2 : 1;
+  const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers, c->planes);
   if ((e = c->wpack.ensure(wp ? wp : 1)) != cudaSuccess) return bail(e, "alloc wpack");
   if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
   // K2 variant: CTA pairs win when the head is deep and wide (4x512: 1158 vs 1133 TFLOP/s),
@@ -342,7 +346,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   if ((e = cudaMemsetAsync(c->barrier.ptr, 0, 2 * sizeof(unsigned int), c->stream)) != cudaSuccess)
     return bail(e, "memset barrier");
   if ((e = timed(c, K_PACK, [&] {
-         return launch_pack(c->params.ptr, c->off, desc->hidden_width, desc->hidden_layers, c->wpack.ptr, c->stream);
+         return launch_pack(c->params.ptr, c->off, desc->hidden_width, desc->hidden_layers, c->planes, c->wpack.ptr,
+                            c->stream);
        })) != cudaSuccess)
     return bail(e, "pack weights");
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return bail(e, "synchronize");
@@ -487,8 +492,24 @@ autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* sample
   AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
   if (steps > 0)
     AB_CUDA(c, timed(c, K_PACK, [&] {
-              return launch_pack(c->params.ptr, c->off, H, L, c->wpack.ptr, c->stream);
+              return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
             }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_trigger(autobyte_ctx* c, int32_t J, const int32_t* best_idx, const float* best_score,
+                                 const int32_t* cur_idx, const float* cur_score, const float* v_observed,
+                                 float gain, float drift, int32_t* action) {
+  if (!c) return AB_E_INVALID;
+  if (J < 1) return fail(c, AB_E_SHAPE, "J must be >= 1");
+  if (!best_idx || !best_score || !cur_idx || !cur_score || !action)
+    return fail(c, AB_E_INVALID, "trigger array pointer is NULL");
+  if (!(gain >= 0.f) || !(drift >= 0.f)) return fail(c, AB_E_INVALID, "thresholds must be >= 0");
+  DeviceGuard guard(c->device);
+  AB_CUDA(c, timed(c, K_OTHER, [&] {
+            return launch_trigger(J, best_idx, best_score, cur_idx, cur_score, v_observed, gain, drift, action,
+                                  c->stream);
+          }));
   return AB_OK;
 }
 

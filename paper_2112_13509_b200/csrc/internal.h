@@ -50,6 +50,7 @@ struct EncodeParams {
 struct alignas(64) ScoreParams {
   CUtensorMap wmap;             // 2-D view of wpack (rows of 128 B) for the CTA-pair TMA loads
   int cta_group;                // 1: one CTA per tile (M = 128); 2: CTA pairs (M = 256)
+  int precision3;               // 1: fp32-accuracy path (bf16 hi/lo split, 3 products per K step)
   int J, H, G;                  // G = L - 1 tensor-core layers
   int P, Q;
   long long c_begin, c_end;     // shard [begin, end)
@@ -88,18 +89,20 @@ struct AdaptParams {
 cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s);
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s);
+cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_score, const int32_t* cur_idx,
+                           const float* cur_score, const float* v_obs, float gain, float drift, int32_t* action,
+                           cudaStream_t s);
 cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigned long long* cur_keys,
                             int32_t* best_idx, float* best_score, float* cur_score, cudaStream_t s);
-cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, __nv_bfloat16* wpack,
-                        cudaStream_t s);
-__host__ __device__ size_t packed_weight_elems(int H, int L);
+cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
+                        __nv_bfloat16* wpack, cudaStream_t s);
+__host__ __device__ size_t packed_weight_elems(int H, int L, int planes);
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
 size_t adapt_ws_floats(int B, int H, int L);
 constexpr int kAdaptSplitK = 4;   // must match adapt.cu kSplitK (gradient partial buffers)
 cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
-size_t score_smem_bytes(int H, int cta_group);
 bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L);
 
 }  // namespace ab

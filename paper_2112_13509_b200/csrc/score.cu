@@ -58,21 +58,28 @@ __device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3
 #define AB_ACC(st, i, v)
 #endif
 
-template <int H, int CG>
+// P3 = 1 is the fp32-accuracy path (AB_PREC_FP32): every operand x is split into bf16 hi = rn(x) and
+// lo = rn(x - hi), and each product is hi*hi + hi*lo + lo*hi (the lo*lo term, ~2^-16 relative, is
+// dropped), so activations and weights take twice the storage and three MMAs per K step.
+template <int H, int CG, int P3 = 0>
 struct ScoreCfg {
-  static constexpr int NCH = H >= 128 ? 128 : H;  // N of one MMA / one TMEM accumulator chunk
+  static constexpr int NCH = P3 ? 64 : (H >= 128 ? 128 : H);  // N of one MMA / one TMEM accumulator chunk
+  static constexpr int NP = P3 ? 2 : 1;           // operand planes (hi, lo)
   static constexpr int NQ = H / NCH;              // chunks per layer
   static constexpr int NKB = H / 64;              // 64-element K blocks per layer
   static constexpr int KB_PER_Q = NCH / 64;       // K blocks of the next layer produced by one chunk
-  static constexpr int STAGE_BYTES = NCH * 128;   // one (chunk, K block) weight tile
+  static constexpr int TILE_BYTES = NCH * 128;    // one (chunk, K block) weight tile of one plane
+  static constexpr int STAGE_BYTES = TILE_BYTES * NP;   // ... of all planes
   static constexpr int KBS = (CG == 2 && NKB >= 2) ? AB_KBS : 1;  // K blocks per pipeline stage
   static constexpr int ATOM_BYTES = STAGE_BYTES / CG;        // this CTA's part of one K block (N-half for CG=2)
   static constexpr int CTA_STAGE_BYTES = ATOM_BYTES * KBS;   // this CTA's bytes per stage
   static constexpr int STAGE_TX = STAGE_BYTES * KBS;         // bytes per stage over the pair
-  static constexpr int A_BYTES = kTileM * H * 2;  // bf16 activation tile, buffer X
+  static constexpr int A_PLANE = kTileM * H * 2;  // bf16 activation tile (one plane), buffer X
+  static constexpr int A_BYTES = A_PLANE * NP;
   static constexpr int NSPLIT = 4;                // epilogue warps per TMEM lane quadrant
   static constexpr int QC = NCH / NSPLIT;         // columns per epilogue warp per chunk
   static constexpr int G_CAP = H == 512 ? 3 : 7;  // hidden-layer biases kept in shared memory
+  static constexpr uint32_t Y_LO = H / 2;         // TMEM column offset of the lo plane of buffer Y
   static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
   static constexpr int WV = H + 4;                // w_j | beta_j, 0, 0, 0 (one tile slot)
   static constexpr int WHAT_BYTES = 2 * WV * 4;   // two tile slots
@@ -140,6 +147,16 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
           } else {
             if (TS) umma_ts(d_t, at, bd + 2 * kk, C::IDESC, acc);
             else umma_ss(d_t, ad, bd + 2 * kk, C::IDESC, acc);
+            if (C::NP == 2) {   // + A_hi * W_lo + A_lo * W_hi
+              const uint64_t bl = bd + 2 * kk + (C::TILE_BYTES >> 4);
+              if (TS) {
+                umma_ts(d_t, at, bl, C::IDESC, 1u);
+                umma_ts(d_t, at + C::Y_LO, bd + 2 * kk, C::IDESC, 1u);
+              } else {
+                umma_ss(d_t, ad, bl, C::IDESC, 1u);
+                umma_ss(d_t, ad + (C::A_PLANE >> 4), bd + 2 * kk, C::IDESC, 1u);
+              }
+            }
           }
         }
       }
@@ -156,9 +173,9 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
 // (its A rows, its TMEM accumulators, its epilogue) and half of every weight stage (64 of the 128
 // output rows), and the leader issues M = 256 tcgen05.mma.cta_group::2 for both. Weight bytes
 // streamed from L2 per candidate are halved.
-template <int H, int CG>
+template <int H, int CG, int P3>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
-  using C = ScoreCfg<H, CG>;
+  using C = ScoreCfg<H, CG, P3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -241,8 +258,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
                                      (ti + a) * C::NCH + static_cast<int>(rank) * (C::NCH / 2), &full[s], pol);
                 } else {
                   mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-                  bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)ti * (C::NCH * 64), C::STAGE_BYTES,
-                           &full[s], pol);
+                  bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)ti * (C::NCH * 64 * C::NP),
+                           C::STAGE_BYTES, &full[s], pol);
                 }
               }
               __syncwarp();
@@ -343,15 +360,30 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       uc = uu.y;
     };
     // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
-    auto store_cols = [&](int dst, int c0, const uint32_t (&pk)[C::QC / 2]) {
+    auto store_plane = [&](int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
       if (dst == 0) {  // buffer X: SW128 K-major, 16-byte chunk j of row r stored at chunk j ^ (r % 8)
-        const uint32_t rowbase = smem_u32(sA) + (c0 >> 6) * 16384 + row * 128;
+        const uint32_t rowbase = smem_u32(sA) + plane * C::A_PLANE + (c0 >> 6) * 16384 + row * 128;
         const int j0 = (c0 & 63) >> 3;
 #pragma unroll
         for (int u = 0; u < C::QC / 8; ++u)
           st_shared_v4(rowbase + (((j0 + u) ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       } else {         // buffer Y: TMEM, column = element pair index
-        tmem_st_cols<C::QC / 2>(lane_base + C::Y_COL + (c0 >> 1), pk);
+        tmem_st_cols<C::QC / 2>(lane_base + C::Y_COL + plane * C::Y_LO + (c0 >> 1), pk);
+      }
+    };
+    // QC post-activation values v (fp32) of this thread's row -> the A operand of the next layer:
+    // bf16 (P3 = 0, values already ReLU'd) or hi/lo bf16 planes (P3 = 1)
+    auto store_vals = [&](int dst, int c0, const float (&v)[C::QC]) {
+      uint32_t hi[C::QC / 2];
+#pragma unroll
+      for (int i = 0; i < C::QC / 2; ++i) hi[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+      store_plane(dst, c0, hi, 0);
+      if (C::NP == 2) {
+        uint32_t lo[C::QC / 2];
+#pragma unroll
+        for (int i = 0; i < C::QC / 2; ++i)
+          lo[i] = pack_bf16x2(v[2 * i] - __uint_as_float(hi[i] << 16), v[2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
+        store_plane(dst, c0, lo, 1);
       }
     };
     // make this warp's part of A-chunk q visible to the tensor core and count the warp in
@@ -364,16 +396,31 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     // layer-1 activations h1 = ReLU(a_j + W1c u_c) for the 128-column piece q (this warp's columns)
     auto build_piece = [&](int q, float up, float uc, int dst) {
       const int c0 = q * C::NCH + grp * C::QC;
-      uint32_t pk[C::QC / 2];
+      if (C::NP == 1) {
+        uint32_t pk[C::QC / 2];
 #pragma unroll
-      for (int i = 0; i < C::QC / 4; ++i) {
-        const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
-        const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
-        const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-        pk[2 * i] = pack_relu_bf16x2(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)), fmaf(v4.y, uc, fmaf(u4.y, up, a4.y)));
-        pk[2 * i + 1] = pack_relu_bf16x2(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)), fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
+        for (int i = 0; i < C::QC / 4; ++i) {
+          const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+          const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
+          const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+          pk[2 * i] = pack_relu_bf16x2(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)), fmaf(v4.y, uc, fmaf(u4.y, up, a4.y)));
+          pk[2 * i + 1] = pack_relu_bf16x2(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)), fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
+        }
+        store_plane(dst, c0, pk, 0);
+      } else {
+        float v[C::QC];
+#pragma unroll
+        for (int i = 0; i < C::QC / 4; ++i) {
+          const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+          const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
+          const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
+          v[4 * i] = relu(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)));
+          v[4 * i + 1] = relu(fmaf(v4.y, uc, fmaf(u4.y, up, a4.y)));
+          v[4 * i + 2] = relu(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)));
+          v[4 * i + 3] = relu(fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
+        }
+        store_vals(dst, c0, v);
       }
-      store_cols(dst, c0, pk);
       publish(dst, q);
     };
 
@@ -447,7 +494,18 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           {
             const int n0 = q * C::NCH + grp * C::QC;
             const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
-            if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
+            if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
+              float v[C::QC];
+#pragma unroll
+              for (int i = 0; i < C::QC / 4; ++i) {
+                const float4 bb = b4[i];
+                v[4 * i] = relu(__uint_as_float(acc[4 * i]) + bb.x);
+                v[4 * i + 1] = relu(__uint_as_float(acc[4 * i + 1]) + bb.y);
+                v[4 * i + 2] = relu(__uint_as_float(acc[4 * i + 2]) + bb.z);
+                v[4 * i + 3] = relu(__uint_as_float(acc[4 * i + 3]) + bb.w);
+              }
+              store_vals(dst, n0, v);
+            } else if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
               uint32_t pk[C::QC / 2];
 #pragma unroll
               for (int i = 0; i < C::QC / 4; ++i) {
@@ -456,7 +514,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
                 pk[2 * i + 1] =
                     pack_relu_bf16x2(__uint_as_float(acc[4 * i + 2]) + bb.z, __uint_as_float(acc[4 * i + 3]) + bb.w);
               }
-              store_cols(dst, n0, pk);
+              store_plane(dst, n0, pk, 0);
             } else {       // last hidden layer stays fp32: dot with the folded output row w_j (R#16)
               const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * C::WV + n0);
 #pragma unroll
@@ -540,12 +598,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   }
 }
 
-template <int H, int CG>
+template <int H, int CG, int P3>
 static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
-  using C = ScoreCfg<H, CG>;
+  using C = ScoreCfg<H, CG, P3>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<H, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<H, CG, P3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -565,23 +623,18 @@ static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG>, p);
+  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG, P3>, p);
 }
 
 template <int H>
 static cudaError_t launch_score_h(const ScoreParams& p, int num_sms, cudaStream_t s) {
-  if (p.cta_group == 2) return launch_score_hc<H, 2>(p, num_sms, s);
-  return launch_score_hc<H, 1>(p, num_sms, s);
-}
-
-size_t score_smem_bytes(int H, int cg) {
-  switch (H) {
-    case 64: return cg == 2 ? ScoreCfg<64, 2>::SMEM : ScoreCfg<64, 1>::SMEM;
-    case 128: return cg == 2 ? ScoreCfg<128, 2>::SMEM : ScoreCfg<128, 1>::SMEM;
-    case 256: return cg == 2 ? ScoreCfg<256, 2>::SMEM : ScoreCfg<256, 1>::SMEM;
-    case 512: return cg == 2 ? ScoreCfg<512, 2>::SMEM : ScoreCfg<512, 1>::SMEM;
+  if constexpr (H <= 256) {
+    if (p.precision3) return launch_score_hc<H, 1, 1>(p, num_sms, s);
+  } else {
+    if (p.precision3) return cudaErrorNotSupported;
   }
-  return 0;
+  if (p.cta_group == 2) return launch_score_hc<H, 2, 0>(p, num_sms, s);
+  return launch_score_hc<H, 1, 0>(p, num_sms, s);
 }
 
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s) {
@@ -620,36 +673,69 @@ cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigne
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- Optimization Trigger (NEXT 1)
+// P:435 (5% gain hysteresis) and P:438 (10% drift -> online adaptation), drift checked first.
+__global__ void trigger_kernel(int J, const int32_t* __restrict__ best_idx, const float* __restrict__ best_score,
+                               const int32_t* __restrict__ cur_idx, const float* __restrict__ cur_score,
+                               const float* __restrict__ v_obs, float gain, float drift, int32_t* action) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  const float sc = cur_score[j], sb = best_score[j];
+  const int b = best_idx[j], c = cur_idx[j];
+  int a = 0;
+  if (v_obs) {
+    const float v = v_obs[j];
+    if (v > 0.f && fabsf(sc - v) / v > drift) a = 2;
+  }
+  if (a == 0 && b >= 0 && b != c && sb - sc > gain * fabsf(sc)) a = 1;   // NaN compares false
+  action[j] = a;
+}
+
+cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_score, const int32_t* cur_idx,
+                           const float* cur_score, const float* v_obs, float gain, float drift, int32_t* action,
+                           cudaStream_t s) {
+  trigger_kernel<<<(J + 255) / 256, 256, 0, s>>>(J, best_idx, best_score, cur_idx, cur_score, v_obs, gain, drift,
+                                                 action);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- weight packing (bf16 shadows)
 // wpack layout: for GEMM layer g (W_{g+2}), chunk q of NCH output rows, K block b of 64 inputs:
-// a contiguous NCH x 128-byte tile in UMMA SW128 K-major order (row n at n*128 bytes, 16-byte
-// chunk j stored at chunk j ^ (n % 8)) — exactly what one cp.async.bulk drops into a stage.
-__host__ __device__ size_t packed_weight_elems(int H, int L) { return (size_t)(L > 1 ? L - 1 : 0) * H * H; }
+// NP contiguous NCH x 128-byte tiles (hi, then lo for the fp32 path) in UMMA SW128 K-major order
+// (row n at n*128 bytes, 16-byte chunk j stored at chunk j ^ (n % 8)) — exactly what one
+// cp.async.bulk drops into a pipeline stage.
+__host__ __device__ size_t packed_weight_elems(int H, int L, int planes) {
+  return (size_t)(L > 1 ? L - 1 : 0) * H * H * planes;
+}
 
-__global__ void pack_kernel(const float* __restrict__ params, ParamOffsets off, int H, int L,
+__global__ void pack_kernel(const float* __restrict__ params, ParamOffsets off, int H, int L, int planes,
                             __nv_bfloat16* __restrict__ wpack) {
-  const int NCH = H >= 128 ? 128 : H, NQ = H / NCH, NKB = H / 64;
-  const size_t total = packed_weight_elems(H, L);
+  const int NCH = planes == 2 ? 64 : (H >= 128 ? 128 : H), NQ = H / NCH, NKB = H / 64;
+  const size_t total = packed_weight_elems(H, L, planes);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const size_t tile_elems = (size_t)NCH * 64;
-    const size_t tile = e / tile_elems;
+    const size_t tile = e / tile_elems;                        // (g, q, b, plane)
+    const int plane = static_cast<int>(tile % planes);
+    const size_t tq = tile / planes;
     const int within = static_cast<int>(e % tile_elems);
     const int nl = within / 64, slot = within % 64;         // slot = position inside the 128-byte row
     const int kl = (((slot >> 3) ^ (nl & 7)) << 3) | (slot & 7);   // logical k of that position
-    const int b = static_cast<int>(tile % NKB);
-    const int q = static_cast<int>((tile / NKB) % NQ);
-    const int g = static_cast<int>(tile / ((size_t)NKB * NQ));
+    const int b = static_cast<int>(tq % NKB);
+    const int q = static_cast<int>((tq / NKB) % NQ);
+    const int g = static_cast<int>(tq / ((size_t)NKB * NQ));
     const int n = q * NCH + nl, k = b * 64 + kl;
-    wpack[e] = __float2bfloat16_rn(params[off.W[g + 2] + (size_t)n * H + k]);
+    const float w = params[off.W[g + 2] + (size_t)n * H + k];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    wpack[e] = plane == 0 ? hi : __float2bfloat16_rn(w - __bfloat162float(hi));
   }
 }
 
-cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, __nv_bfloat16* wpack,
-                        cudaStream_t s) {
-  const size_t total = packed_weight_elems(H, L);
+cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
+                        __nv_bfloat16* wpack, cudaStream_t s) {
+  const size_t total = packed_weight_elems(H, L, planes);
   if (total == 0) return cudaSuccess;
   const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-  pack_kernel<<<blocks, 256, 0, s>>>(params, off, H, L, wpack);
+  pack_kernel<<<blocks, 256, 0, s>>>(params, off, H, L, planes, wpack);
   return cudaGetLastError();
 }
 
@@ -689,7 +775,7 @@ bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const int NCH = H >= 128 ? 128 : H;
-  const size_t rows = packed_weight_elems(H, L) / 64;
+  const size_t rows = packed_weight_elems(H, L, 1) / 64;
   if (rows == 0) { std::memset(map, 0, sizeof(*map)); return true; }
   cuuint64_t dims[2] = {64, rows};
   cuuint64_t strides[1] = {128};

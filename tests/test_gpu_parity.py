@@ -353,3 +353,62 @@ def test_host_entry_point_matches_device():
     sample = [0, 127, 128, 255]
     s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample)
     check_argmax(bi_h[sample], s_ora, RTOL)
+
+
+# ------------------------------------------------------------------------------------- fp32 path
+def make_fp32(L, H, W):
+    from paper_2112_13509_b200.autobyte import AutoByte
+    return AutoByte(L, H, W, device=0, precision="fp32")
+
+
+RTOL32 = 1e-4
+
+
+@pytest.mark.parametrize("L,H,P,Q", [(1, 64, 7, 9), (2, 64, 8, 8), (2, 128, 7, 13), (3, 128, 5, 31), (3, 256, 31, 9),
+                                     (4, 256, 16, 16)])
+def test_fp32_path_scores_and_argmax(L, H, P, Q):
+    W = synth.make_weights(synth.NetDesc(L, H), seed=L * 31 + H)
+    jobs = synth.small_fleet(5, L + H)
+    grid = synth.log_grid(P, Q)
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    net = make_fp32(L, H, W)
+    s = gpu_scores(net, jobs, grid)
+    err = check_scores(s, s_ora, RTOL32)
+    bi, bs, _ = gpu_argmax(net, jobs, grid)
+    nt = check_argmax(bi, s_ora, RTOL32)
+    assert np.array_equal(bs, s[np.arange(5), bi])
+    print(f"fp32 L={L} H={H}: max err {err.max():.2e}, non-tied jobs {nt}/5")
+
+
+def test_fp32_path_c3_sampled_and_exact_dyadic():
+    c = synth.config("C3")
+    W = synth.make_weights(c.desc)
+    net = make_fp32(c.desc.hidden_layers, c.desc.hidden_width, W)
+    sample = [0, 100, 200, 255]
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample)
+    s = gpu_scores(net, c.jobs.subset(sample), c.grid)
+    check_scores(s, s_ora, RTOL32)
+    bi, _, _ = gpu_argmax(net, c.jobs.subset(sample), c.grid)
+    check_argmax(bi, s_ora, RTOL32)
+    Wd, jobs, grid, _ = dyadic_net(3, 256, seed=3 * 1000 + 256)
+    s_d = gpu_scores(make_fp32(3, 256, Wd), jobs, grid).astype(np.float64)
+    assert np.array_equal(s_d[0], oracle.score_matrix(Wd, jobs, grid)[0])
+
+
+def test_fp32_path_rejects_h512():
+    from paper_2112_13509_b200.autobyte import AutoByteError
+    W = synth.make_weights(synth.NetDesc(2, 512))
+    with pytest.raises(AutoByteError):
+        make_fp32(2, 512, W)
+
+
+def test_fp32_path_after_adapt():
+    L, H = 3, 128
+    W = synth.make_weights(synth.NetDesc(L, H))
+    batch = synth.make_adapt_batch(synth.small_fleet(32, 4), synth.log_grid(8, 8), 6)
+    W_ora, _ = oracle.adapt(W, batch, lr=1e-2, steps=2)
+    net = make_fp32(L, H, W)
+    net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=1e-2, steps=2)
+    jobs, grid = synth.small_fleet(3, 9), synth.log_grid(6, 7)
+    # the adapted fp32 masters differ from the oracle's float64 ones by ~1e-7; scores stay within 1e-4
+    check_scores(gpu_scores(net, jobs, grid), oracle.score_matrix(W_ora, jobs, grid), RTOL32)

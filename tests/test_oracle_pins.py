@@ -283,3 +283,16 @@ def test_adapt_descends():
     Wn, before = oracle.adapt(W, batch, lr=1e-3, steps=1)
     _, after = oracle.adapt(Wn, batch, lr=0.0, steps=1)
     assert after < before
+
+
+# ---------------------------------------------------------------- Optimization Trigger (NEXT 1)
+def test_trigger_spec_examples():
+    """SPEC controller examples (S:371-373): gain 4% / drift 2% -> keep; gain 12% -> reconfigure;
+    drift 15% -> adapt regardless of gain; drift is checked first."""
+    T = oracle.trigger_decide
+    assert T([5], [1.04], [3], [1.0], [1.02]) == [oracle.KEEP]
+    assert T([5], [1.12], [3], [1.0], [1.02]) == [oracle.RECONFIGURE]
+    assert T([5], [1.12], [3], [1.0], [1.0 / 1.15]) == [oracle.ADAPT]
+    assert T([5], [2.0], [3], [1.0], None) == [oracle.RECONFIGURE]        # no observation: gain only
+    assert T([3], [2.0], [3], [1.0], None) == [oracle.KEEP]               # best is current
+    assert T([-1], [float("nan")], [3], [1.0], None) == [oracle.KEEP]     # all-NaN job
