@@ -36,9 +36,21 @@ struct Gemm {
   __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
 };
 
+constexpr int kStages = 3;   // cp.async pipeline depth of the SIMT GEMM tiles
+
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One 64 x 64 output tile (or one K-slice of it for split-K). Each thread owns 4 x 4 outputs;
-// the next 16-wide K slice is fetched into registers while the current one is multiplied.
-__device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (*Bs)[kTN + 4]) {
+// 16-wide K slices of both operands stream through a 3-stage cp.async ring (zero-filled at the
+// edges), so global-load latency overlaps the FMAs of the two slices ahead.
+__device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTK][kTM + 4], float (*Bs)[kTK][kTN + 4]) {
   const int tiles_n = (g.N + kTN - 1) / kTN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
   const int split = g.ksplit > 1 ? work / tiles_mn : 0;
@@ -51,7 +63,6 @@ __device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (
     kend = min(g.K, kbeg + chunk);
   }
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  // per-thread staging coordinates (coalesced along each operand's contiguous dimension)
   int aml[4], akl[4], bnl[4], bkl[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -59,28 +70,35 @@ __device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (
     if (g.lak == 1) { akl[r] = e % kTK; aml[r] = e / kTK; } else { aml[r] = e % kTM; akl[r] = e / kTM; }
     if (g.lbk == 1) { bkl[r] = e % kTK; bnl[r] = e / kTK; } else { bnl[r] = e % kTN; bkl[r] = e / kTN; }
   }
-  float ra[4], rb[4];
-  auto fetch = [&](int k0) {
+  const int nk = kend > kbeg ? (kend - kbeg + kTK - 1) / kTK : 0;
+  auto issue = [&](int it) {
+    if (it < nk) {
+      const int k0 = kbeg + it * kTK, st = it % kStages;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int m = m0 + aml[r], k = k0 + akl[r];
-      ra[r] = (m < g.M && k < kend) ? g.A[m * g.lam + k * g.lak] : 0.f;
-      const int n = n0 + bnl[r], kk = k0 + bkl[r];
-      rb[r] = (n < g.N && kk < kend) ? g.Bm[kk * g.lbk + n * g.lbn] : 0.f;
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + aml[r], k = k0 + akl[r];
+        const bool va = m < g.M && k < kend;
+        cp_async4(&As[st][akl[r]][aml[r]], va ? g.A + (m * g.lam + k * g.lak) : g.A, va);
+        const int n = n0 + bnl[r], kk = k0 + bkl[r];
+        const bool vb = n < g.N && kk < kend;
+        cp_async4(&Bs[st][bkl[r]][bnl[r]], vb ? g.Bm + (kk * g.lbk + n * g.lbn) : g.Bm, vb);
+      }
     }
+    cp_async_commit();   // (empty groups keep the wait arithmetic uniform)
   };
   float acc[4][4] = {};
-  if (kbeg < kend) fetch(kbeg);
-  for (int k0 = kbeg; k0 < kend; k0 += kTK) {
+  __syncthreads();       // the ring may still be read by the previous tile
+  issue(0);
+  issue(1);
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<kStages - 2>();
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 4; ++r) { As[akl[r]][aml[r]] = ra[r]; Bs[bkl[r]][bnl[r]] = rb[r]; }
-    __syncthreads();
-    if (k0 + kTK < kend) fetch(k0 + kTK);
+    issue(it + 2);       // overwrites the stage read two slices ago (all threads are past it)
+    const int st = it % kStages;
 #pragma unroll
     for (int kk = 0; kk < kTK; ++kk) {
-      const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 a = *reinterpret_cast<const float4*>(&As[st][kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[st][kk][tx * 4]);
       const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -88,6 +106,7 @@ __device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (
         for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(av[i], bv[jj], acc[i][jj]);
     }
   }
+  cp_async_wait<0>();
   float* C = g.C + (g.ksplit > 1 ? split * g.cpart : 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -106,7 +125,14 @@ __device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTM + 4], float (
   }
 }
 
+#ifdef AB_STATS
+__device__ unsigned long long g_adapt_phase[64];   // block 0: clock at entry of each grid barrier
+__device__ int g_adapt_nphase;
+#endif
 __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) {
+#ifdef AB_STATS
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_adapt_nphase < 64) g_adapt_phase[g_adapt_nphase++] = clock64();
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -127,18 +153,33 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
   __syncthreads();
 }
 
-// column sums out[n] = scale * sum_b X[b][n] in fixed order; spread over the whole grid
-__device__ void colsum(const float* X, int B, int N, long long ld, float* out, int gtid, int gthreads) {
-  for (int n = gtid; n < N; n += gthreads) {
-    float s = 0.f;
-    for (int b = 0; b < B; ++b) s += X[(long long)b * ld + n];
-    out[n] = s;
+// Column sums over the batch as kSplitK partials (like the split-K weight gradients, summed in fixed
+// order by the SGD sweep): out[s * stride + n] = sum_{b in segment s} X[b][n]. One warp per
+// (32-column group, segment); each lane walks its column down the segment (coalesced rows).
+__device__ void colsum_split(const float* X, int B, int N, long long ld, float* out, long long stride) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int groups = (N + 31) / 32, seg = (B + kSplitK - 1) / kSplitK;
+  for (int w = gwarp; w < groups * kSplitK; w += nwarps) {
+    const int sgi = w / groups, n = (w % groups) * 32 + lane;
+    const int b0 = sgi * seg, b1 = min(B, b0 + seg);
+    if (n >= N) continue;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int b = b0;
+    for (; b + 3 < b1; b += 4) {
+      a0 += X[(long long)b * ld + n];
+      a1 += X[(long long)(b + 1) * ld + n];
+      a2 += X[(long long)(b + 2) * ld + n];
+      a3 += X[(long long)(b + 3) * ld + n];
+    }
+    for (; b < b1; ++b) a0 += X[(long long)b * ld + n];
+    out[sgi * stride + n] = (a0 + a1) + (a2 + a3);
   }
 }
 
 __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_constant__ AdaptParams p) {
-  __shared__ float As[kTK][kTM + 4];
-  __shared__ float Bs[kTK][kTN + 4];
+  __shared__ __align__(16) float As[kStages][kTK][kTM + 4];
+  __shared__ __align__(16) float Bs[kStages][kTK][kTN + 4];
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   unsigned int gen = 0;
@@ -214,7 +255,7 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
         if (t < t1) gemm_tile(gw, t, As, Bs);
         else gemm_tile(gd, t - t1, As, Bs);
       }
-      colsum(R, B, kNMax, kNMax, Gr + p.off.b_o, gtid, gthreads);
+      colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
       grid_sync(p.barrier, gen);
     }
     // ---------------- backward: hidden layers L..1
@@ -236,7 +277,7 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
         if (t < t1) gemm_tile(gw, t, As, Bs);
         else gemm_tile(gd, t - t1, As, Bs);
       }
-      colsum(Dk, B, H, H, Gr + p.off.b[k], gtid, gthreads);
+      colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
       grid_sync(p.barrier, gen);
     }
     // ---------------- SGD on the head parameters (contiguous from W1 to b_o in the blob order)
@@ -268,3 +309,15 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
 }
 
 }  // namespace ab
+
+#ifdef AB_STATS
+extern "C" int ab_debug_adapt_phases(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, ab::g_adapt_nphase, sizeof(int));
+  cudaMemcpyFromSymbol(out, ab::g_adapt_phase, sizeof(unsigned long long) * 64);
+  int z = 0;
+  cudaMemcpyToSymbol(ab::g_adapt_nphase, &z, sizeof(int));
+  return n;
+}
+#endif
