@@ -40,7 +40,8 @@ static __device__ __noinline__ void mbar_wait_slow(uint32_t addr, uint32_t parit
   const long long t0 = clock64();
   while (!mbar_try(addr, parity)) {
     if (clock64() - t0 > (1ll << 36)) {
-      printf("autobyte: mbarrier watchdog (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
+      printf("autobyte: mbarrier watchdog (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x, addr,
+             parity);
       __trap();
     }
   }
