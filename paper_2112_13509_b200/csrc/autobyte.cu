@@ -68,6 +68,7 @@ struct autobyte_ctx {
   CUtensorMap wmap{};            // tensor map over wpack for the CTA-pair TMA
   cudaStream_t stream = nullptr;
   bool check = false;
+  bool shard_encode = true;      // G > 1: K1a on 1/G of the jobs + all-gather of x (AUTOBYTE_SHARD_ENCODE=0 off)
   std::string last_error;
 
   DevBuf<float> params;          // fp32 masters (blob payload order)
@@ -168,7 +169,6 @@ autobyte_status ensure_job_ws(autobyte_ctx* c, int J) {
   const int H = c->desc.hidden_width;
   AB_CUDA(c, c->jobvec.ensure((size_t)J * (2 * H + 4)));
   AB_CUDA(c, c->keys.ensure((size_t)2 * J));
-  AB_CUDA(c, c->x.ensure((size_t)J * kXDim));
   return AB_OK;
 }
 
@@ -181,18 +181,47 @@ EncodeParams encode_params(autobyte_ctx* c, const autobyte_job_stats* j) {
   return p;
 }
 
+// K1a into c->x for all jobs (returns the params K1b continues from). At G > 1 each rank encodes
+// its 1/G slice of the jobs and the x rows are all-gathered in place over NCCL: K1a's per-job
+// arithmetic does not depend on how jobs are grouped, so x (and every key after it) is
+// bit-identical to the single-rank result.
+autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, EncodeParams* out) {
+  const int J = jobs->J;
+  const bool shard = c->shard_encode && c->comm && c->world > 1;
+  const int G = shard ? c->world : 1;
+  const int Jp = (J + G - 1) / G;
+  AB_CUDA(c, c->x.ensure((size_t)Jp * G * kXDim));
+  EncodeParams ep = encode_params(c, jobs);
+  ep.x_out = c->x.ptr;
+  ep.j_begin = shard ? std::min(J, c->rank * Jp) : 0;
+  ep.j_end = shard ? std::min(J, (c->rank + 1) * Jp) : J;
+  if (ep.j_end > ep.j_begin)
+    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
+  if (shard) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
+    ncclResult_t r = ncclAllGather(c->x.ptr + (size_t)c->rank * Jp * kXDim, c->x.ptr, (size_t)Jp * kXDim, ncclFloat,
+                                   c->comm, c->stream);
+    if (c->profiling) { cudaEventRecord(b, c->stream); c->pending.push_back({K_EXCHANGE, {a, b}}); }
+    if (r != ncclSuccess) return fail(c, AB_E_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    c->launches[K_EXCHANGE] += 1;
+  }
+  *out = ep;
+  return AB_OK;
+}
+
 autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                      const int32_t* cur_idx, float* scores) {
   const int J = jobs->J;
   autobyte_status st = ensure_job_ws(c, J);
   if (st != AB_OK) return st;
-  EncodeParams ep = encode_params(c, jobs);
+  EncodeParams ep{};
+  if ((st = run_lstm(c, jobs, &ep)) != AB_OK) return st;
   const int H = c->desc.hidden_width;
   ep.jv = 2 * H + 4;
-  ep.x_out = c->x.ptr; ep.a_out = c->jobvec.ptr; ep.what_out = c->jobvec.ptr + H; ep.beta_out = c->jobvec.ptr + 2 * H;
+  ep.a_out = c->jobvec.ptr; ep.what_out = c->jobvec.ptr + H; ep.beta_out = c->jobvec.ptr + 2 * H;
   ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
-  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
-  c->launches[K_ENCODE] += 1;   // launch_encode issued K1a + K1b (projections)
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_project(ep, c->stream); }));
   // K0: candidate encodings u_c of this shard (§8(a) a-1), 8 bytes per candidate
   AB_CUDA(c, c->u.ensure((size_t)(grid->shard_end - grid->shard_begin)));
   AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_grid(*grid, c->u.ptr, c->stream); }));
@@ -315,6 +344,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   c->stream = static_cast<cudaStream_t>(cuda_stream);
+  const char* se = std::getenv("AUTOBYTE_SHARD_ENCODE");
+  c->shard_encode = !(se && se[0] == '0');
   const char* chk = std::getenv("AUTOBYTE_CHECK");
   c->check = chk && chk[0] == '1';
   auto bail = [&](cudaError_t e, const char* what) {
@@ -423,7 +454,8 @@ autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs,
   if ((s = device_checks(c, jobs, nullptr)) != AB_OK) return s;
   EncodeParams ep = encode_params(c, jobs);
   ep.x_out = x_out;
-  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+  ep.j_begin = 0; ep.j_end = jobs->J;
+  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
   return AB_OK;
 }
 
@@ -477,11 +509,9 @@ autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* sample
   if ((s = device_checks(c, samples, nullptr)) != AB_OK) return s;
   if (steps == 0 && !loss_before) return AB_OK;
   const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
-  AB_CUDA(c, c->x.ensure((size_t)B * kXDim));
   AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
-  EncodeParams ep = encode_params(c, samples);
-  ep.x_out = c->x.ptr;
-  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode(ep, c->stream); }));
+  EncodeParams ep{};
+  if ((s = run_lstm(c, samples, &ep)) != AB_OK) return s;
   AdaptParams ap{};
   ap.B = B; ap.H = H; ap.L = L; ap.steps = steps; ap.lr = lr;
   ap.x = c->x.ptr; ap.S_p = reinterpret_cast<const long long*>(sp_bytes); ap.S_c = sc_mult; ap.v_obs = v_obs;

@@ -1,14 +1,16 @@
 // encode.cu — K1: per-job prologue of the scoring path.
 //
-// K1a, 16 jobs per 256-thread CTA:
+// K1a, 2*HJ jobs per 256-thread CTA (HJ sized so the grid is about one wave):
 //   t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers (R#7, R#8); e_i = W_e t'_i + b_e (R#4)
 //   two-layer LSTM over i = 0..l_j-1, gates i,f,g,o, h0 = c0 = 0 ("two-layer LSTM", R#5);
-//     thread (g, half) owns gate row g of both layers, weights in registers, for 8 jobs
+//     thread (g, half) owns gate row g of both layers, weights in registers, for HJ jobs
 //   x_j = [h | log2 B_d | log2 B_u | n/16 | l/64 | E_m[m] | E_arc[arc]]   (Table 2)
-//   beta_j = (1/n) sum_{w<n} b_o[w], and resets the job's arg-max keys.
-// K1b, 32 jobs per CTA:
+//   K1a takes a job range, so at G > 1 each rank encodes 1/G of the jobs and the x rows are
+//   all-gathered before K1b (autobyte.cu run_encode).
+// K1b, 32 jobs per CTA, all jobs:
 //   a_j = W1[:, :82] x_j + b1     (layer-1 projection of the job half of the concatenation)
 //   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3)
+//   beta_j = (1/n) sum_{w<n} b_o[w], and resets the job's arg-max keys.
 // This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
 #include "internal.h"
 #include "ptx.cuh"
@@ -16,36 +18,58 @@
 namespace ab {
 
 constexpr int kEncThreads = 256;   // 128 LSTM gate rows x 2 job halves
-constexpr int kEncJobs = 16;       // jobs per CTA (8 per half)
-constexpr int kHalfJobs = kEncJobs / 2;
-constexpr int kChunk = 16;         // layers whose embeddings are staged in shared memory at a time
 
 // logistic and tanh from the ex2 unit: |error| ~ 1e-7 absolute, well inside the 1e-4 / 2e-5
 // tolerance the encoder is held to against the float64 oracle (tests/test_gpu_parity.py)
 __device__ __forceinline__ float sigmoidf_acc(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
-__device__ __forceinline__ float tanh_acc(float z) { return 2.0f * sigmoidf_acc(2.0f * z) - 1.0f; }
+__device__ __forceinline__ float tanh_acc(float z) { return fmaf(2.0f, sigmoidf_acc(2.0f * z), -1.0f); }
 
-// K1a: 16 jobs per CTA. Thread (g, half) owns LSTM gate row g of both layers (weights in
-// registers) and evaluates it for the 8 jobs of its half, so each step is an FMA-rich
-// [8 jobs x 48|64] x [48|64] product per thread instead of a latency-bound matvec. Jobs with fewer
+// K1a: 2*HJ jobs per 256-thread CTA (HJ = jobs per half, chosen per call so the grid is about one
+// wave: HJ = ceil(J / (2 * SMs)), 1..16). Thread (g, half) owns LSTM gate row g of both layers
+// (weights in registers) and evaluates it for the HJ jobs of its half, so each step is an FMA-rich
+// [HJ jobs x 48|64] x [48|64] product per thread instead of a latency-bound matvec. Jobs with fewer
 // layers freeze after their last step (h, c kept), so the final h is the state at step l_j - 1.
+// Every job's arithmetic (operation order, explicit fmaf) is independent of HJ and of the CTA it
+// lands in, so x is bit-identical however the jobs are split across CTAs or ranks.
+template <int HJ>
+struct EncCfg {
+  static constexpr int NJ = 2 * HJ;                       // jobs per CTA
+  static constexpr int CH = HJ <= 8 ? 16 : 8;             // layers staged per chunk
+  static constexpr int RC = (NJ * kLstm + kEncThreads - 1) / kEncThreads;   // cells per thread
+  static constexpr int XS = kXDim + 2;
+  static constexpr int E_OFF = 0;                         // sE [NJ][CH][16]
+  static constexpr int TL_OFF = E_OFF + NJ * CH * kEmbed;  // sTl [NJ][CH][16]; sX [NJ][XS] aliases it
+  static constexpr int H1_OFF = TL_OFF + NJ * CH * kNMax;  // sH1 [NJ][32]
+  static constexpr int H2_OFF = H1_OFF + NJ * kLstm;       // sH2 [NJ][32]
+  static constexpr int G_OFF = H2_OFF + NJ * kLstm;        // sG [NJ][128]
+  static constexpr int N_OFF = G_OFF + NJ * 4 * kLstm;     // int sN[NJ], sL[NJ]
+  static constexpr int FLOATS = N_OFF + 2 * NJ;
+  static constexpr size_t BYTES = sizeof(float) * FLOATS;
+  static_assert(CH * kNMax >= XS, "sX must fit in the sTl chunk it aliases");
+};
+
+template <int HJ>
 __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_constant__ EncodeParams p) {
-  __shared__ __align__(16) float sE[kEncJobs][kChunk][kEmbed];   // layer embeddings e_i of the chunk
-  __shared__ float sTl[kEncJobs][kChunk][kNMax];                  // log2(1 + T) of the chunk
-  __shared__ __align__(16) float sH1[kEncJobs][kLstm], sH2[kEncJobs][kLstm];
-  __shared__ float sG[kEncJobs][4 * kLstm];
-  float (*sX)[kXDim + 2] = reinterpret_cast<float (*)[kXDim + 2]>(&sTl[0][0][0]);   // reused after the LSTM
-  __shared__ int sN[kEncJobs], sL[kEncJobs];
+  using C = EncCfg<HJ>;
+  extern __shared__ __align__(16) float smem[];
+  float (*sE)[C::CH][kEmbed] = reinterpret_cast<float (*)[C::CH][kEmbed]>(smem + C::E_OFF);
+  float (*sTl)[C::CH][kNMax] = reinterpret_cast<float (*)[C::CH][kNMax]>(smem + C::TL_OFF);
+  float (*sX)[C::XS] = reinterpret_cast<float (*)[C::XS]>(smem + C::TL_OFF);   // after the LSTM
+  float (*sH1)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H1_OFF);
+  float (*sH2)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H2_OFF);
+  float (*sG)[4 * kLstm] = reinterpret_cast<float (*)[4 * kLstm]>(smem + C::G_OFF);
+  int* sN = reinterpret_cast<int*>(smem + C::N_OFF);
+  int* sL = sN + C::NJ;
   const int tid = threadIdx.x;
   const int g = tid & (4 * kLstm - 1), half = tid >> 7;
-  const int j0 = blockIdx.x * kEncJobs;
-  const int nj = min(kEncJobs, p.J - j0);
+  const int j0 = p.j_begin + blockIdx.x * C::NJ;
+  const int nj = min(C::NJ, p.j_end - j0);
   const float* P = p.params;
-  if (tid < kEncJobs) {
+  if (tid < C::NJ) {
     sN[tid] = tid < nj ? p.n[j0 + tid] : 1;
     sL[tid] = tid < nj ? p.l[j0 + tid] : 0;
   }
-  for (int e = tid; e < kEncJobs * kLstm; e += kEncThreads) {
+  for (int e = tid; e < C::NJ * kLstm; e += kEncThreads) {
     (&sH1[0][0])[e] = 0.f;
     (&sH2[0][0])[e] = 0.f;
   }
@@ -59,18 +83,36 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     wh2[d] = P[p.off.l2Wh + g * kLstm + d];
   }
   const float bg1 = P[p.off.l1b + g], bg2 = P[p.off.l2b + g];
-  // cell states: thread owns (job = tid / 16, cells 2*(tid % 16), +1) of each layer
-  const int cj = tid >> 4, cc = (tid & 15) * 2;
-  float c1[2] = {0.f, 0.f}, c2[2] = {0.f, 0.f};
+  // cell states: thread owns cells e = tid + 256 r (job e / 32, unit e % 32) of each layer
+  float c1[C::RC], c2[C::RC];
+#pragma unroll
+  for (int r = 0; r < C::RC; ++r) c1[r] = c2[r] = 0.f;
   __syncthreads();
   int lmax = 0;
-  for (int k = 0; k < kEncJobs; ++k) lmax = max(lmax, sL[k]);
+  for (int k = 0; k < C::NJ; ++k) lmax = max(lmax, sL[k]);
 
-  for (int i0 = 0; i0 < lmax; i0 += kChunk) {
-    const int len = min(kChunk, lmax - i0);
+  // gates of one layer for the HJ jobs of this half: z = b + Wx in + Wh h  (4 partial sums)
+  auto cell_update = [&](float (*sHout)[kLstm], float* cst, int step) {
+#pragma unroll
+    for (int r = 0; r < C::RC; ++r) {
+      const int e = tid + r * kEncThreads;
+      if (e < C::NJ * kLstm) {
+        const int jj = e >> 5, u = e & (kLstm - 1);
+        if (step < sL[jj]) {
+          const float ig = sigmoidf_acc(sG[jj][u]), fg = sigmoidf_acc(sG[jj][kLstm + u]);
+          const float gg = tanh_acc(sG[jj][2 * kLstm + u]), og = sigmoidf_acc(sG[jj][3 * kLstm + u]);
+          cst[r] = fmaf(fg, cst[r], ig * gg);
+          sHout[jj][u] = og * tanh_acc(cst[r]);
+        }
+      }
+    }
+  };
+
+  for (int i0 = 0; i0 < lmax; i0 += C::CH) {
+    const int len = min(C::CH, lmax - i0);
     __syncthreads();
     // t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers, 0 on padding (R#7, R#8)
-    for (int e = tid; e < kEncJobs * len * kNMax; e += kEncThreads) {
+    for (int e = tid; e < C::NJ * len * kNMax; e += kEncThreads) {
       const int jj = e / (len * kNMax), r = e % (len * kNMax), i = r / kNMax, w = r % kNMax;
       float v = 0.f;
       if (jj < nj && i0 + i < sL[jj] && w < sN[jj]) v = log2f(1.0f + p.T[((size_t)(j0 + jj) * p.l_max + i0 + i) * kNMax + w]);
@@ -78,7 +120,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     }
     __syncthreads();
     // e_i = W_e t'_i + b_e (R#4)
-    for (int e = tid; e < kEncJobs * len * kEmbed; e += kEncThreads) {
+    for (int e = tid; e < C::NJ * len * kEmbed; e += kEncThreads) {
       const int jj = e / (len * kEmbed), r = e % (len * kEmbed), i = r / kEmbed, d = r % kEmbed;
       float acc = P[p.off.b_e + d];
 #pragma unroll
@@ -87,11 +129,11 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     }
     __syncthreads();
     for (int i = 0; i < len; ++i) {
-      // ---- layer 1 gates for the 8 jobs of this half
-      float z[kHalfJobs];
+      // ---- layer 1 gates for the HJ jobs of this half
+      float z[HJ];
 #pragma unroll
-      for (int k = 0; k < kHalfJobs; ++k) {
-        const int jj = half * kHalfJobs + k;
+      for (int k = 0; k < HJ; ++k) {
+        const int jj = half * HJ + k;
         const float4* e4 = reinterpret_cast<const float4*>(sE[jj][i]);
         const float4* h4 = reinterpret_cast<const float4*>(sH1[jj]);
         float a0 = bg1, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -110,23 +152,14 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
         z[k] = (a0 + a1) + (a2 + a3);
       }
 #pragma unroll
-      for (int k = 0; k < kHalfJobs; ++k) sG[half * kHalfJobs + k][g] = z[k];
+      for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
       __syncthreads();
-      if (i0 + i < sL[cj]) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = cc + u;
-          const float ig = sigmoidf_acc(sG[cj][c]), fg = sigmoidf_acc(sG[cj][kLstm + c]);
-          const float gg = tanh_acc(sG[cj][2 * kLstm + c]), og = sigmoidf_acc(sG[cj][3 * kLstm + c]);
-          c1[u] = fg * c1[u] + ig * gg;
-          sH1[cj][c] = og * tanh_acc(c1[u]);
-        }
-      }
+      cell_update(sH1, c1, i0 + i);
       __syncthreads();
       // ---- layer 2 gates
 #pragma unroll
-      for (int k = 0; k < kHalfJobs; ++k) {
-        const int jj = half * kHalfJobs + k;
+      for (int k = 0; k < HJ; ++k) {
+        const int jj = half * HJ + k;
         const float4* x4 = reinterpret_cast<const float4*>(sH1[jj]);
         const float4* h4 = reinterpret_cast<const float4*>(sH2[jj]);
         float a0 = bg2, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -141,18 +174,9 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
         z[k] = (a0 + a1) + (a2 + a3);
       }
 #pragma unroll
-      for (int k = 0; k < kHalfJobs; ++k) sG[half * kHalfJobs + k][g] = z[k];
+      for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
       __syncthreads();
-      if (i0 + i < sL[cj]) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = cc + u;
-          const float ig = sigmoidf_acc(sG[cj][c]), fg = sigmoidf_acc(sG[cj][kLstm + c]);
-          const float gg = tanh_acc(sG[cj][2 * kLstm + c]), og = sigmoidf_acc(sG[cj][3 * kLstm + c]);
-          c2[u] = fg * c2[u] + ig * gg;
-          sH2[cj][c] = og * tanh_acc(c2[u]);
-        }
-      }
+      cell_update(sH2, c2, i0 + i);
       __syncthreads();
     }
   }
@@ -170,11 +194,38 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     sX[jj][i] = v;
   }
   __syncthreads();
-  if (p.x_out)
-    for (int e = tid; e < nj * kXDim; e += kEncThreads)
-      p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
-  if (tid < nj) {
-    const int j = j0 + tid, n = sN[tid];
+  for (int e = tid; e < nj * kXDim; e += kEncThreads)
+    p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
+}
+
+// K1b: per-job projections for K2, 32 jobs per CTA, one output column per thread per pass:
+//   a[j][c]    = b1[c] + sum_i W1[c][i] x[j][i]            (job half of layer 1)
+//   what[j][c] = sum_{w < n_j} W_o[w][c] / n_j             (worker-mean fold of the output layer)
+//   beta[j]    = sum_{w < n_j} b_o[w] / n_j, and the job's arg-max keys reset to 0.
+// W1's job columns stream through shared memory in 16-wide K slices (coalesced row segments), so
+// every weight is fetched once per CTA and read conflict-free; each x_j is a broadcast LDS.128.
+constexpr int kProjJobs = 32;
+constexpr int kProjThreads = 256;
+constexpr int kProjK = 16;
+
+__global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ EncodeParams p) {
+  __shared__ __align__(16) float sXt[kXDim][kProjJobs];    // transposed: 4 jobs per LDS.128
+  __shared__ __align__(16) float sM[kNMax][kProjJobs];     // mask / n
+  __shared__ float sW[kProjK][kProjThreads + 1];          // W1[cb + c][i0 + k] at sW[k][c]
+  const int j0 = blockIdx.x * kProjJobs, tid = threadIdx.x;
+  const float* P = p.params;
+  const int jn = min(kProjJobs, p.J - j0);
+  for (int e = tid; e < kXDim * kProjJobs; e += kProjThreads) {
+    const int jj = e / kXDim, i = e % kXDim;
+    sXt[i][jj] = (jj < jn) ? p.x_out[(size_t)(j0 + jj) * kXDim + i] : 0.f;
+  }
+  for (int e = tid; e < kNMax * kProjJobs; e += kProjThreads) {
+    const int w = e / kProjJobs, jj = e % kProjJobs;
+    const int nj = (jj < jn) ? p.n[j0 + jj] : 1;
+    sM[w][jj] = w < nj ? 1.0f / static_cast<float>(nj) : 0.f;
+  }
+  if (tid < jn) {
+    const int j = j0 + tid, n = p.n[j];
     if (p.beta_out) {
       float acc = 0.f;
       for (int w = 0; w < n; ++w) acc += P[p.off.b_o + w];
@@ -183,46 +234,32 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     if (p.keys) p.keys[j] = 0ull;
     if (p.cur_keys) p.cur_keys[j] = 0ull;
   }
-}
-
-// K1b: per-job projections for K2, 32 jobs per CTA, one output column per thread per pass:
-//   a[j][c]    = b1[c] + sum_i W1[c][i] x[j][i]            (job half of layer 1)
-//   what[j][c] = sum_{w < n_j} W_o[w][c] / n_j             (worker-mean fold of the output layer)
-constexpr int kProjJobs = 32;
-constexpr int kProjThreads = 256;
-
-__global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ EncodeParams p) {
-  __shared__ __align__(16) float sXt[kXDim][kProjJobs];    // transposed: 4 jobs per LDS.128
-  __shared__ __align__(16) float sM[kNMax][kProjJobs];     // mask / n
-  const int j0 = blockIdx.x * kProjJobs, tid = threadIdx.x;
-  const float* P = p.params;
-  for (int e = tid; e < kXDim * kProjJobs; e += kProjThreads) {
-    const int jj = e / kXDim, i = e % kXDim;
-    sXt[i][jj] = (j0 + jj < p.J) ? p.x_out[(size_t)(j0 + jj) * kXDim + i] : 0.f;
-  }
-  for (int e = tid; e < kNMax * kProjJobs; e += kProjThreads) {
-    const int w = e / kProjJobs, jj = e % kProjJobs;
-    const int nj = (j0 + jj < p.J) ? p.n[j0 + jj] : 1;
-    sM[w][jj] = w < nj ? 1.0f / static_cast<float>(nj) : 0.f;
-  }
-  __syncthreads();
   const int H = p.H;
-  const int jn = min(kProjJobs, p.J - j0);
-  for (int col = tid; col < H; col += kProjThreads) {
+  for (int cb = 0; cb < H; cb += kProjThreads) {
+    const int col = cb + tid;
     float acc[kProjJobs];
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
-    const float* wrow = P + p.off.W[1] + (size_t)col * kZDim;
-    for (int i = 0; i < kXDim; ++i) {
-      const float w = wrow[i];
-      const float4* xv = reinterpret_cast<const float4*>(sXt[i]);
+    for (int i0 = 0; i0 < kXDim; i0 += kProjK) {
+      const int len = min(kProjK, kXDim - i0);
+      __syncthreads();   // previous slice consumed (and sXt / sM staged on the first pass)
+      for (int e = tid; e < kProjThreads * kProjK; e += kProjThreads) {
+        const int c = e / kProjK, k = e % kProjK;
+        sW[k][c] = (cb + c < H && k < len) ? P[p.off.W[1] + (size_t)(cb + c) * kZDim + i0 + k] : 0.f;
+      }
+      __syncthreads();
+      for (int k = 0; k < len; ++k) {
+        const float w = sW[k][tid];
+        const float4* xv = reinterpret_cast<const float4*>(sXt[i0 + k]);
 #pragma unroll
-      for (int q = 0; q < kProjJobs / 4; ++q) {
-        const float4 v = xv[q];
-        acc[4 * q] = fmaf(w, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(w, v.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(w, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(w, v.w, acc[4 * q + 3]);
+        for (int q = 0; q < kProjJobs / 4; ++q) {
+          const float4 v = xv[q];
+          acc[4 * q] = fmaf(w, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(w, v.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = fmaf(w, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(w, v.w, acc[4 * q + 3]);
+        }
       }
     }
+    if (col >= H) continue;
     const float b1 = P[p.off.b[1] + col];
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj)
@@ -245,12 +282,55 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
   }
 }
 
-// K1 = K1a (+ K1b when the projections are requested; they need x, so x_out must be set).
-cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s) {
+template <int HJ>
+cudaError_t launch_lstm_hj(const EncodeParams& p, cudaStream_t s) {
+  using C = EncCfg<HJ>;
+  static unsigned long long attr_done = 0;   // per device: opt in to > 48 KB dynamic shared memory
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!(attr_done >> (dev & 63) & 1ull)) {
+    e = cudaFuncSetAttribute(encode_kernel<HJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::BYTES));
+    if (e != cudaSuccess) return e;
+    attr_done |= 1ull << (dev & 63);
+  }
+  const int n = p.j_end - p.j_begin;
+  encode_kernel<HJ><<<(n + C::NJ - 1) / C::NJ, kEncThreads, C::BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+int encode_jobs_per_half(int n, int num_sms) {
+  const int hj = (n + 2 * num_sms - 1) / (2 * num_sms);
+  return hj < 1 ? 1 : (hj > 16 ? 16 : hj);
+}
+
+// K1a over jobs [p.j_begin, p.j_end): writes rows of p.x_out (global job index).
+cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s) {
+  if (p.j_end <= p.j_begin) return cudaSuccess;
+  switch (encode_jobs_per_half(p.j_end - p.j_begin, num_sms)) {
+    case 1: return launch_lstm_hj<1>(p, s);
+    case 2: return launch_lstm_hj<2>(p, s);
+    case 3: return launch_lstm_hj<3>(p, s);
+    case 4: return launch_lstm_hj<4>(p, s);
+    case 5: return launch_lstm_hj<5>(p, s);
+    case 6: return launch_lstm_hj<6>(p, s);
+    case 7: return launch_lstm_hj<7>(p, s);
+    case 8: return launch_lstm_hj<8>(p, s);
+    case 9: return launch_lstm_hj<9>(p, s);
+    case 10: return launch_lstm_hj<10>(p, s);
+    case 11: return launch_lstm_hj<11>(p, s);
+    case 12: return launch_lstm_hj<12>(p, s);
+    case 13: return launch_lstm_hj<13>(p, s);
+    case 14: return launch_lstm_hj<14>(p, s);
+    case 15: return launch_lstm_hj<15>(p, s);
+    default: return launch_lstm_hj<16>(p, s);
+  }
+}
+
+// K1b over all p.J jobs (reads p.x_out rows 0..J-1).
+cudaError_t launch_project(const EncodeParams& p, cudaStream_t s) {
   if (p.J <= 0) return cudaSuccess;
-  encode_kernel<<<(p.J + kEncJobs - 1) / kEncJobs, kEncThreads, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || !p.a_out) return e;
   project_kernel<<<(p.J + kProjJobs - 1) / kProjJobs, kProjThreads, 0, s>>>(p);
   return cudaGetLastError();
 }

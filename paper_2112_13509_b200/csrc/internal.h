@@ -34,10 +34,11 @@ ParamOffsets make_offsets(const autobyte_net_desc& d);
 // ---------------------------------------------------------------- kernel parameter blocks
 struct EncodeParams {
   int J, l_max, H;
+  int j_begin, j_end;  // K1a job range (K1b always covers [0, J))
   const float* T; const float* B_d; const float* B_u;
   const int32_t* n; const int32_t* l; const int32_t* m; const int32_t* arc;
   const float* params; ParamOffsets off;
-  float* x_out;        // [J][82] or null
+  float* x_out;        // [J][82] (K1a writes rows of its range, K1b reads all rows)
   // per-job vectors, row stride jv floats (K2 reads one contiguous block [a | w | beta] per job)
   long long jv;
   float* a_out;        // [J][jv]: W1x x + b1 in [0, H), or null
@@ -86,7 +87,8 @@ struct AdaptParams {
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)
-cudaError_t launch_encode(const EncodeParams& p, cudaStream_t s);
+cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s);   // K1a
+cudaError_t launch_project(const EncodeParams& p, cudaStream_t s);                    // K1b
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s);
 cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_score, const int32_t* cur_idx,

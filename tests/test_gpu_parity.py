@@ -66,6 +66,24 @@ def test_encoder_matches_oracle():
     np.testing.assert_allclose(x, ref, rtol=1e-4, atol=2e-5)
 
 
+@pytest.mark.parametrize("J", [1, 300, 1000, 4400])
+def test_encoder_job_grouping_is_bit_invariant(J):
+    """K1a packs 2*HJ jobs per CTA with HJ = ceil(J / (2 SMs)) (1, 2, 4, 15 here); a job's x must
+    not depend on its grouping (this is what keeps the encode-sharded multi-GPU keys identical
+    to one GPU's): x(all jobs)[idx] == x(jobs idx alone) bit for bit, and both match the oracle."""
+    desc = synth.NetDesc(2, 64)
+    W = synth.make_weights(desc)
+    jobs = synth.small_fleet(J, synth.BASE_SEED + 7)
+    net = make(2, 64, W)
+    x = net.encode(dev(jobs)).cpu().numpy()
+    rng = np.random.default_rng(J)
+    idx = np.unique(np.concatenate([[0, J - 1], rng.integers(0, J, size=min(J, 6))]))
+    sub = jobs.subset(idx)
+    xs = net.encode(dev(sub)).cpu().numpy()
+    assert np.array_equal(x[idx].view(np.uint32), xs.view(np.uint32))
+    np.testing.assert_allclose(x[idx], oracle.encode_jobs(W, sub), rtol=1e-4, atol=2e-5)
+
+
 # ------------------------------------------------------------------------------------- exact cases
 def _pad_hand_net(L):
     """The hand-computed H=2 net of tests/golden/hand_net.json embedded in H=64 with zeros."""

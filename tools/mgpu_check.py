@@ -1,6 +1,7 @@
 """Multi-GPU parity (run under torchrun, one rank per GPU): candidate-sharded arg-max with the NCCL
 key exchange must be bit-identical on every rank and to the single-GPU result (G-invariance), and
-agree with the float64 oracle on sampled jobs. Prints one JSON line per config on rank 0."""
+agree with the float64 oracle on sampled jobs; the replicated adapt after the encode-sharded K1a
+must leave bit-identical weights on every rank and equal to one GPU's. Prints one JSON line per config on rank 0."""
 import json
 import os
 import sys
@@ -44,6 +45,23 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
         s_ora = oracle.score_matrix(W, jobs, grid, job_idx=sample)
         check_argmax(bi.cpu().numpy()[sample], s_ora, 2e-2)
         res["oracle_sampled_ok"] = True
+    # adapt: replicated K4 after the encode-sharded K1a must leave bit-identical weights on every
+    # rank, equal to the single-GPU update
+    batch = synth.make_adapt_batch(jobs, grid, 11)
+    sp = torch.as_tensor(batch.S_p, device=dev)
+    sc = torch.as_tensor(batch.S_c, device=dev)
+    vb = torch.as_tensor(batch.V_bar, device=dev)
+    loss = net.adapt(dj, sp, sc, vb, lr=1e-3, steps=1)
+    torch.cuda.synchronize(dev)
+    blob = torch.frombuffer(bytearray(net.get_weights_blob()), dtype=torch.uint8).to(dev)
+    allb = [torch.empty_like(blob) for _ in range(world)]
+    dist.all_gather(allb, blob)
+    res["adapt_same_on_all_ranks"] = all(torch.equal(allb[0], x) for x in allb)
+    if rank == 0:
+        loss1 = single.adapt(dj, sp, sc, vb, lr=1e-3, steps=1)
+        torch.cuda.synchronize(dev)
+        res["adapt_g_invariant"] = (single.get_weights_blob() == net.get_weights_blob()
+                                    and float(loss1.item()) == float(loss.item()))
         single.close()
     net.close()
     return res
@@ -67,7 +85,7 @@ def main():
         r = run(name, desc, jobs, grid, cg, dev, rank, world)
         if rank == 0:
             print(json.dumps(r), flush=True)
-            ok &= r["same_on_all_ranks"] and r["g_invariant"]
+            ok &= r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
