@@ -3,54 +3,101 @@
 // P:438 triggered when prediction error > 10%; R#12 objective, R#13 head-only plain SGD).
 //
 // Per step, phases separated by a grid-wide barrier:
-//   F_k   H_k = ReLU(H_{k-1} W_k^T + b_k), k = 1..L (H_0 = Z = [x | u])      fp32 SIMT tiles
-//   OUT   R = mask_b (H_L W_o^T + b_o - V_bar) / B                            (dV of the objective)
+//   F_k   H_k = ReLU(H_{k-1} W_k^T + b_k), k = 1..L (H_0 = Z = [x | u])      3xTF32 tensor-core tiles
+//   OUT   R = mask_b (H_L W_o^T + b_o - V_bar) / B        (dV of the objective; one warp per row)
 //   BO    dW_o = R^T H_L, db_o = colsum R, D_L = (R W_o) * [H_L > 0]
 //   Bk    dW_k = D_k^T H_{k-1}, db_k = colsum D_k, D_{k-1} = (D_k W_k) * [H_{k-1} > 0]  (pre-update W_k)
-//   SGD   theta -= lr * grad over all head parameters
+//         + SGD of the layer above (its gradient is complete and no later phase reads it)
+//   SGD   W1, b1 (after B1)
 // Every output element is produced by exactly one thread with a fixed summation order, so the
 // update is deterministic and replicas on different GPUs stay bit-identical without traffic.
-// The work is ~3x a B-row forward (5 GFLOP at B=1024, 4x512): latency-bound, << 1% of a C5 step;
-// fp32 SIMT keeps the gradient well inside the parity tolerance (K4).
+// The work is ~3x a B-row forward (5 GFLOP at B=1024, 4x512): latency-bound, << 1% of a C5 step.
+// Every GEMM runs on the legacy mma.sync tensor path with 3xTF32 split operands (big*big +
+// big*small + small*big, ~fp32 accuracy), which keeps the gradient well inside the parity
+// tolerance (K4) at a fraction of the SIMT instruction count.
+#include <cstdlib>
+
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace ab {
 
 constexpr int kAdaptThreads = 256;
-constexpr int kTM = 64, kTN = 64, kTK = 16;
+constexpr int kTM = 64, kTN = 64, kTK = 32;
 constexpr int kSplitK = kAdaptSplitK;   // K = B splits of the weight-gradient GEMMs (partials in grads[kSplitK][total])
 
 struct Gemm {
   int M, N, K;
-  const float* A; long long lam, lak;    // A(m, k) = A[m*lam + k*lak]
-  const float* Bm; long long lbk, lbn;   // B(k, n) = Bm[k*lbk + n*lbn]
+  const float* A; long long lam, lak;    // A(m, k) = A[m*lam + k*lak]; lak == 1 or lam == 1
+  const float* Bm; long long lbk, lbn;   // B(k, n) = Bm[k*lbk + n*lbn]; lbk == 1 or lbn == 1
   float* C; long long ldc;               // C[m*ldc + n]
-  int mode;                              // 0: ReLU(acc + bias[n]); 1: acc * [mask(m,n) > 0]; 2: acc;
-                                         // 3: (acc + bias[n] - vbar[m][n]) * [n < nvalid[m]] * scale
+  int mode;                              // 0: ReLU(acc + bias[n]); 1: acc * [mask(m,n) > 0]; 2: acc
   const float* bias;
   const float* mask; long long ldmask;
-  const float* vbar; const int32_t* nvalid; float scale;
   int ksplit;                            // split-K count (mode 2 only): partial s -> C + s*cpart
   long long cpart;
   __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
 };
 
-constexpr int kStages = 3;   // cp.async pipeline depth of the SIMT GEMM tiles
+constexpr int kStages = 4;   // cp.async pipeline depth of the GEMM tiles (prefetch distance kStages - 1)
+// One operand slice in shared memory, in the orientation of its global layout so every 16-byte
+// cp.async copies a contiguous vector: K-contiguous [64][kTK + 4] or MN-contiguous [kTK][64 + 8].
+// Both paddings make the m16n8k8 fragment reads (lanes g = lane/4 along M|N, t = lane%4 along K)
+// hit 32 distinct banks.
+constexpr int kSK = kTK + 4, kSM = kTM + 8;
+constexpr int kSliceFloats = (kTM * kSK > kTK * kSM) ? kTM * kSK : kTK * kSM;
+constexpr size_t kAdaptSmemBytes = sizeof(float) * kStages * 2 * kSliceFloats;
 
-__device__ __forceinline__ void cp_async4(float* smem_dst, const float* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
-               "r"(valid ? 4 : 0)
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
+               "r"(valid ? 16 : 0)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// One 64 x 64 output tile (or one K-slice of it for split-K). Each thread owns 4 x 4 outputs;
-// 16-wide K slices of both operands stream through a 3-stage cp.async ring (zero-filled at the
-// edges), so global-load latency overlaps the FMAs of the two slices ahead.
-__device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTK][kTM + 4], float (*Bs)[kTK][kTN + 4]) {
+// x = big + small with both parts tf32 (10-bit mantissa each): the 3xTF32 product
+// big*big + big*small + small*big carries ~fp32 accuracy (the dropped small*small is ~2^-22 relative).
+__device__ __forceinline__ void split_tf32(float x, uint32_t& big, uint32_t& small) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(big) : "f"(x));
+  const float r = x - __uint_as_float(big);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(small) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// Stage one 64 x kTK slice of an operand: X(mn, k) = base[mn*lmn + k*lk] for mn in [mn0, mn0+64),
+// k in [k0, k0+kTK), zero-filled outside [0, MN) x [k0, kend). 16-byte vectors, kTK/16 per thread.
+__device__ __forceinline__ void stage_slice(float* dst, const float* base, long long lmn, long long lk, int MN,
+                                            int mn0, int k0, int kend) {
+#pragma unroll
+  for (int r = 0; r < kTK / 16; ++r) {
+    const int e = threadIdx.x + r * kAdaptThreads;
+    if (lk == 1) {   // K-contiguous: vector (mn, 4 k)
+      const int mn = e / (kTK / 4), kq = (e % (kTK / 4)) * 4;
+      const bool v = mn0 + mn < MN && k0 + kq < kend;
+      cp_async16(dst + mn * kSK + kq, v ? base + (long long)(mn0 + mn) * lmn + (k0 + kq) : base, v);
+    } else {         // MN-contiguous: vector (k, 4 mn)
+      const int k = e >> 4, mq = (e & 15) * 4;
+      const bool v = k0 + k < kend && mn0 + mq < MN;
+      cp_async16(dst + k * kSM + mq, v ? base + (long long)(k0 + k) * lk + (mn0 + mq) : base, v);
+    }
+  }
+}
+__device__ __forceinline__ float slice_at(const float* s, bool kcontig, int mn, int k) {
+  return kcontig ? s[mn * kSK + k] : s[k * kSM + mn];
+}
+
+// One 64 x 64 output tile (or one K-slice range of it for split-K) on the tensor cores, 3xTF32.
+// 8 warps as 2 (M) x 4 (N), each a 32 x 16 warp tile = 2 x 2 m16n8 fragments; kTK-wide K slices
+// of both operands stream through a kStages-deep cp.async ring. The accumulation order is fixed, so
+// the result is deterministic (replicas stay bit-identical).
+__device__ void gemm_tile(const Gemm& g, int work, float* ring) {
   const int tiles_n = (g.N + kTN - 1) / kTN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
   const int split = g.ksplit > 1 ? work / tiles_mn : 0;
@@ -62,72 +109,88 @@ __device__ void gemm_tile(const Gemm& g, int work, float (*As)[kTK][kTM + 4], fl
     kbeg = split * chunk;
     kend = min(g.K, kbeg + chunk);
   }
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  int aml[4], akl[4], bnl[4], bkl[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int e = tid + r * kAdaptThreads;
-    if (g.lak == 1) { akl[r] = e % kTK; aml[r] = e / kTK; } else { aml[r] = e % kTM; akl[r] = e / kTM; }
-    if (g.lbk == 1) { bkl[r] = e % kTK; bnl[r] = e / kTK; } else { bnl[r] = e % kTN; bkl[r] = e / kTN; }
-  }
+  const bool a_kc = g.lak == 1, b_kc = g.lbk == 1;
   const int nk = kend > kbeg ? (kend - kbeg + kTK - 1) / kTK : 0;
+  auto As = [&](int st) { return ring + st * 2 * kSliceFloats; };
+  auto Bs = [&](int st) { return ring + st * 2 * kSliceFloats + kSliceFloats; };
   auto issue = [&](int it) {
     if (it < nk) {
       const int k0 = kbeg + it * kTK, st = it % kStages;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int m = m0 + aml[r], k = k0 + akl[r];
-        const bool va = m < g.M && k < kend;
-        cp_async4(&As[st][akl[r]][aml[r]], va ? g.A + (m * g.lam + k * g.lak) : g.A, va);
-        const int n = n0 + bnl[r], kk = k0 + bkl[r];
-        const bool vb = n < g.N && kk < kend;
-        cp_async4(&Bs[st][bkl[r]][bnl[r]], vb ? g.Bm + (kk * g.lbk + n * g.lbn) : g.Bm, vb);
-      }
+      stage_slice(As(st), g.A, g.lam, g.lak, g.M, m0, k0, kend);
+      stage_slice(Bs(st), g.Bm, g.lbn, g.lbk, g.N, n0, k0, kend);
     }
     cp_async_commit();   // (empty groups keep the wait arithmetic uniform)
   };
-  float acc[4][4] = {};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16, gq = lane >> 2, tq = lane & 3;
+  float acc[2][2][4] = {};
   __syncthreads();       // the ring may still be read by the previous tile
-  issue(0);
-  issue(1);
+#pragma unroll
+  for (int i = 0; i < kStages - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
-    issue(it + 2);       // overwrites the stage read two slices ago (all threads are past it)
-    const int st = it % kStages;
+    issue(it + kStages - 1);   // overwrites the stage read one slice ago (all threads are past it)
+    const float* sa = As(it % kStages);
+    const float* sb = Bs(it % kStages);
+    // per-slice partial sums start from zero and are added to acc with IEEE fp32 adds: the
+    // tensor core's internal accumulation then only spans 6 products-of-8, not the whole K
+    float part[2][2][4] = {};
 #pragma unroll
-    for (int kk = 0; kk < kTK; ++kk) {
-      const float4 a = *reinterpret_cast<const float4*>(&As[st][kk][ty * 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[st][kk][tx * 4]);
-      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    for (int kk = 0; kk < kTK; kk += 8) {
+      uint32_t ab[2][4], as[2][4], bb[2][2], bs[2][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm + i * 16 + gq;
+        split_tf32(slice_at(sa, a_kc, r, kk + tq), ab[i][0], as[i][0]);
+        split_tf32(slice_at(sa, a_kc, r + 8, kk + tq), ab[i][1], as[i][1]);
+        split_tf32(slice_at(sa, a_kc, r, kk + tq + 4), ab[i][2], as[i][2]);
+        split_tf32(slice_at(sa, a_kc, r + 8, kk + tq + 4), ab[i][3], as[i][3]);
+      }
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(av[i], bv[jj], acc[i][jj]);
+      for (int j = 0; j < 2; ++j) {
+        const int c = wn + j * 8 + gq;
+        split_tf32(slice_at(sb, b_kc, c, kk + tq), bb[j][0], bs[j][0]);
+        split_tf32(slice_at(sb, b_kc, c, kk + tq + 4), bb[j][1], bs[j][1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          mma_tf32(part[i][j], as[i], bb[j]);
+          mma_tf32(part[i][j], ab[i], bs[j]);
+          mma_tf32(part[i][j], ab[i], bb[j]);
+        }
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[i][j][r] += part[i][j][r];
   }
   cp_async_wait<0>();
   float* C = g.C + (g.ksplit > 1 ? split * g.cpart : 0);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
-    if (m >= g.M) continue;
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int n = n0 + tx * 4 + jj;
-      if (n >= g.N) continue;
-      float v = acc[i][jj];
-      if (g.mode == 0) v = relu(v + g.bias[n]);
-      else if (g.mode == 1) v = g.mask[m * g.ldmask + n] > 0.f ? v : 0.f;
-      else if (g.mode == 3) v = (n < g.nvalid[m]) ? (v + g.bias[n] - g.vbar[m * 16 + n]) * g.scale : 0.f;
-      C[m * g.ldc + n] = v;
-    }
-  }
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + wm + i * 16 + gq + (r >> 1) * 8;
+        const int n = n0 + wn + j * 8 + 2 * tq + (r & 1);
+        if (m >= g.M || n >= g.N) continue;
+        float v = acc[i][j][r];
+        if (g.mode == 0) v = relu(v + g.bias[n]);
+        else if (g.mode == 1) v = g.mask[m * g.ldmask + n] > 0.f ? v : 0.f;
+        C[m * g.ldc + n] = v;
+      }
 }
 
 #ifdef AB_STATS
 __device__ unsigned long long g_adapt_phase[64];   // block 0: clock at entry of each grid barrier
 __device__ int g_adapt_nphase;
+__device__ long long g_adapt_blk[1024][3];   // per block: smid, clock at F2 tile start, at F2 tile end
 #endif
 __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) {
 #ifdef AB_STATS
@@ -154,32 +217,85 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
 }
 
 // Column sums over the batch as kSplitK partials (like the split-K weight gradients, summed in fixed
-// order by the SGD sweep): out[s * stride + n] = sum_{b in segment s} X[b][n]. One warp per
-// (32-column group, segment); each lane walks its column down the segment (coalesced rows).
+// order by the SGD sweep): out[s * stride + n] = sum_{b in segment s} X[b][n]. One CTA per
+// (32-column group, segment), handed out from the highest block index down (those CTAs hold the
+// fewest GEMM tiles); warp w sums rows w, w+8, ... of the segment (coalesced, 4 loads in flight)
+// and warp 0 adds the 8 warp partials in fixed order.
 __device__ void colsum_split(const float* X, int B, int N, long long ld, float* out, long long stride) {
-  const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  __shared__ float red[kAdaptThreads / 32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kAdaptThreads / 32;
   const int groups = (N + 31) / 32, seg = (B + kSplitK - 1) / kSplitK;
-  for (int w = gwarp; w < groups * kSplitK; w += nwarps) {
-    const int sgi = w / groups, n = (w % groups) * 32 + lane;
+  for (int item = gridDim.x - 1 - blockIdx.x; item < groups * kSplitK; item += gridDim.x) {
+    const int sgi = item / groups, n = (item % groups) * 32 + lane;
     const int b0 = sgi * seg, b1 = min(B, b0 + seg);
-    if (n >= N) continue;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    int b = b0;
-    for (; b + 3 < b1; b += 4) {
-      a0 += X[(long long)b * ld + n];
-      a1 += X[(long long)(b + 1) * ld + n];
-      a2 += X[(long long)(b + 2) * ld + n];
-      a3 += X[(long long)(b + 3) * ld + n];
+    if (n < N) {
+      int b = b0 + warp;
+      for (; b + 3 * nw < b1; b += 4 * nw) {
+        a0 += X[(long long)b * ld + n];
+        a1 += X[(long long)(b + nw) * ld + n];
+        a2 += X[(long long)(b + 2 * nw) * ld + n];
+        a3 += X[(long long)(b + 3 * nw) * ld + n];
+      }
+      for (; b < b1; b += nw) a0 += X[(long long)b * ld + n];
     }
-    for (; b < b1; ++b) a0 += X[(long long)b * ld + n];
-    out[sgi * stride + n] = (a0 + a1) + (a2 + a3);
+    red[warp][lane] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    if (warp == 0 && n < N) {
+      float t = red[0][lane];
+      for (int w = 1; w < nw; ++w) t += red[w][lane];
+      out[sgi * stride + n] = t;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_constant__ AdaptParams p) {
-  __shared__ __align__(16) float As[kStages][kTK][kTM + 4];
-  __shared__ __align__(16) float Bs[kStages][kTK][kTN + 4];
+// Output layer residual, one warp per sample row (the N = 16 output is too narrow for a GEMM tile):
+// R[b][w] = [w < n_b] (W_o h_L,b + b_o - V_bar_b)[w] * scale, scale = 1/B (dV of the objective, R#12).
+// W_o is staged in shared memory once per CTA; lane l accumulates k = l, l+32, ... in fp32 FMA and
+// the 16 sums are reduced with a fixed xor butterfly (deterministic).
+__device__ void out_rows(const float* Hl, const float* Wo, const float* bo, const float* vbar, const int32_t* nvalid,
+                         float scale, int B, int H, float* R, float* sW) {
+  for (int e = threadIdx.x; e < kNMax * H; e += kAdaptThreads) sW[e] = Wo[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * kAdaptThreads + threadIdx.x) >> 5, nwarps = (gridDim.x * kAdaptThreads) >> 5;
+  for (int b = gwarp; b < B; b += nwarps) {
+    float acc[kNMax];
+#pragma unroll
+    for (int w = 0; w < kNMax; ++w) acc[w] = 0.f;
+    for (int k = lane; k < H; k += 32) {
+      const float h = Hl[(long long)b * H + k];
+#pragma unroll
+      for (int w = 0; w < kNMax; ++w) acc[w] = fmaf(h, sW[w * H + k], acc[w]);
+    }
+    float mine = 0.f;
+#pragma unroll
+    for (int w = 0; w < kNMax; ++w) {
+      float v = acc[w];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == w) mine = v;
+    }
+    if (lane < kNMax)
+      R[b * kNMax + lane] = lane < nvalid[b] ? (mine + bo[lane] - vbar[b * kNMax + lane]) * scale : 0.f;
+  }
+  __syncthreads();   // sW aliases the GEMM ring
+}
+
+// theta[i] -= lr * (sum of the kSplitK gradient partials, fixed order) over [begin, end).
+__device__ void sgd_range(float* P, const float* Gr, long long total, long long begin, long long end, float lr) {
+  const long long gtid = (long long)blockIdx.x * kAdaptThreads + threadIdx.x, gthreads = (long long)gridDim.x * kAdaptThreads;
+  for (long long i = begin + gtid; i < end; i += gthreads) {
+    float gsum = Gr[i];
+#pragma unroll
+    for (int sk = 1; sk < kSplitK; ++sk) gsum += Gr[sk * total + i];
+    P[i] = P[i] - lr * gsum;
+  }
+}
+
+__global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_constant__ AdaptParams p) {
+  extern __shared__ __align__(16) float ring[];   // kStages x {A, B} slices
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   unsigned int gen = 0;
@@ -216,17 +332,24 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
     for (int k = 1; k <= L; ++k) {
       const int Kin = k == 1 ? kZDim : H;
       const float* in = k == 1 ? Z : Hk(k - 1);
-      Gemm g{B, H, Kin, in, Kin, 1, P + p.off.W[k], 1, Kin, Hk(k), H, 0, P + p.off.b[k],
-             nullptr, 0, nullptr, nullptr, 0.f};
-      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, As, Bs);
+      Gemm g{B, H, Kin, in, Kin, 1, P + p.off.W[k], 1, Kin, Hk(k), H, 0, P + p.off.b[k], nullptr, 0};
+#ifdef AB_STATS
+      const long long tw0 = clock64();
+#endif
+      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, ring);
+#ifdef AB_STATS
+      if (k == 2 && step == 0 && threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_adapt_blk[blockIdx.x][0] = smid;
+        g_adapt_blk[blockIdx.x][1] = tw0;
+        g_adapt_blk[blockIdx.x][2] = clock64();
+      }
+#endif
       grid_sync(p.barrier, gen);
     }
-    {
-      Gemm g{B, kNMax, H, Hk(L), H, 1, P + p.off.W_o, 1, H, R, kNMax, 3, P + p.off.b_o,
-             nullptr, 0, p.v_obs, p.n, 1.0f / static_cast<float>(B)};
-      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, As, Bs);
-      grid_sync(p.barrier, gen);
-    }
+    out_rows(Hk(L), P + p.off.W_o, P + p.off.b_o, p.v_obs, p.n, 1.0f / static_cast<float>(B), B, H, R, ring);
+    grid_sync(p.barrier, gen);
     if (step == 0 && p.loss_before && blockIdx.x == 0) {
       // mean over b of the Eq. 2 norm ||mask (V_hat - V_bar)||_2; R holds residual / B
       __shared__ float s_norm[kAdaptThreads];
@@ -247,13 +370,12 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
     if (fwd_only) break;
     // ---------------- backward: output layer
     {
-      Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f,
-              kSplitK, p.off.total};
-      Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H, nullptr, nullptr, 0.f};
+      Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
+      Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H};
       const int t1 = gw.tiles(), t2 = gd.tiles();
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, As, Bs);
-        else gemm_tile(gd, t - t1, As, Bs);
+        if (t < t1) gemm_tile(gw, t, ring);
+        else gemm_tile(gd, t - t1, ring);
       }
       colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
       grid_sync(p.barrier, gen);
@@ -263,33 +385,28 @@ __global__ void __launch_bounds__(kAdaptThreads) adapt_kernel(const __grid_const
       const int Kin = k == 1 ? kZDim : H;
       const float* in = k == 1 ? Z : Hk(k - 1);
       const float* Dk = D[k & 1];
-      Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, nullptr, nullptr, 0.f,
-              kSplitK, p.off.total};
+      Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
       const int t1 = gw.tiles();
       int t2 = 0;
       Gemm gd{};
       if (k > 1) {
-        gd = Gemm{B, H, H, Dk, H, 1, P + p.off.W[k], H, 1, D[(k - 1) & 1], H, 1, nullptr, Hk(k - 1), H,
-                  nullptr, nullptr, 0.f};
+        gd = Gemm{B, H, H, Dk, H, 1, P + p.off.W[k], H, 1, D[(k - 1) & 1], H, 1, nullptr, Hk(k - 1), H};
         t2 = gd.tiles();
       }
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, As, Bs);
-        else gemm_tile(gd, t - t1, As, Bs);
+        if (t < t1) gemm_tile(gw, t, ring);
+        else gemm_tile(gd, t - t1, ring);
       }
       colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
+      // SGD of the layer above, whose gradient partials completed in the previous phase and whose
+      // weights no phase reads any more this step (W_o after BO; W_{k+1} after B_{k+1})
+      if (k == L) sgd_range(P, Gr, p.off.total, p.off.W_o, p.off.total, p.lr);
+      else sgd_range(P, Gr, p.off.total, p.off.W[k + 1], p.off.b[k + 1] + H, p.lr);
       grid_sync(p.barrier, gen);
     }
-    // ---------------- SGD on the head parameters (contiguous from W1 to b_o in the blob order)
-    const float lr = p.lr;
-    // (the weight gradients arrive as kSplitK partial sums over B; summed here in fixed order)
-    for (long long i = p.off.W[1] + gtid; i < p.off.total; i += gthreads) {
-      float gsum = Gr[i];
-#pragma unroll
-      for (int sk = 1; sk < kSplitK; ++sk) gsum += Gr[sk * p.off.total + i];
-      P[i] = P[i] - lr * gsum;
-    }
-    grid_sync(p.barrier, gen);
+    // ---------------- SGD of layer 1 (W1, b1); the kernel exit orders it after the last step
+    sgd_range(P, Gr, p.off.total, p.off.W[1], p.off.b[1] + H, p.lr);
+    if (step + 1 < nsteps) grid_sync(p.barrier, gen);
   }
 }
 
@@ -299,18 +416,28 @@ size_t adapt_ws_floats(int B, int H, int L) {
 
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adapt_kernel, kAdaptThreads, 0);
+  cudaError_t e = cudaFuncSetAttribute(adapt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kAdaptSmemBytes));
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adapt_kernel, kAdaptThreads, kAdaptSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int grid = num_sms * (per_sm < 2 ? per_sm : 2);
+  int want = 1;   // one CTA per SM: two co-resident CTAs with tiles halve each other's speed
+  if (const char* env = std::getenv("AUTOBYTE_ADAPT_PER_SM")) want = std::atoi(env) == 2 ? 2 : 1;
+  int grid = num_sms * (per_sm < want ? per_sm : want);
   *grid_used = grid;
   void* args[] = {const_cast<AdaptParams*>(&p)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(adapt_kernel), dim3(grid), dim3(kAdaptThreads), args, 0, s);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(adapt_kernel), dim3(grid), dim3(kAdaptThreads), args,
+                                     kAdaptSmemBytes, s);
 }
 
 }  // namespace ab
 
 #ifdef AB_STATS
+extern "C" int ab_debug_adapt_blocks(long long* out, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ab::g_adapt_blk, sizeof(long long) * 3 * (n < 1024 ? n : 1024)) == cudaSuccess;
+}
 extern "C" int ab_debug_adapt_phases(unsigned long long* out) {
   cudaDeviceSynchronize();
   int n = 0;

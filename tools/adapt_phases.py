@@ -25,3 +25,23 @@ prev = buf[0]
 for i in range(1, n):
     print(f"{names[i - 1] if i - 1 < len(names) else i:5s} {buf[i] - prev:8d} cycles")
     prev = buf[i]
+
+# per-block F2 work time and SM placement (who does the tiles, and do two busy CTAs share an SM)
+fb = lib.ab_debug_adapt_blocks
+fb.argtypes = [ctypes.c_void_p, ctypes.c_int]
+nb = 296
+blk = (ctypes.c_longlong * (3 * 1024))()
+fb(blk, 1024)
+import collections  # noqa: E402
+busy = collections.Counter()
+durs = []
+for b in range(nb):
+    sm, t0, t1 = blk[3 * b], blk[3 * b + 1], blk[3 * b + 2]
+    if t1 - t0 > 2000:
+        busy[sm] += 1
+        durs.append(t1 - t0)
+print("F2 busy blocks", len(durs), "distinct SMs", len(busy), "SMs with 2 busy", sum(1 for v in busy.values() if v > 1))
+if durs:
+    durs.sort()
+    print("F2 tile cycles min/med/max", durs[0], durs[len(durs) // 2], durs[-1])
+print("block->smid first 8:", [blk[3 * b] for b in range(8)])
