@@ -168,6 +168,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t ra
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive on a barrier of another CTA of the cluster with the default .release.cta semantics: the
+// producer side has already fenced what the consumer needs (tcgen05.fence::before_thread_sync for
+// TMEM reads, fence.proxy.async for shared-memory operands), and the cluster-scope release of
+// mbar_arrive_cluster costs ~1k cycles per arrive in K2's peer epilogue.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ uint32_t mbar_try_cluster(uint32_t addr, uint32_t parity) {
   uint32_t done;
   asm volatile(

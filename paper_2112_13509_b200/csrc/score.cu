@@ -94,7 +94,7 @@ struct ScoreCfg {
   static constexpr uint32_t IDESC = umma_idesc_bf16(128 * CG, NCH);
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t Y_COL = 256;          // TMEM column of activation buffer Y
-  static constexpr int EPI_ARRIVALS = CG == 2 ? 17 : 16;   // leader's 16 warps (+1 forwarded by the peer)
+  static constexpr int EPI_ARRIVALS = CG == 2 ? 32 : 16;   // 16 epilogue warps per CTA of the pair
   static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(CTA_STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
@@ -104,7 +104,6 @@ constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kScoreThreads = 64 + kEpiThreads;
 constexpr uint32_t kEpiBar = 1;
-constexpr uint32_t kPeerBar = 2;
 
 // One output chunk of one layer: NKB weight stages x 4 MMAs (K = 16 each) into accumulator d_t.
 // A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address). For the first
@@ -314,17 +313,15 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     const long long cshard = p.c_end - p.c_begin;
     const float* w0s = sAw + H;
     const float* w1s = sAw + 2 * H;
-    // the MMA issuer's barriers live in the leader CTA
-    // CG = 2: the leader's 8 epilogue warps arrive locally; the peer's 8 warps meet at a named
-    // barrier and one thread forwards a single cluster-scope arrive to the leader's barrier
+    // the MMA issuer's barriers live in the leader CTA: every epilogue warp of the pair counts in
+    // on its own (the leader's locally, the peer's with a remote arrive), so no warp waits for the
+    // other warps of its CTA
     const uint32_t dempty_c[2] = {mapa_shared(smem_u32(&dempty[0]), 0), mapa_shared(smem_u32(&dempty[1]), 0)};
     auto my_tile = [&](long long u) { return CG == 2 ? 2 * u + rank : u; };
-    auto signal = [&](uint64_t* bar, uint32_t cluster_addr) {   // called by the whole warp
-      if (CG == 2 && !leader) {
-        named_bar_sync(kPeerBar, kEpiThreads);
-        if (etid == 0) mbar_arrive_cluster(cluster_addr);
-      } else if (lane == 0) {
-        mbar_arrive(bar);
+    auto signal = [&](uint64_t* bar, uint32_t cluster_addr) {   // called by the whole warp after __syncwarp
+      if (lane == 0) {
+        if (CG == 2 && !leader) mbar_arrive_remote(cluster_addr);
+        else mbar_arrive(bar);
       }
     };
 
@@ -576,6 +573,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   }
 #ifdef AB_STATS
   // slots: 0-3 producer/MMA/epilogue waits, see tools/kstats.py
+  if (lane == 0 && rank == 1 && warp >= 2)   // the peer's epilogue: dfull wait, ld, compute+store, h1
+    for (int i = 0; i < 4; ++i) atomicAdd(&g_ab_stats[12 + i], st[i]);
   if (lane == 0 && rank == 0) {
     const long long total = clock64() - t_start;
     if (warp == 0) { atomicAdd(&g_ab_stats[0], st[0]); atomicAdd(&g_ab_stats[1], total); }

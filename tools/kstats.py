@@ -14,7 +14,8 @@ from paper_2112_13509_b200 import autobyte as ab  # noqa: E402
 from paper_2112_13509_b200.build import STATS_LIB  # noqa: E402
 
 NAMES = ["prod.wait_empty", "prod.total", "mma.wait_dempty", "mma.wait_full", "mma.wait_afull", "mma.total",
-         "epi.wait_dfull", "epi.ld", "epi.compute_store", "epi.build_h1", "epi.tile_reduce", "epi.total"]
+         "epi.wait_dfull", "epi.ld", "epi.compute_store", "epi.build_h1", "epi.tile_reduce", "epi.total",
+         "peer.epi.wait_dfull", "peer.epi.ld", "peer.epi.compute_store", "peer.epi.build_h1"]
 
 
 def main():
@@ -36,11 +37,11 @@ def main():
         net.argmax(jobs, grid)
         torch.cuda.synchronize()
         fn(buf, 1)
-        ctas = 148 // cg
-        epi_warps = 8 * ctas
+        ctas = 148 // cg            # leader CTAs (the stats slots 0-11 come from rank 0)
+        epi_warps = 16 * ctas
         print(f"--- L={L} H={H} J={J} cta_group={cg}  (per producer/MMA warp and per epilogue warp, Mcycles)")
         for i, n in enumerate(NAMES):
-            div = epi_warps if n.startswith("epi") else ctas
+            div = epi_warps if n.startswith(("epi", "peer")) else ctas
             print(f"{n:20s} {buf[i] / div / 1e6:9.3f}")
         net.close()
 
