@@ -366,9 +366,10 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   if ((e = c->wpack.ensure(wp ? wp : 1)) != cudaSuccess) return bail(e, "alloc wpack");
   if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
   // K2 variant: CTA pairs win when the head is deep and wide (4x512: 1158 vs 1133 TFLOP/s),
-  // single CTAs win on smaller heads (3x256: 726 vs 580); AUTOBYTE_CTA_GROUP=1|2 overrides.
+  // CTA pairs win from H = 256 up (C4 4x512: 1416 vs 1119 TFLOP/s; 3x256: 808 vs 757); single
+  // CTAs on the narrow heads (3x128: 320 vs 314). AUTOBYTE_CTA_GROUP=1|2 overrides.
   const char* cg = std::getenv("AUTOBYTE_CTA_GROUP");
-  c->cta_group = (desc->hidden_width == 512 && desc->hidden_layers >= 4) ? 2 : 1;
+  c->cta_group = desc->hidden_width >= 256 ? 2 : 1;
   if (cg && (cg[0] == '1' || cg[0] == '2')) c->cta_group = cg[0] - '0';
   if (!make_weight_tmap(&c->wmap, c->wpack.ptr, desc->hidden_width, desc->hidden_layers)) {
     autobyte_destroy(c);
