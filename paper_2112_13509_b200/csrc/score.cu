@@ -176,7 +176,9 @@ template <int H, int CG, int P3>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
   using C = ScoreCfg<H, CG, P3>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned base derived by pointer arithmetic on the __shared__ array (no integer round trip),
+  // so the compiler keeps every derived pointer in the shared window and emits LDS/STS, not generic loads
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = base;
   uint8_t* sStage = sA + C::A_BYTES;
   float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::CTA_STAGE_BYTES);   // [3][H]: a_j | W1c0 | W1c1
@@ -249,6 +251,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
               AB_TRACE(u == first + 2 * stride && lane == 0, 40, g, q * 16 + b);
               if (elect_one()) {
                 const int ti = (g * C::NQ + q) * C::NKB + b;
+#if defined(AB_EXP) && (AB_EXP & 2)
+                (void)ti;
+                if (leader || CG == 1) mbar_arrive(&full[s]);   // timing experiment: no weight traffic
+                if (false)
+#endif
                 if (CG == 2) {
                   if (leader) mbar_arrive_expect_tx(&full[s], C::STAGE_TX);   // both halves of KBS blocks
 #pragma unroll
@@ -287,7 +294,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
             uint64_t* aw = q == 0 ? afull : nullptr;
+#if defined(AB_EXP) && (AB_EXP & 8)
+            if (false)   // timing experiment: every layer reads A from TMEM
+#else
             if (src == 0)
+#endif
               mma_chunk<C, CG, false>(d_t, a_desc0, 0u, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
             else
               mma_chunk<C, CG, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
@@ -358,6 +369,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     };
     // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
     auto store_plane = [&](int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
+#if defined(AB_EXP) && (AB_EXP & 4)
+      if (dst == 0) return;   // timing experiment: no shared-memory activation stores
+#endif
       if (dst == 0) {  // buffer X: SW128 K-major, 16-byte chunk j of row r stored at chunk j ^ (r % 8)
         const uint32_t rowbase = smem_u32(sA) + plane * C::A_PLANE + (c0 >> 6) * 16384 + row * 128;
         const int j0 = (c0 & 63) >> 3;
@@ -393,6 +407,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     // layer-1 activations h1 = ReLU(a_j + W1c u_c) for the 128-column piece q (this warp's columns)
     auto build_piece = [&](int q, float up, float uc, int dst) {
       const int c0 = q * C::NCH + grp * C::QC;
+#if defined(AB_EXP) && (AB_EXP & 17)
+      if (true) { publish(dst, q); return; }   // timing experiment: no h1 build
+#endif
       if (C::NP == 1) {
         uint32_t pk[C::QC / 2];
 #pragma unroll
@@ -461,7 +478,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       for (int g = 0; g < G; ++g) {
         const int src = (b0 + g) & 1, dst = src ^ 1;
         const bool last = (g == G - 1);
-        const float* bias = g < C::G_CAP ? sBias + g * H : p.params + p.off.b[g + 2];
+        const float* gbias = p.params + p.off.b[g + 2];   // beyond G_CAP layers: read through L1
         if (last && has_next) {
           // the next tile's h1 is built one 128-column piece per chunk of this layer into the
           // buffer this layer does not read (free once chunk 0's MMAs, so every earlier MMA, are done)
@@ -471,6 +488,25 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           AB_ACC(st, 3, th);
         }
         for (int q = 0; q < C::NQ; ++q) {
+          // this warp's QC biases of chunk q, loaded before the accumulator wait so their latency
+          // hides behind it (they sat on the critical path of every chunk epilogue)
+          const int n0 = q * C::NCH + grp * C::QC;
+          float bq[C::QC];
+          if (g < C::G_CAP) {
+            const float4* s4 = reinterpret_cast<const float4*>(sBias + g * H + n0);
+#pragma unroll
+            for (int i = 0; i < C::QC / 4; ++i) {
+              const float4 v = s4[i];
+              bq[4 * i] = v.x; bq[4 * i + 1] = v.y; bq[4 * i + 2] = v.z; bq[4 * i + 3] = v.w;
+            }
+          } else {
+            const float4* g4 = reinterpret_cast<const float4*>(gbias + n0);
+#pragma unroll
+            for (int i = 0; i < C::QC / 4; ++i) {
+              const float4 v = __ldg(g4 + i);
+              bq[4 * i] = v.x; bq[4 * i + 1] = v.y; bq[4 * i + 2] = v.z; bq[4 * i + 3] = v.w;
+            }
+          }
           AB_T0(tw);
           mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
           AB_ACC(st, 0, tw);
@@ -488,48 +524,48 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
           AB_T0(tc);
           dq ^= 1;
+#if defined(AB_EXP) && (AB_EXP & 1)
+          if (false)   // timing experiment: no epilogue math or activation stores
+#endif
           {
-            const int n0 = q * C::NCH + grp * C::QC;
-            const float4* b4 = reinterpret_cast<const float4*>(bias + n0);
             if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
               float v[C::QC];
 #pragma unroll
-              for (int i = 0; i < C::QC / 4; ++i) {
-                const float4 bb = b4[i];
-                v[4 * i] = relu(__uint_as_float(acc[4 * i]) + bb.x);
-                v[4 * i + 1] = relu(__uint_as_float(acc[4 * i + 1]) + bb.y);
-                v[4 * i + 2] = relu(__uint_as_float(acc[4 * i + 2]) + bb.z);
-                v[4 * i + 3] = relu(__uint_as_float(acc[4 * i + 3]) + bb.w);
-              }
+              for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
               store_vals(dst, n0, v);
             } else if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
               uint32_t pk[C::QC / 2];
 #pragma unroll
-              for (int i = 0; i < C::QC / 4; ++i) {
-                const float4 bb = b4[i];
-                pk[2 * i] = pack_relu_bf16x2(__uint_as_float(acc[4 * i]) + bb.x, __uint_as_float(acc[4 * i + 1]) + bb.y);
-                pk[2 * i + 1] =
-                    pack_relu_bf16x2(__uint_as_float(acc[4 * i + 2]) + bb.z, __uint_as_float(acc[4 * i + 3]) + bb.w);
-              }
+              for (int i = 0; i < C::QC / 2; ++i)
+                pk[i] = pack_relu_bf16x2(__uint_as_float(acc[2 * i]) + bq[2 * i], __uint_as_float(acc[2 * i + 1]) + bq[2 * i + 1]);
               store_plane(dst, n0, pk, 0);
             } else {       // last hidden layer stays fp32: dot with the folded output row w_j (R#16)
               const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * C::WV + n0);
+              float d4[4] = {0.f, 0.f, 0.f, 0.f};   // four independent FMA chains
+#if defined(AB_EXP) && (AB_EXP & 32)
+              if (false)   // timing experiment: no last-layer dot
+#endif
 #pragma unroll
               for (int i = 0; i < C::QC / 4; ++i) {
-                const float4 bb = b4[i], ww = w4[i];
-                dot = fmaf(relu(__uint_as_float(acc[4 * i]) + bb.x), ww.x, dot);
-                dot = fmaf(relu(__uint_as_float(acc[4 * i + 1]) + bb.y), ww.y, dot);
-                dot = fmaf(relu(__uint_as_float(acc[4 * i + 2]) + bb.z), ww.z, dot);
-                dot = fmaf(relu(__uint_as_float(acc[4 * i + 3]) + bb.w), ww.w, dot);
+                const float4 ww = w4[i];
+                d4[0] = fmaf(relu(__uint_as_float(acc[4 * i]) + bq[4 * i]), ww.x, d4[0]);
+                d4[1] = fmaf(relu(__uint_as_float(acc[4 * i + 1]) + bq[4 * i + 1]), ww.y, d4[1]);
+                d4[2] = fmaf(relu(__uint_as_float(acc[4 * i + 2]) + bq[4 * i + 2]), ww.z, d4[2]);
+                d4[3] = fmaf(relu(__uint_as_float(acc[4 * i + 3]) + bq[4 * i + 3]), ww.w, d4[3]);
               }
+              dot += (d4[0] + d4[1]) + (d4[2] + d4[3]);
             }
           }
           if (!last) publish(dst, q);
           AB_ACC(st, 2, tc);
           AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
-          if (last && has_next) {
+          if (last && has_next && q == 0) {
+            // the next tile's h1, all pieces at once: once this warp has seen chunk 0 of the last
+            // layer, the issuer has consumed every afull phase of this tile, so publishing the
+            // next tile's phase cannot alias; building early takes h1 off the tile boundary
             AB_T0(th);
-            build_piece(q, up2, uc2, src ^ 1);
+#pragma unroll 1
+            for (int pq = 0; pq < C::NQ; ++pq) build_piece(pq, up2, uc2, src ^ 1);
             AB_ACC(st, 3, th);
             AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
           }
