@@ -228,3 +228,46 @@ def adapt(W, batch, lr: float, steps: int):
     if loss_before is None:
         _, loss_before, _ = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
     return Wn, loss_before
+
+
+def train(W, batch, steps: int, optimizer: str = "adam", lr: float = 1e-3, beta1: float = 0.9,
+          beta2: float = 0.999, eps: float = 1e-8, state=None):
+    """Offline training of the head on one minibatch (P:418 "Offline training online adapting";
+    P:415 the meta-network trained on collected runtime samples; optimiser R#18): `steps` updates
+    of every head parameter (encoder frozen, as in adapt) on the objective of R#12.
+      "sgd":  theta <- theta - lr * g
+      "adam": t <- t + 1; m <- b1 m + (1 - b1) g; v <- b2 v + (1 - b2) g^2;
+              theta <- theta - lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+    `state` = {"t": int, "m": {name: array}, "v": {name: array}} carries the Adam moments across
+    calls (None = fresh, all zero). Returns (new weights, new state, [mean Eq.2 norm before each
+    step])."""
+    Wn = {k: _f64(v).copy() for k, v in W.items()}
+    names = HEAD_PARAMS(Wn)
+    if state is None:
+        state = {"t": 0, "m": {k: np.zeros_like(Wn[k]) for k in names}, "v": {k: np.zeros_like(Wn[k]) for k in names}}
+    else:
+        state = {"t": int(state["t"]), "m": {k: _f64(a).copy() for k, a in state["m"].items()},
+                 "v": {k: _f64(a).copy() for k, a in state["v"].items()}}
+    jobs = batch.jobs
+    X = encode_jobs(Wn, jobs)
+    U = np.stack([encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(jobs.J)])
+    Z_in = np.concatenate([X, U], axis=1)
+    losses = []
+    for _ in range(int(steps)):
+        _, norm_mean, g = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
+        losses.append(norm_mean)
+        if optimizer == "sgd":
+            for k in names:
+                Wn[k] = Wn[k] - lr * g[k]
+        elif optimizer == "adam":
+            state["t"] += 1
+            t = state["t"]
+            for k in names:
+                state["m"][k] = beta1 * state["m"][k] + (1.0 - beta1) * g[k]
+                state["v"][k] = beta2 * state["v"][k] + (1.0 - beta2) * g[k] * g[k]
+                m_hat = state["m"][k] / (1.0 - beta1 ** t)
+                v_hat = state["v"][k] / (1.0 - beta2 ** t)
+                Wn[k] = Wn[k] - lr * m_hat / (np.sqrt(v_hat) + eps)
+        else:
+            raise ValueError(f"unknown optimizer {optimizer!r}")
+    return Wn, state, losses

@@ -296,3 +296,83 @@ def test_trigger_spec_examples():
     assert T([5], [2.0], [3], [1.0], None) == [oracle.RECONFIGURE]        # no observation: gain only
     assert T([3], [2.0], [3], [1.0], None) == [oracle.KEEP]               # best is current
     assert T([-1], [float("nan")], [3], [1.0], None) == [oracle.KEEP]     # all-NaN job
+
+
+# ---------------------------------------------------------------- offline training (NEXT 2)
+def _torch_head_loss(P, Z, V_bar, n, L):
+    h = torch.tensor(Z)
+    for k in range(1, L + 1):
+        h = torch.relu(h @ P[f"W{k}"].T + P[f"b{k}"])
+    V = h @ P["W_o"].T + P["b_o"]
+    mask = torch.tensor((np.arange(16)[None, :] < np.asarray(n)[:, None]).astype(np.float64))
+    r = (V - torch.tensor(np.asarray(V_bar, np.float64))) * mask
+    return 0.5 * (r * r).sum() / Z.shape[0]
+
+
+@pytest.mark.parametrize("L,steps", [(1, 1), (2, 3), (4, 5)])
+def test_train_adam_matches_torch_optim_adam(L, steps):
+    """oracle.train('adam') == torch.optim.Adam (float64, autograd gradients) on the head
+    parameters, over several steps and across two calls that carry the optimiser state."""
+    desc = synth.NetDesc(L, 12)
+    W = synth.make_weights(desc, seed=L)
+    batch = _tiny_batch(20 + L, J=9)
+    X = oracle.encode_jobs(W, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    Z = np.concatenate([X, U], 1)
+    names = oracle.HEAD_PARAMS(W)
+    P = {k: torch.tensor(W[k].astype(np.float64), requires_grad=True) for k in names}
+    opt = torch.optim.Adam(list(P.values()), lr=3e-3, betas=(0.8, 0.99), eps=1e-7)
+    for _ in range(2 * steps):
+        opt.zero_grad()
+        _torch_head_loss(P, Z, batch.V_bar, batch.jobs.n, L).backward()
+        opt.step()
+    W1, st, _ = oracle.train(W, batch, steps, "adam", lr=3e-3, beta1=0.8, beta2=0.99, eps=1e-7)
+    W2, st2, _ = oracle.train(W1, batch, steps, "adam", lr=3e-3, beta1=0.8, beta2=0.99, eps=1e-7, state=st)
+    assert st2["t"] == 2 * steps
+    for k in names:
+        np.testing.assert_allclose(W2[k], P[k].detach().numpy(), rtol=1e-10, atol=1e-13, err_msg=k)
+
+
+def test_train_adam_first_step_closed_form():
+    """At t = 1 the bias-corrected moments are g and g^2, so every head parameter moves by
+    exactly -lr * g / (|g| + eps) (Kingma & Ba's first step: ~lr * sign(g))."""
+    desc = synth.NetDesc(2, 10)
+    W = synth.make_weights(desc, seed=5)
+    batch = _tiny_batch(31, J=5)
+    X = oracle.encode_jobs(W, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    _, _, g = oracle.head_loss_and_grad(W, np.concatenate([X, U], 1), batch.V_bar, batch.jobs.n)
+    lr, eps = 1e-2, 1e-8
+    Wn, st, losses = oracle.train(W, batch, 1, "adam", lr=lr, eps=eps)
+    for k in oracle.HEAD_PARAMS(W):
+        np.testing.assert_allclose(Wn[k] - W[k].astype(np.float64), -lr * g[k] / (np.abs(g[k]) + eps),
+                                   rtol=1e-9, atol=1e-15, err_msg=k)
+    assert st["t"] == 1 and len(losses) == 1
+
+
+def test_train_sgd_equals_adapt_and_reports_per_step_losses():
+    desc = synth.NetDesc(3, 16)
+    W = synth.make_weights(desc, seed=7)
+    batch = _tiny_batch(41, J=8)
+    Wa, loss_a = oracle.adapt(W, batch, lr=0.02, steps=3)
+    Wt, _, losses = oracle.train(W, batch, 3, "sgd", lr=0.02)
+    for k in W:
+        assert np.array_equal(Wa[k], Wt[k]), k
+    assert losses[0] == loss_a and len(losses) == 3
+
+
+def test_train_adam_learns_a_teacher():
+    """A student head fitted with Adam to a teacher of the same architecture (labels =
+    teacher speeds at the samples' configurations) drives the Eq. 2 loss down by >5x."""
+    desc = synth.NetDesc(2, 32)
+    W = synth.make_weights(desc, seed=1)
+    teacher = synth.make_weights(desc, seed=2)
+    for k in ["E_m", "E_arc", "W_e", "b_e", "lstm1_Wx", "lstm1_Wh", "lstm1_b", "lstm2_Wx", "lstm2_Wh", "lstm2_b"]:
+        teacher[k] = W[k]                      # same frozen encoder
+    batch = _tiny_batch(51, J=32)
+    X = oracle.encode_jobs(teacher, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    Vt = oracle.head_forward(teacher, np.concatenate([X, U], 1))
+    batch.V_bar = (Vt * (np.arange(16)[None, :] < batch.jobs.n[:, None])).astype(np.float32)
+    _, _, losses = oracle.train(W, batch, 300, "adam", lr=1e-2)
+    assert losses[-1] < losses[0] / 5, (losses[0], losses[-1])
