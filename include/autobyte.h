@@ -186,6 +186,35 @@ autobyte_status autobyte_adapt(autobyte_ctx* ctx, const autobyte_job_stats* samp
                                const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,
                                float lr, int32_t steps, float* loss_before);
 
+/* Offline training of the head ("offline training, online adapting"; R#18;
+ * SURVEY §8(f) NEXT 2): `steps` optimiser steps on one minibatch, same inputs, objective,
+ * frozen encoder and head scope as autobyte_adapt.
+ *   AB_OPT_SGD:  theta <- theta - lr * g
+ *   AB_OPT_ADAM: t <- t + 1; m <- beta1 m + (1 - beta1) g; v <- beta2 v + (1 - beta2) g^2;
+ *                theta <- theta - (lr / (1 - beta1^t)) * m / (sqrt(v) / sqrt(1 - beta2^t) + eps)
+ * The Adam moments m, v (fp32, one per head parameter) and the step count t live in the
+ * context and carry across calls (autobyte_reset_optimizer zeroes them); autobyte_adapt does not
+ * touch them. losses (nullable, DEVICE [steps] fp32) receives, per step, the mean Eq. 2 norm
+ * (1/B) sum_b ||mask_b (V_hat_b - V_bar_b)||_2 before that step's update. Errors: NULL opt or
+ * input pointer, steps < 0, non-finite lr, beta outside [0, 1) or eps <= 0 -> AB_E_INVALID with
+ * no launch. Deterministic (fixed summation order); the bf16 shadows are refreshed in stream
+ * order. */
+typedef enum { AB_OPT_SGD = 0, AB_OPT_ADAM = 1 } autobyte_opt_kind;
+typedef struct {
+  int32_t kind;    /* autobyte_opt_kind */
+  float lr;
+  float beta1;     /* Adam only; typical 0.9 */
+  float beta2;     /* Adam only; typical 0.999 */
+  float eps;       /* Adam only; typical 1e-8 */
+} autobyte_optimizer;
+autobyte_status autobyte_train(autobyte_ctx* ctx, const autobyte_job_stats* samples,
+                               const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,
+                               const autobyte_optimizer* opt, int32_t steps, float* losses);
+/* Zero the Adam moments and step count (asynchronous, stream-ordered). */
+autobyte_status autobyte_reset_optimizer(autobyte_ctx* ctx);
+/* Adam step count t so far (host value; no synchronisation). */
+int64_t autobyte_optimizer_step(const autobyte_ctx* ctx);
+
 /* Optimization Trigger, per job j, DEVICE pointers, [J] each:
  *   1. drift first: v_observed[j] > 0 and |cur_score - v_observed| / v_observed > drift
  *      -> action 2 (adapt, then decide again)

@@ -47,6 +47,15 @@ class Grid(ctypes.Structure):
                 ("shard_begin", ctypes.c_int64), ("shard_end", ctypes.c_int64)]
 
 
+class Optimizer(ctypes.Structure):
+    """autobyte_optimizer: kind 0 = SGD, 1 = Adam (R#18)."""
+    _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
+
+
+OPT_SGD, OPT_ADAM = 0, 1
+
+
 class Profile(ctypes.Structure):
     _fields_ = [("encode_ms", ctypes.c_double), ("encode_launches", ctypes.c_int64),
                 ("score_ms", ctypes.c_double), ("score_launches", ctypes.c_int64),
@@ -64,7 +73,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_validate_blob", "autobyte_create", "autobyte_destroy", "autobyte_last_error",
            "autobyte_synchronize", "autobyte_get_unique_id", "autobyte_attach_comm", "autobyte_encode",
            "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
-           "autobyte_adapt_host",
+           "autobyte_adapt_host", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile"]
 
 _lib = None
@@ -100,6 +109,9 @@ def load_library(path: Optional[str] = None):
         "autobyte_trigger": (I32, [P, I32, P, P, P, P, P, F32, F32, P]),
         "autobyte_argmax_host": (I32, [P, P, P, P, P, P, P]),
         "autobyte_adapt_host": (I32, [P, P, P, P, P, F32, I32, P]),
+        "autobyte_train": (I32, [P, P, P, P, P, P, I32, P]),
+        "autobyte_reset_optimizer": (I32, [P]),
+        "autobyte_optimizer_step": (I64, [P]),
         "autobyte_get_weights": (I32, [P, P, SZ]),
         "autobyte_set_profiling": (I32, [P, ctypes.c_int]),
         "autobyte_get_profile": (I32, [P, P]),
@@ -307,6 +319,27 @@ class AutoByte:
                                             V_bar.data_ptr(), float(lr), int(steps),
                                             loss.data_ptr() if loss is not None else None), "adapt")
         return loss
+
+    def train(self, samples: DeviceJobs, S_p, S_c, V_bar, steps: int, optimizer: str = "adam", lr: float = 1e-3,
+              beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, want_losses: bool = True):
+        """Offline training of the head on one minibatch (autobyte_train): `steps` SGD or Adam
+        updates; returns the per-step mean Eq. 2 norms before each update (device tensor)."""
+        import torch
+        kind = {"sgd": OPT_SGD, "adam": OPT_ADAM}[optimizer]
+        opt = Optimizer(kind, lr, beta1, beta2, eps)
+        losses = torch.empty(max(int(steps), 1), dtype=torch.float32, device=self.torch_device) if want_losses else None
+        js = samples.struct()
+        self._check(self.lib.autobyte_train(self.ctx, ctypes.byref(js), S_p.data_ptr(), S_c.data_ptr(),
+                                            V_bar.data_ptr(), ctypes.byref(opt), int(steps),
+                                            losses.data_ptr() if losses is not None else None), "train")
+        return losses[:int(steps)] if losses is not None else None
+
+    def reset_optimizer(self):
+        self._check(self.lib.autobyte_reset_optimizer(self.ctx), "reset_optimizer")
+
+    @property
+    def optimizer_step(self) -> int:
+        return int(self.lib.autobyte_optimizer_step(self.ctx))
 
     def trigger(self, best_idx, best_score, cur_idx, cur_score, v_observed=None, gain: float = 0.05,
                 drift: float = 0.10):

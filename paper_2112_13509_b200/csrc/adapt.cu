@@ -8,7 +8,7 @@
 //   BO    dW_o = R^T H_L, db_o = colsum R, D_L = (R W_o) * [H_L > 0]
 //   Bk    dW_k = D_k^T H_{k-1}, db_k = colsum D_k, D_{k-1} = (D_k W_k) * [H_{k-1} > 0]  (pre-update W_k)
 //         + SGD of the layer above (its gradient is complete and no later phase reads it)
-//   SGD   W1, b1 (after B1)
+//   SGD   W1, b1 (after B1)   (SGD or Adam, see update_range)
 // Every output element is produced by exactly one thread with a fixed summation order, so the
 // update is deterministic and replicas on different GPUs stay bit-identical without traffic.
 // The work is ~3x a B-row forward (5 GFLOP at B=1024, 4x512): latency-bound, << 1% of a C5 step.
@@ -283,14 +283,36 @@ __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, cons
   __syncthreads();   // sW aliases the GEMM ring
 }
 
-// theta[i] -= lr * (sum of the kSplitK gradient partials, fixed order) over [begin, end).
-__device__ void sgd_range(float* P, const float* Gr, long long total, long long begin, long long end, float lr) {
+// One optimiser update over parameters [begin, end); g = the kSplitK gradient partials summed in
+// fixed order. SGD: theta -= lr g. Adam (R#18, torch semantics): m = b1 m + (1-b1) g,
+// v = b2 v + (1-b2) g^2, theta -= (lr / (1 - b1^t)) m / (sqrt(v) / sqrt(1 - b2^t) + eps).
+__device__ void update_range(const AdaptParams& p, long long begin, long long end, int step) {
+  float* P = p.params;
+  const float* Gr = p.grads;
+  const long long total = p.off.total;
   const long long gtid = (long long)blockIdx.x * kAdaptThreads + threadIdx.x, gthreads = (long long)gridDim.x * kAdaptThreads;
-  for (long long i = begin + gtid; i < end; i += gthreads) {
-    float gsum = Gr[i];
+  if (p.opt == AB_OPT_ADAM) {
+    const double t = static_cast<double>(p.t0 + step + 1);
+    const float step_size = static_cast<float>(p.lr / (1.0 - pow(static_cast<double>(p.beta1), t)));
+    const float sqrt_bc2 = static_cast<float>(sqrt(1.0 - pow(static_cast<double>(p.beta2), t)));
+    const float b1 = p.beta1, b2 = p.beta2, c1 = 1.0f - p.beta1, c2 = 1.0f - p.beta2;
+    for (long long i = begin + gtid; i < end; i += gthreads) {
+      float g = Gr[i];
 #pragma unroll
-    for (int sk = 1; sk < kSplitK; ++sk) gsum += Gr[sk * total + i];
-    P[i] = P[i] - lr * gsum;
+      for (int sk = 1; sk < kSplitK; ++sk) g += Gr[sk * total + i];
+      const float m = fmaf(b1, p.m[i], c1 * g);
+      const float v = fmaf(b2, p.v[i], c2 * (g * g));
+      p.m[i] = m;
+      p.v[i] = v;
+      P[i] = P[i] - step_size * (m / (sqrtf(v) / sqrt_bc2 + p.eps));
+    }
+  } else {
+    for (long long i = begin + gtid; i < end; i += gthreads) {
+      float g = Gr[i];
+#pragma unroll
+      for (int sk = 1; sk < kSplitK; ++sk) g += Gr[sk * total + i];
+      P[i] = P[i] - p.lr * g;
+    }
   }
 }
 
@@ -350,7 +372,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
     }
     out_rows(Hk(L), P + p.off.W_o, P + p.off.b_o, p.v_obs, p.n, 1.0f / static_cast<float>(B), B, H, R, ring);
     grid_sync(p.barrier, gen);
-    if (step == 0 && p.loss_before && blockIdx.x == 0) {
+    if (((step == 0 && p.loss_before) || (p.losses && !fwd_only)) && blockIdx.x == 0) {
       // mean over b of the Eq. 2 norm ||mask (V_hat - V_bar)||_2; R holds residual / B
       __shared__ float s_norm[kAdaptThreads];
       float acc = 0.f;
@@ -364,7 +386,9 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       if (threadIdx.x == 0) {
         float tot = 0.f;
         for (int i = 0; i < kAdaptThreads; ++i) tot += s_norm[i];
-        *p.loss_before = tot / static_cast<float>(B);
+        const float lb = tot / static_cast<float>(B);
+        if (step == 0 && p.loss_before) *p.loss_before = lb;
+        if (p.losses && !fwd_only) p.losses[step] = lb;
       }
     }
     if (fwd_only) break;
@@ -400,12 +424,12 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
       // SGD of the layer above, whose gradient partials completed in the previous phase and whose
       // weights no phase reads any more this step (W_o after BO; W_{k+1} after B_{k+1})
-      if (k == L) sgd_range(P, Gr, p.off.total, p.off.W_o, p.off.total, p.lr);
-      else sgd_range(P, Gr, p.off.total, p.off.W[k + 1], p.off.b[k + 1] + H, p.lr);
+      if (k == L) update_range(p, p.off.W_o, p.off.total, step);
+      else update_range(p, p.off.W[k + 1], p.off.b[k + 1] + H, step);
       grid_sync(p.barrier, gen);
     }
     // ---------------- SGD of layer 1 (W1, b1); the kernel exit orders it after the last step
-    sgd_range(P, Gr, p.off.total, p.off.W[1], p.off.b[1] + H, p.lr);
+    update_range(p, p.off.W[1], p.off.b[1] + H, step);
     if (step + 1 < nsteps) grid_sync(p.barrier, gen);
   }
 }

@@ -78,6 +78,8 @@ struct autobyte_ctx {
   DevBuf<int> flag;              // AUTOBYTE_CHECK device flag
   // per-call workspace
   DevBuf<float> jobvec, x, adapt_ws, loss_tmp;
+  DevBuf<float> opt_m, opt_v;        // Adam moments (autobyte_train), blob layout
+  long long opt_t = 0;               // Adam step count
   DevBuf<float2> u;                  // [shard] candidate encodings (K0)
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
   // staging for the *_host entry points
@@ -398,6 +400,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
   c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
+  c->opt_m.release(); c->opt_v.release();
   c->loss_tmp.release(); c->keys.release();
   c->sT.release(); c->sBd.release(); c->sBu.release(); c->sSc.release(); c->sV.release();
   c->rScore.release(); c->rCur.release();
@@ -497,6 +500,47 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
   return AB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// K1a on the samples (sharded across ranks) + K4 + re-pack: the body of adapt and train.
+autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
+                                const float* sc_mult, const float* v_obs, int opt, float lr, float beta1,
+                                float beta2, float eps, int32_t steps, float* loss_before, float* losses) {
+  const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
+  AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
+  EncodeParams ep{};
+  autobyte_status s = run_lstm(c, samples, &ep);
+  if (s != AB_OK) return s;
+  AdaptParams ap{};
+  ap.B = B; ap.H = H; ap.L = L; ap.steps = steps; ap.lr = lr;
+  ap.x = c->x.ptr; ap.S_p = reinterpret_cast<const long long*>(sp_bytes); ap.S_c = sc_mult; ap.v_obs = v_obs;
+  ap.n = samples->n_workers;
+  ap.params = c->params.ptr; ap.off = c->off; ap.ws = c->adapt_ws.ptr; ap.grads = c->grads.ptr;
+  ap.loss_before = loss_before; ap.losses = losses; ap.barrier = c->barrier.ptr;
+  ap.opt = opt; ap.beta1 = beta1; ap.beta2 = beta2; ap.eps = eps;
+  if (opt == AB_OPT_ADAM) {
+    if (!c->opt_m.ptr) {   // moments start at zero (blob layout; only the head part is used)
+      AB_CUDA(c, c->opt_m.ensure(c->off.total));
+      AB_CUDA(c, c->opt_v.ensure(c->off.total));
+      AB_CUDA(c, cudaMemsetAsync(c->opt_m.ptr, 0, c->off.total * sizeof(float), c->stream));
+      AB_CUDA(c, cudaMemsetAsync(c->opt_v.ptr, 0, c->off.total * sizeof(float), c->stream));
+    }
+    ap.m = c->opt_m.ptr; ap.v = c->opt_v.ptr; ap.t0 = c->opt_t;
+  }
+  int grid_used = 0;
+  AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
+  if (opt == AB_OPT_ADAM) c->opt_t += steps;
+  if (steps > 0)
+    AB_CUDA(c, timed(c, K_PACK, [&] {
+              return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
+            }));
+  return AB_OK;
+}
+}  // namespace
+
+extern "C" {
+
 autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                const float* sc_mult, const float* v_obs, float lr, int32_t steps,
                                float* loss_before) {
@@ -509,24 +553,43 @@ autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* sample
   DeviceGuard guard(c->device);
   if ((s = device_checks(c, samples, nullptr)) != AB_OK) return s;
   if (steps == 0 && !loss_before) return AB_OK;
-  const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
-  AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
-  EncodeParams ep{};
-  if ((s = run_lstm(c, samples, &ep)) != AB_OK) return s;
-  AdaptParams ap{};
-  ap.B = B; ap.H = H; ap.L = L; ap.steps = steps; ap.lr = lr;
-  ap.x = c->x.ptr; ap.S_p = reinterpret_cast<const long long*>(sp_bytes); ap.S_c = sc_mult; ap.v_obs = v_obs;
-  ap.n = samples->n_workers;
-  ap.params = c->params.ptr; ap.off = c->off; ap.ws = c->adapt_ws.ptr; ap.grads = c->grads.ptr;
-  ap.loss_before = loss_before; ap.barrier = c->barrier.ptr;
-  int grid_used = 0;
-  AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
-  if (steps > 0)
-    AB_CUDA(c, timed(c, K_PACK, [&] {
-              return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
-            }));
+  return run_head_update(c, samples, sp_bytes, sc_mult, v_obs, AB_OPT_SGD, lr, 0.f, 0.f, 0.f, steps, loss_before,
+                         nullptr);
+}
+
+autobyte_status autobyte_train(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
+                               const float* sc_mult, const float* v_obs, const autobyte_optimizer* opt,
+                               int32_t steps, float* losses) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, samples);
+  if (s != AB_OK) return s;
+  if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "train input pointer is NULL");
+  if (!opt) return fail(c, AB_E_INVALID, "optimizer is NULL");
+  if (opt->kind != AB_OPT_SGD && opt->kind != AB_OPT_ADAM) return fail(c, AB_E_INVALID, "unknown optimizer kind");
+  if (steps < 0) return fail(c, AB_E_INVALID, "steps must be >= 0");
+  if (!std::isfinite(opt->lr)) return fail(c, AB_E_INVALID, "lr must be finite");
+  if (opt->kind == AB_OPT_ADAM && !(opt->beta1 >= 0.f && opt->beta1 < 1.f && opt->beta2 >= 0.f && opt->beta2 < 1.f &&
+                                    opt->eps > 0.f && std::isfinite(opt->eps)))
+    return fail(c, AB_E_INVALID, "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, samples, nullptr)) != AB_OK) return s;
+  if (steps == 0) return AB_OK;
+  return run_head_update(c, samples, sp_bytes, sc_mult, v_obs, opt->kind, opt->lr, opt->beta1, opt->beta2, opt->eps,
+                         steps, nullptr, losses);
+}
+
+autobyte_status autobyte_reset_optimizer(autobyte_ctx* c) {
+  if (!c) return AB_E_INVALID;
+  DeviceGuard guard(c->device);
+  if (c->opt_m.ptr) {
+    AB_CUDA(c, cudaMemsetAsync(c->opt_m.ptr, 0, c->off.total * sizeof(float), c->stream));
+    AB_CUDA(c, cudaMemsetAsync(c->opt_v.ptr, 0, c->off.total * sizeof(float), c->stream));
+  }
+  c->opt_t = 0;
   return AB_OK;
 }
+
+int64_t autobyte_optimizer_step(const autobyte_ctx* c) { return c ? c->opt_t : -1; }
 
 autobyte_status autobyte_trigger(autobyte_ctx* c, int32_t J, const int32_t* best_idx, const float* best_score,
                                  const int32_t* cur_idx, const float* cur_score, const float* v_observed,

@@ -83,7 +83,14 @@ struct AdaptParams {
   float* ws;               // workspace (see adapt.cu)
   float* grads;            // [head params] gradient buffer
   float* loss_before;      // [1] or null
+  float* losses;           // [steps] or null: mean Eq. 2 norm before each step
   unsigned int* barrier;   // grid barrier counter (2 words)
+  // optimiser (autobyte_train; autobyte_adapt = SGD with no state)
+  int opt;                 // AB_OPT_SGD / AB_OPT_ADAM
+  float beta1, beta2, eps;
+  long long t0;            // Adam steps taken before this launch
+  float* m;                // Adam first moments (blob layout, head part used) or null
+  float* v;                // Adam second moments
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)

@@ -360,6 +360,88 @@ def test_adapt_is_deterministic():
     assert outs[0] == outs[1]
 
 
+# ------------------------------------------------------------------------------------- NEXT 2 train
+def _dev_batch(batch):
+    return (dev(batch.jobs), torch.as_tensor(batch.S_p, device="cuda"), torch.as_tensor(batch.S_c, device="cuda"),
+            torch.as_tensor(batch.V_bar, device="cuda"))
+
+
+def _check_update(W0, W_ora, W_gpu, tol):
+    for k in oracle.HEAD_PARAMS(W_ora):
+        d_ora = W_ora[k] - W0[k].astype(np.float64)
+        d_gpu = W_gpu[k].astype(np.float64) - W0[k].astype(np.float64)
+        rel = np.linalg.norm(d_gpu - d_ora) / max(np.linalg.norm(d_ora), 1e-30)
+        assert rel <= tol, (k, rel)
+
+
+@pytest.mark.parametrize("L,H,B,steps", [(2, 64, 40, 2), (3, 256, 256, 2), (4, 512, 100, 3)])
+def test_train_adam_matches_oracle(L, H, B, steps):
+    """autobyte_train (Adam) over two calls that carry the moments == oracle.train with state:
+    per-tensor update within 2e-3 (Adam normalises every coordinate, so the fp32 vs float64
+    difference of a near-zero gradient shows up at ~lr scale), per-step losses within 1e-3
+    (1e-4 before the first update)."""
+    W = synth.make_weights(synth.NetDesc(L, H), seed=3 * L + H)
+    batch = synth.make_adapt_batch(synth.small_fleet(B, 70 + L), synth.log_grid(64, 64), 8)
+    kw = dict(lr=2e-3 if H < 512 else 3e-4, beta1=0.9, beta2=0.99, eps=1e-6)
+    W1, st, l1 = oracle.train(W, batch, steps, "adam", **kw)
+    W2, st2, l2 = oracle.train(W1, batch, steps, "adam", state=st, **kw)
+    net = make(L, H, W)
+    db = _dev_batch(batch)
+    g1 = net.train(*db, steps, "adam", **kw).cpu().numpy()
+    g2 = net.train(*db, steps, "adam", **kw).cpu().numpy()
+    assert net.optimizer_step == 2 * steps
+    got, want = np.concatenate([g1, g2]), np.array(l1 + l2)
+    assert abs(got[0] - want[0]) <= 1e-4 * want[0]          # before any update: the forward bar
+    np.testing.assert_allclose(got, want, rtol=1e-3)          # later steps inherit update rounding
+    _check_update(W, W2, net.get_weights(), 2e-3)
+    # scoring sees the trained weights
+    g = synth.log_grid(9, 7)
+    check_scores(gpu_scores(net, batch.jobs.subset(np.arange(3)), g),
+                 oracle.score_matrix(W2, batch.jobs.subset(np.arange(3)), g), RTOL)
+
+
+def test_train_sgd_is_adapt_and_reset_restarts_adam():
+    L, H = 3, 128
+    W = synth.make_weights(synth.NetDesc(L, H), seed=11)
+    batch = synth.make_adapt_batch(synth.small_fleet(48, 12), synth.log_grid(16, 16), 9)
+    a, b = make(L, H, W), make(L, H, W)
+    db = _dev_batch(batch)
+    a.adapt(*db, 1e-2, 2)
+    b.train(*db, 2, "sgd", lr=1e-2)
+    torch.cuda.synchronize()
+    assert a.get_weights_blob() == b.get_weights_blob()
+    assert b.optimizer_step == 0
+    # Adam from a reset state == Adam on a fresh context
+    c, d = make(L, H, W), make(L, H, W)
+    c.train(*db, 3, "adam", lr=1e-3)
+    c.reset_optimizer()
+    assert c.optimizer_step == 0
+    Wc = c.get_weights()
+    d2 = make(L, H, {k: v.copy() for k, v in Wc.items()})
+    c.train(*db, 2, "adam", lr=1e-3)
+    d2.train(*db, 2, "adam", lr=1e-3)
+    torch.cuda.synchronize()
+    assert c.get_weights_blob() == d2.get_weights_blob()
+
+
+def test_train_adam_learns_a_teacher_on_gpu():
+    """Many Adam steps on teacher labels drive the device-reported loss down (descent at scale)."""
+    L, H = 3, 256
+    desc = synth.NetDesc(L, H)
+    W = synth.make_weights(desc, seed=1)
+    teacher = synth.make_weights(desc, seed=2)
+    for k in ["E_m", "E_arc", "W_e", "b_e", "lstm1_Wx", "lstm1_Wh", "lstm1_b", "lstm2_Wx", "lstm2_Wh", "lstm2_b"]:
+        teacher[k] = W[k]
+    batch = synth.make_adapt_batch(synth.small_fleet(512, 5), synth.log_grid(64, 64), 6)
+    X = oracle.encode_jobs(teacher, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    Vt = oracle.head_forward(teacher, np.concatenate([X, U], 1))
+    batch.V_bar = (Vt * (np.arange(16)[None, :] < batch.jobs.n[:, None])).astype(np.float32)
+    net = make(L, H, W)
+    losses = net.train(*_dev_batch(batch), 200, "adam", lr=1e-3).cpu().numpy()
+    assert np.all(np.isfinite(losses)) and losses[-1] < losses[0] / 3, (losses[0], losses[-1])
+
+
 def test_host_entry_point_matches_device():
     c = synth.config("C3")
     W = synth.make_weights(c.desc)
