@@ -39,14 +39,17 @@ struct Gemm {
   __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
 };
 
-constexpr int kStages = 4;   // cp.async pipeline depth of the GEMM tiles (prefetch distance kStages - 1)
-// One operand slice in shared memory, in the orientation of its global layout so every 16-byte
-// cp.async copies a contiguous vector: K-contiguous [64][kTK + 4] or MN-contiguous [kTK][64 + 8].
-// Both paddings make the m16n8k8 fragment reads (lanes g = lane/4 along M|N, t = lane%4 along K)
-// hit 32 distinct banks.
+constexpr int kStages = 4;   // cp.async pipeline depth of the raw operand slices (prefetch distance kStages - 1)
+// Raw operand slices land in shared memory in the orientation of their global layout so every
+// 16-byte cp.async copies a contiguous vector: K-contiguous [64][kTK + 4] or MN-contiguous
+// [kTK][64 + 8]. A conversion pass then splits every element once per CTA into tf32 big / small
+// planes stored K-contiguous [64][kTK + 4] (transposing MN-contiguous slices), from which the
+// warps read whole m16n8k8 fragments with ldmatrix (a tf32 element is a pair of b16 lanes).
+// Row stride kTK + 4 = 36 floats puts the 8 rows of an ldmatrix in 8 distinct 16-byte bank groups.
 constexpr int kSK = kTK + 4, kSM = kTM + 8;
 constexpr int kSliceFloats = (kTM * kSK > kTK * kSM) ? kTM * kSK : kTK * kSM;
-constexpr size_t kAdaptSmemBytes = sizeof(float) * kStages * 2 * kSliceFloats;
+constexpr int kPlaneFloats = kTM * kSK;                  // one split plane [64][36]
+constexpr size_t kAdaptSmemBytes = sizeof(float) * (kStages * 2 * kSliceFloats + 4 * kPlaneFloats);
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
@@ -59,16 +62,24 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // x = big + small with both parts tf32 (10-bit mantissa each): the 3xTF32 product
 // big*big + big*small + small*big carries ~fp32 accuracy (the dropped small*small is ~2^-22 relative).
-__device__ __forceinline__ void split_tf32(float x, uint32_t& big, uint32_t& small) {
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(big) : "f"(x));
-  const float r = x - __uint_as_float(big);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(small) : "f"(r));
+__device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
+  uint32_t b, sm;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
+  const float r = x - __uint_as_float(b);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(sm) : "f"(r));
+  big = __uint_as_float(b);
+  small = __uint_as_float(sm);
 }
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
                "{%0,%1,%2,%3};"
                : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
 }
 
 // Stage one 64 x kTK slice of an operand: X(mn, k) = base[mn*lmn + k*lk] for mn in [mn0, mn0+64),
@@ -89,14 +100,42 @@ __device__ __forceinline__ void stage_slice(float* dst, const float* base, long 
     }
   }
 }
-__device__ __forceinline__ float slice_at(const float* s, bool kcontig, int mn, int k) {
-  return kcontig ? s[mn * kSK + k] : s[k * kSM + mn];
+
+// Split one raw slice into K-contiguous big / small planes (8 elements per thread). K-contiguous
+// raw: thread -> (mn, 8 consecutive k), LDS.128 / STS.128. MN-contiguous raw: warp w -> k in
+// [4w, 4w+4), lane -> (k = 4w + lane/8, mn = lane%8 + 8j): conflict-free on both the raw read
+// (stride 72) and the transposed plane write (stride 36).
+__device__ __forceinline__ void split_slice(const float* raw, bool kcontig, float* big, float* small) {
+  const int tid = threadIdx.x;
+  if (kcontig) {
+    const int mn = tid >> 2, k0 = (tid & 3) * 8;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 v = *reinterpret_cast<const float4*>(raw + mn * kSK + k0 + 4 * h);
+      float4 b, sm;
+      split_tf32(v.x, b.x, sm.x); split_tf32(v.y, b.y, sm.y);
+      split_tf32(v.z, b.z, sm.z); split_tf32(v.w, b.w, sm.w);
+      *reinterpret_cast<float4*>(big + mn * kSK + k0 + 4 * h) = b;
+      *reinterpret_cast<float4*>(small + mn * kSK + k0 + 4 * h) = sm;
+    }
+  } else {
+    const int lane = tid & 31, w = tid >> 5;
+    const int k = 4 * w + (lane >> 3);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int mn = (lane & 7) + 8 * j;
+      float b, sm;
+      split_tf32(raw[k * kSM + mn], b, sm);
+      big[mn * kSK + k] = b;
+      small[mn * kSK + k] = sm;
+    }
+  }
 }
 
 // One 64 x 64 output tile (or one K-slice range of it for split-K) on the tensor cores, 3xTF32.
 // 8 warps as 2 (M) x 4 (N), each a 32 x 16 warp tile = 2 x 2 m16n8 fragments; kTK-wide K slices
-// of both operands stream through a kStages-deep cp.async ring. The accumulation order is fixed, so
-// the result is deterministic (replicas stay bit-identical).
+// of both operands stream through a kStages-deep cp.async ring and are split once per CTA. The
+// accumulation order is fixed, so the result is deterministic (replicas stay bit-identical).
 __device__ void gemm_tile(const Gemm& g, int work, float* ring) {
   const int tiles_n = (g.N + kTN - 1) / kTN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
@@ -113,6 +152,7 @@ __device__ void gemm_tile(const Gemm& g, int work, float* ring) {
   const int nk = kend > kbeg ? (kend - kbeg + kTK - 1) / kTK : 0;
   auto As = [&](int st) { return ring + st * 2 * kSliceFloats; };
   auto Bs = [&](int st) { return ring + st * 2 * kSliceFloats + kSliceFloats; };
+  float* planes = ring + kStages * 2 * kSliceFloats;   // A big, A small, B big, B small
   auto issue = [&](int it) {
     if (it < nk) {
       const int k0 = kbeg + it * kTK, st = it % kStages;
@@ -122,44 +162,47 @@ __device__ void gemm_tile(const Gemm& g, int work, float* ring) {
     cp_async_commit();   // (empty groups keep the wait arithmetic uniform)
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16, gq = lane >> 2, tq = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int gq = lane >> 2, tq = lane & 3;
+  // ldmatrix lane addresses (bytes, relative to a plane): A matrices (rows 0-7 | 8-15) x (k 0-3 | 4-7),
+  // B matrices (n 0-7, k 0-3 | 4-7) then (n 8-15, ...)
+  const uint32_t pl = smem_u32(planes);
+  const uint32_t a_off = static_cast<uint32_t>(((wm + (lane & 7) + 8 * ((lane >> 3) & 1)) * kSK + 4 * (lane >> 4)) * 4);
+  const uint32_t b_off = static_cast<uint32_t>(((wn + (lane & 7) + 8 * (lane >> 4)) * kSK + 4 * ((lane >> 3) & 1)) * 4);
+  constexpr uint32_t kPlaneBytes = kPlaneFloats * 4;
   float acc[2][2][4] = {};
-  __syncthreads();       // the ring may still be read by the previous tile
+  __syncthreads();       // the ring and planes may still be read by the previous tile
 #pragma unroll
   for (int i = 0; i < kStages - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
     cp_async_wait<kStages - 2>();
+    __syncthreads();     // slice `it` landed for everyone; every warp is past the previous MMAs
+    issue(it + kStages - 1);
+    split_slice(As(it % kStages), a_kc, planes, planes + kPlaneFloats);
+    split_slice(Bs(it % kStages), b_kc, planes + 2 * kPlaneFloats, planes + 3 * kPlaneFloats);
     __syncthreads();
-    issue(it + kStages - 1);   // overwrites the stage read one slice ago (all threads are past it)
-    const float* sa = As(it % kStages);
-    const float* sb = Bs(it % kStages);
     // per-slice partial sums start from zero and are added to acc with IEEE fp32 adds: the
-    // tensor core's internal accumulation then only spans 6 products-of-8, not the whole K
+    // tensor core's internal accumulation then only spans 12 products-of-8, not the whole K
     float part[2][2][4] = {};
 #pragma unroll
     for (int kk = 0; kk < kTK; kk += 8) {
-      uint32_t ab[2][4], as[2][4], bb[2][2], bs[2][2];
+      uint32_t ab[2][4], as[2][4], bb[4], bs[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int r = wm + i * 16 + gq;
-        split_tf32(slice_at(sa, a_kc, r, kk + tq), ab[i][0], as[i][0]);
-        split_tf32(slice_at(sa, a_kc, r + 8, kk + tq), ab[i][1], as[i][1]);
-        split_tf32(slice_at(sa, a_kc, r, kk + tq + 4), ab[i][2], as[i][2]);
-        split_tf32(slice_at(sa, a_kc, r + 8, kk + tq + 4), ab[i][3], as[i][3]);
+        const uint32_t o = a_off + static_cast<uint32_t>((16 * i * kSK + kk) * 4);
+        ldsm_x4(ab[i], pl + o);
+        ldsm_x4(as[i], pl + kPlaneBytes + o);
       }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = wn + j * 8 + gq;
-        split_tf32(slice_at(sb, b_kc, c, kk + tq), bb[j][0], bs[j][0]);
-        split_tf32(slice_at(sb, b_kc, c, kk + tq + 4), bb[j][1], bs[j][1]);
-      }
+      const uint32_t ob = b_off + static_cast<uint32_t>(kk * 4);
+      ldsm_x4(bb, pl + 2 * kPlaneBytes + ob);
+      ldsm_x4(bs, pl + 3 * kPlaneBytes + ob);
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          mma_tf32(part[i][j], as[i], bb[j]);
-          mma_tf32(part[i][j], ab[i], bs[j]);
-          mma_tf32(part[i][j], ab[i], bb[j]);
+          mma_tf32(part[i][j], as[i], bb[2 * j], bb[2 * j + 1]);
+          mma_tf32(part[i][j], ab[i], bs[2 * j], bs[2 * j + 1]);
+          mma_tf32(part[i][j], ab[i], bb[2 * j], bb[2 * j + 1]);
         }
     }
 #pragma unroll
@@ -316,7 +359,7 @@ __device__ void update_range(const AdaptParams& p, long long begin, long long en
   }
 }
 
-__global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_constant__ AdaptParams p) {
+__global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_constant__ AdaptParams p) {
   extern __shared__ __align__(16) float ring[];   // kStages x {A, B} slices
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
@@ -446,7 +489,11 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adapt_kernel, kAdaptThreads, kAdaptSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int want = 1;   // one CTA per SM: two co-resident CTAs with tiles halve each other's speed
+  // Small batches (online adaptation): one CTA per SM — phases have fewer tiles than CTAs and two
+  // co-resident busy CTAs halve each other's speed (B = 1024, 4x512: 0.31 vs 0.35 ms). Large
+  // batches (offline training): two CTAs per SM hide the mma.sync / ldmatrix latency of the other
+  // (B = 32768: 28.1 vs 21.5 TFLOP/s). AUTOBYTE_ADAPT_PER_SM=1|2 overrides.
+  int want = p.B >= 4096 ? 2 : 1;
   if (const char* env = std::getenv("AUTOBYTE_ADAPT_PER_SM")) want = std::atoi(env) == 2 ? 2 : 1;
   int grid = num_sms * (per_sm < want ? per_sm : want);
   *grid_used = grid;
