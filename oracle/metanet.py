@@ -167,6 +167,32 @@ def argmax_rows(s: np.ndarray, c_offset: int = 0) -> Tuple[np.ndarray, np.ndarra
     return best_idx, best_val
 
 
+def topk_rows(s: np.ndarray, k: int, c_offset: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+    """Per-row k best candidates in descending score order (SURVEY NEXT 4 "top-k output"; R#19):
+    the definition extends the arg-max — the i-th entry is the best candidate not among
+    the first i-1, ties to the smallest index (R#11), NaN never selected; rows with fewer than k
+    non-NaN scores are padded with (-1, NaN). Written as k literal scans, so topk_rows(s, 1) is
+    argmax_rows(s) by construction."""
+    R, C = s.shape
+    idx = np.full((R, k), -1, np.int64)
+    val = np.full((R, k), np.nan)
+    for r in range(R):
+        taken = set()
+        for i in range(k):
+            best = -1
+            for c in range(C):
+                v = s[r, c]
+                if c in taken or np.isnan(v):
+                    continue
+                if best < 0 or v > s[r, best]:
+                    best = c
+            if best < 0:
+                break
+            taken.add(best)
+            idx[r, i], val[r, i] = best + c_offset, s[r, best]
+    return idx, val
+
+
 # -------------------------------------------------------------------------------------------
 # Eq. 2 loss and online adaptation (P:404-408, P:418-423, P:438; R#12, R#13)
 # -------------------------------------------------------------------------------------------

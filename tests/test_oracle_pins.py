@@ -376,3 +376,27 @@ def test_train_adam_learns_a_teacher():
     batch.V_bar = (Vt * (np.arange(16)[None, :] < batch.jobs.n[:, None])).astype(np.float32)
     _, _, losses = oracle.train(W, batch, 300, "adam", lr=1e-2)
     assert losses[-1] < losses[0] / 5, (losses[0], losses[-1])
+
+
+# ---------------------------------------------------------------- top-k output (NEXT 4)
+def test_topk_k1_is_argmax_and_matches_a_sort():
+    rng = np.random.default_rng(3)
+    s = rng.integers(-5, 5, size=(7, 40)).astype(np.float64)   # many exact ties
+    s[2, :] = np.nan
+    s[3, ::3] = np.nan
+    i1, v1 = oracle.topk_rows(s, 1)
+    ia, va = oracle.argmax_rows(s)
+    assert np.array_equal(i1[:, 0], ia) and np.array_equal(np.nan_to_num(v1[:, 0], nan=-99), np.nan_to_num(va, nan=-99))
+    ik, vk = oracle.topk_rows(s, 6, c_offset=100)
+    for r in range(7):   # independent: a stable sort on (-score, c) over the non-NaN entries
+        ok = [c for c in np.lexsort((np.arange(40), -np.nan_to_num(s[r], nan=-np.inf))) if not np.isnan(s[r, c])][:6]
+        want = np.array([c + 100 for c in ok] + [-1] * (6 - len(ok)))
+        assert np.array_equal(ik[r], want), r
+    assert np.all(ik[2] == -1) and np.all(np.isnan(vk[2]))
+
+
+def test_topk_closed_forms():
+    s = np.arange(10, dtype=np.float64)[None, :]
+    assert np.array_equal(oracle.topk_rows(s, 3)[0][0], [9, 8, 7])
+    assert np.array_equal(oracle.topk_rows(-s, 3)[0][0], [0, 1, 2])
+    assert np.array_equal(oracle.topk_rows(np.zeros((1, 5)), 7)[0][0], [0, 1, 2, 3, 4, -1, -1])
