@@ -174,6 +174,16 @@ autobyte_status autobyte_argmax(autobyte_ctx* ctx, const autobyte_job_stats* job
                                 const autobyte_grid* grid, const int32_t* cur_idx,
                                 int32_t* best_idx, float* best_score, float* cur_score);
 
+/* Per-job top-k candidates (R#19): idx[j][i] / score[j][i] (i < k, [J][k]
+ * each, DEVICE) are the i-th best global candidate of job j over the grid — descending score,
+ * ties to the smaller c (R#11), NaN never selected, (-1, NaN) padding when fewer than k scores
+ * are valid; idx[j][0] == autobyte_argmax's best_idx. 1 <= k <= 32 (else AB_E_INVALID, no
+ * launch). Scores the shard like autobyte_score (the [J][shard] matrix lives in a context
+ * workspace), selects per job, and at G > 1 all-gathers the per-rank lists (J*k u64 per rank)
+ * and merges them, so every rank returns the same, shard-layout-independent result. */
+autobyte_status autobyte_topk(autobyte_ctx* ctx, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                              int32_t k, int32_t* idx, float* score);
+
 /* Online adaptation (R#12, R#13): `steps` plain-SGD steps with learning
  * rate lr on the minibatch of B = samples->J observations: sample b has job statistics
  * samples[b], observed configuration (sp_bytes[b], sc_mult[b]) and observed per-worker speed

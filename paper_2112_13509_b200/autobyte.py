@@ -73,7 +73,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_validate_blob", "autobyte_create", "autobyte_destroy", "autobyte_last_error",
            "autobyte_synchronize", "autobyte_get_unique_id", "autobyte_attach_comm", "autobyte_encode",
            "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
-           "autobyte_adapt_host", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
+           "autobyte_adapt_host", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile"]
 
 _lib = None
@@ -109,6 +109,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_trigger": (I32, [P, I32, P, P, P, P, P, F32, F32, P]),
         "autobyte_argmax_host": (I32, [P, P, P, P, P, P, P]),
         "autobyte_adapt_host": (I32, [P, P, P, P, P, F32, I32, P]),
+        "autobyte_topk": (I32, [P, P, P, I32, P, P]),
         "autobyte_train": (I32, [P, P, P, P, P, P, I32, P]),
         "autobyte_reset_optimizer": (I32, [P]),
         "autobyte_optimizer_step": (I64, [P]),
@@ -319,6 +320,16 @@ class AutoByte:
                                             V_bar.data_ptr(), float(lr), int(steps),
                                             loss.data_ptr() if loss is not None else None), "adapt")
         return loss
+
+    def topk(self, jobs: DeviceJobs, grid: DeviceGrid, k: int, begin: int = 0, end: Optional[int] = None):
+        """Per-job k best candidates (global indices, descending score; -1 / NaN padding)."""
+        import torch
+        idx = torch.empty((jobs.J, k), dtype=torch.int32, device=self.torch_device)
+        score = torch.empty((jobs.J, k), dtype=torch.float32, device=self.torch_device)
+        js, gs = jobs.struct(), grid.struct(begin, end)
+        self._check(self.lib.autobyte_topk(self.ctx, ctypes.byref(js), ctypes.byref(gs), int(k), idx.data_ptr(),
+                                           score.data_ptr()), "topk")
+        return idx, score
 
     def train(self, samples: DeviceJobs, S_p, S_c, V_bar, steps: int, optimizer: str = "adam", lr: float = 1e-3,
               beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, want_losses: bool = True):

@@ -79,6 +79,8 @@ struct autobyte_ctx {
   // per-call workspace
   DevBuf<float> jobvec, x, adapt_ws, loss_tmp;
   DevBuf<float> opt_m, opt_v;        // Adam moments (autobyte_train), blob layout
+  DevBuf<float> topk_scores;         // [J][shard] score matrix of autobyte_topk
+  DevBuf<unsigned long long> topk_keys;   // [G][J][k] per-rank top-k keys
   long long opt_t = 0;               // Adam step count
   DevBuf<float2> u;                  // [shard] candidate encodings (K0)
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
@@ -400,7 +402,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
   c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
-  c->opt_m.release(); c->opt_v.release();
+  c->opt_m.release(); c->opt_v.release(); c->topk_scores.release(); c->topk_keys.release();
   c->loss_tmp.release(); c->keys.release();
   c->sT.release(); c->sBd.release(); c->sBu.release(); c->sSc.release(); c->sV.release();
   c->rScore.release(); c->rCur.release();
@@ -540,6 +542,40 @@ autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* sampl
 }  // namespace
 
 extern "C" {
+
+autobyte_status autobyte_topk(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid, int32_t k,
+                              int32_t* idx, float* score) {
+  if (!c) return AB_E_INVALID;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (k < 1 || k > 32) return fail(c, AB_E_INVALID, "k must be in [1, 32]");
+  if (!idx || !score) return fail(c, AB_E_INVALID, "idx / score is NULL");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
+  const int J = jobs->J;
+  const long long cs = grid->shard_end - grid->shard_begin;
+  const int G = (c->comm && c->world > 1) ? c->world : 1;
+  AB_CUDA(c, c->topk_scores.ensure((size_t)J * cs));
+  AB_CUDA(c, c->topk_keys.ensure((size_t)G * J * k));
+  if ((s = run_encode_and_score(c, jobs, grid, nullptr, c->topk_scores.ptr)) != AB_OK) return s;
+  unsigned long long* mine = c->topk_keys.ptr + (G > 1 ? (size_t)c->rank * J * k : 0);
+  AB_CUDA(c, timed(c, K_FINALIZE, [&] {
+            return launch_topk(J, cs, c->topk_scores.ptr, grid->shard_begin, k, mine, c->stream);
+          }));
+  if (G > 1) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
+    ncclResult_t r = ncclAllGather(mine, c->topk_keys.ptr, (size_t)J * k, ncclUint64, c->comm, c->stream);
+    if (c->profiling) { cudaEventRecord(b, c->stream); c->pending.push_back({K_EXCHANGE, {a, b}}); }
+    if (r != ncclSuccess) return fail(c, AB_E_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    c->launches[K_EXCHANGE] += 1;
+  }
+  AB_CUDA(c, timed(c, K_FINALIZE, [&] {
+            return launch_topk_merge(J, G, k, c->topk_keys.ptr, idx, score, c->stream);
+          }));
+  return AB_OK;
+}
 
 autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                const float* sc_mult, const float* v_obs, float lr, int32_t steps,

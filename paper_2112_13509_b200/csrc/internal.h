@@ -107,6 +107,10 @@ cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
+cudaError_t launch_topk(int J, long long C, const float* scores, long long c_begin, int k, unsigned long long* out,
+                        cudaStream_t s);                                                       // K6
+cudaError_t launch_topk_merge(int J, int G, int k, const unsigned long long* lists, int32_t* idx, float* score,
+                              cudaStream_t s);                                                 // K7
 size_t adapt_ws_floats(int B, int H, int L);
 constexpr int kAdaptSplitK = 4;   // must match adapt.cu kSplitK (gradient partial buffers)
 cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,

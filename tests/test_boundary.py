@@ -96,6 +96,7 @@ def test_null_ctx_calls_fail_cleanly(lib):
     assert lib.autobyte_adapt(None, None, None, None, None, 0.1, 1, None) == ab.AB_E_INVALID
     assert lib.autobyte_train(None, None, None, None, None, None, 1, None) == ab.AB_E_INVALID
     assert lib.autobyte_reset_optimizer(None) == ab.AB_E_INVALID
+    assert lib.autobyte_topk(None, None, None, 4, None, None) == ab.AB_E_INVALID
     assert lib.autobyte_optimizer_step(None) == -1
     assert lib.autobyte_last_error(None) == b"NULL ctx"
 

@@ -35,12 +35,22 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
     dist.all_gather(allp, packed)
     same_all_ranks = all(torch.equal(allp[0], x) for x in allp)
     res = {"config": name, "world": world, "cta_group": cg, "same_on_all_ranks": same_all_ranks}
+    # top-k (NEXT 4): per-rank lists all-gathered and merged -> identical everywhere and to 1 GPU
+    ti, ts = net.topk(dj, dg, 8, b, e)
+    torch.cuda.synchronize(dev)
+    tpk = torch.cat([ti.reshape(-1), ts.view(torch.int32).reshape(-1)])
+    allt = [torch.empty_like(tpk) for _ in range(world)]
+    dist.all_gather(allt, tpk)
+    res["topk_same_on_all_ranks"] = all(torch.equal(allt[0], x) for x in allt)
     if rank == 0:
         single = AutoByte(desc.hidden_layers, desc.hidden_width, W, device=dev.index)
         bi1, bs1, cs1 = single.argmax(dj, dg, cur)
         torch.cuda.synchronize(dev)
         res["g_invariant"] = bool(torch.equal(bi, bi1) and torch.equal(bs.view(torch.int32), bs1.view(torch.int32))
                                   and torch.equal(torch.nan_to_num(cs), torch.nan_to_num(cs1)))
+        ti1, ts1 = single.topk(dj, dg, 8)
+        torch.cuda.synchronize(dev)
+        res["topk_g_invariant"] = bool(torch.equal(ti, ti1) and torch.equal(ts.view(torch.int32), ts1.view(torch.int32)))
         sample = [0, jobs.J // 2, jobs.J - 1]
         s_ora = oracle.score_matrix(W, jobs, grid, job_idx=sample)
         check_argmax(bi.cpu().numpy()[sample], s_ora, 2e-2)
@@ -85,7 +95,8 @@ def main():
         r = run(name, desc, jobs, grid, cg, dev, rank, world)
         if rank == 0:
             print(json.dumps(r), flush=True)
-            ok &= r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
+            ok &= (r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
+                   and r["topk_same_on_all_ranks"] and r["topk_g_invariant"])
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
