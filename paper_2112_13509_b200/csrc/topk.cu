@@ -8,11 +8,10 @@
 //
 // K6: one CTA (8 warps) per job. Each warp keeps its current top-32 as one key per lane (lane i =
 // rank i, descending) and consumes the row 32 keys at a time: a batch none of whose keys beats
-// the warp's k-th key is skipped with one ballot (after warm-up almost every batch), otherwise
-// it is bitonic-sorted across the lanes and merged (max of the list against the reversed batch,
-// then a bitonic merge). The 8 warp lists are merged the same way by warp 0. The row is read
-// once with coalesced float4 loads, up to 8 CTAs per SM: HBM-bound (4 B per (job, candidate);
-// C5 = 4.3 GB in ~0.7 ms).
+// the warp's k-th key is skipped with one ballot, otherwise it is bitonic-sorted across the
+// lanes and merged (max of the list against the reversed batch, then a bitonic merge). The 8
+// warp lists are merged the same way by warp 0. The row is read once with coalesced float4
+// loads (4 B per (job, candidate)).
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -58,40 +57,90 @@ __device__ __forceinline__ unsigned long long warp_merge_lists(unsigned long lon
   return warp_merge_desc(m, lane);
 }
 
-__global__ void __launch_bounds__(kTopkThreads) topk_kernel(int J, long long C, const float* __restrict__ scores,
-                                                            long long c_begin, int k,
-                                                            unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long lists[kTopkThreads / 32][32];
-  const int j = blockIdx.x;
-  if (j >= J) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float* row = scores + (size_t)j * C;
-  const bool vec = (C & 3) == 0;   // every row 16-byte aligned
-  unsigned long long list = 0ull;
-  unsigned long long thr = 0ull;   // the warp's current k-th key
-  // each warp takes 128 consecutive candidates per step (one float4 per lane) = four 32-key batches
-  for (long long base = (long long)warp * 128; base < C; base += (long long)kTopkThreads * 4) {
-    const long long c0 = base + 4 * lane;
-    float v[4];
-    if (vec && c0 + 3 < C) {
-      const float4 f = __ldg(reinterpret_cast<const float4*>(row + c0));
-      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = c0 + q < C ? __ldg(row + c0 + q) : __uint_as_float(0x7FC00000u);
-    }
+// One warp's pass over a set of 128-candidate blocks (one float4 per lane = four 32-key groups):
+// blocks whose best score is below the threshold score cost one vote; the rest are keyed, and a
+// 32-key group merges only if one of its keys beats the threshold key.
+struct WarpTopk {
+  unsigned long long list = 0ull;   // this warp's top-32, lane i = rank i (descending)
+  unsigned long long thr = 0ull;    // the k-th key it must beat
+  float thr_s = -INFINITY;          // its score: a float pre-filter (v >= thr_s is a superset of key > thr)
+  __device__ __forceinline__ void raise(unsigned long long t) {
+    if (t > thr) { thr = t; thr_s = unord32(static_cast<uint32_t>(t >> 32)); }
+  }
+  __device__ __forceinline__ void consume(const float (&v)[4], long long c0, long long c_begin, int k, int lane) {
+    const float vmax = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));   // ignores NaN; all-NaN fails
+    if (!__any_sync(0xffffffffu, vmax >= thr_s)) return;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const unsigned long long key = cand_key(v[q], c_begin + c0 + q);   // NaN (incl. padding) -> 0
       if (!__any_sync(0xffffffffu, key > thr)) continue;
       list = warp_merge_lists(list, warp_sort_desc(key, lane), lane);
-      thr = __shfl_sync(0xffffffffu, list, k - 1);
+      raise(__shfl_sync(0xffffffffu, list, k - 1));
     }
   }
-  lists[warp][lane] = list;
+};
+
+__device__ __forceinline__ void load_block(const float* row, long long C, bool vec, long long c0, float (&v)[4]) {
+  if (vec && c0 + 3 < C) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(row + c0));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = c0 + q < C ? __ldg(row + c0 + q) : __uint_as_float(0x7FC00000u);
+  }
+}
+
+// Two phases keep the merges rare whatever the score surface looks like (smooth trends along the
+// grid, or plateaus of exactly equal scores — bf16 activations make neighbouring candidates tie):
+//   A. the warps key a uniform sample (every 64th block) and the CTA takes the best warp k-th key
+//      as a common threshold (a valid lower bound: that warp holds k keys at or above it);
+//   B. each warp scans its remaining blocks in ascending c with kU loads in flight, so equal
+//      scores arrive in tie-break order and stop beating the threshold once k of them are in.
+__global__ void __launch_bounds__(kTopkThreads) topk_kernel(int J, long long C, const float* __restrict__ scores,
+                                                            long long c_begin, int k,
+                                                            unsigned long long* __restrict__ out) {
+  constexpr int kW = kTopkThreads / 32, kSample = 64, kU = 4;
+  __shared__ unsigned long long lists[kW][32];
+  __shared__ unsigned long long s_thr[kW];
+  const int j = blockIdx.x;
+  if (j >= J) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* row = scores + (size_t)j * C;
+  const bool vec = (C & 3) == 0;   // every row 16-byte aligned
+  const long long NB = (C + 127) / 128;
+  WarpTopk t;
+  // phase A: sample blocks b = kSample * m, m = warp, warp + kW, ...
+  for (long long m = warp; m * kSample < NB; m += kW) {
+    float v[4];
+    const long long c0 = m * kSample * 128 + 4 * lane;
+    load_block(row, C, vec, c0, v);
+    t.consume(v, c0, c_begin, k, lane);
+  }
+  if (lane == 0) s_thr[warp] = t.thr;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kW; ++w) t.raise(s_thr[w]);
+  // phase B: blocks b = warp, warp + kW, ... except the sampled ones (b % kSample == 0 only occurs
+  // for warp 0, since kW divides kSample)
+  for (long long b0 = warp; b0 < NB; b0 += (long long)kW * kU) {
+    float v[kU][4];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long b = b0 + (long long)u * kW;
+      const long long c0 = (b < NB && b % kSample != 0) ? b * 128 + 4 * lane : C;   // C: all padding
+      load_block(row, C, vec, c0, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long b = b0 + (long long)u * kW;
+      t.consume(v[u], b * 128 + 4 * lane, c_begin, k, lane);
+    }
+  }
+  lists[warp][lane] = t.list;
   __syncthreads();
   if (warp == 0) {
-    for (int w = 1; w < kTopkThreads / 32; ++w) list = warp_merge_lists(list, lists[w][lane], lane);
+    unsigned long long list = t.list;
+    for (int w = 1; w < kW; ++w) list = warp_merge_lists(list, lists[w][lane], lane);
     if (lane < k) out[(size_t)j * k + lane] = list;
   }
 }
