@@ -22,9 +22,13 @@
 
 namespace ab {
 
-constexpr int kAdaptThreads = 256;
-constexpr int kTM = 64, kTN = 64, kTK = 32;
+constexpr int kWorkThreads = 256;                 // warps 0-7: staging, operand split, epilogue, SIMT phases
+constexpr int kIssuerWarp = kWorkThreads / 32;    // warp 8: tcgen05.mma issuer
+constexpr int kAdaptThreads = kWorkThreads + 32;
+constexpr uint32_t kWorkBar = 1;                  // named barrier of the 256 worker threads
+constexpr int kTM = 128, kTN = 64, kTK = 32;   // tcgen05 tile: M = 128 TMEM lanes, N = 64, K slices of 32 tf32
 constexpr int kSplitK = kAdaptSplitK;   // K = B splits of the weight-gradient GEMMs (partials in grads[kSplitK][total])
+constexpr int kNAcc = 4;                // TMEM accumulators per tile (K slices round-robin, summed in fp32)
 
 struct Gemm {
   int M, N, K;
@@ -39,17 +43,21 @@ struct Gemm {
   __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
 };
 
-constexpr int kStages = 4;   // cp.async pipeline depth of the raw operand slices (prefetch distance kStages - 1)
-// Raw operand slices land in shared memory in the orientation of their global layout so every
-// 16-byte cp.async copies a contiguous vector: K-contiguous [64][kTK + 4] or MN-contiguous
-// [kTK][64 + 8]. A conversion pass then splits every element once per CTA into tf32 big / small
-// planes stored K-contiguous [64][kTK + 4] (transposing MN-contiguous slices), from which the
-// warps read whole m16n8k8 fragments with ldmatrix (a tf32 element is a pair of b16 lanes).
-// Row stride kTK + 4 = 36 floats puts the 8 rows of an ldmatrix in 8 distinct 16-byte bank groups.
-constexpr int kSK = kTK + 4, kSM = kTM + 8;
-constexpr int kSliceFloats = (kTM * kSK > kTK * kSM) ? kTM * kSK : kTK * kSM;
-constexpr int kPlaneFloats = kTM * kSK;                  // one split plane [64][36]
-constexpr size_t kAdaptSmemBytes = sizeof(float) * (kStages * 2 * kSliceFloats + 4 * kPlaneFloats);
+// Shared memory (dynamic, 1 KB aligned):
+//   planes  2 buffers x {A big, A small [128][32] tf32, B big, B small [64][32] tf32}, UMMA SW128
+//           K-major (row r of an 8-row 1 KB atom at 128 r bytes, 16-byte chunk j at chunk j ^ (r % 8))
+//   raw     kStages x {A, B} fp32 slices as copied from global in their own orientation:
+//           K-contiguous [rows][kTK + 4] or MN-contiguous [kTK][rows + 8]
+constexpr int kStages = 3;   // cp.async depth of the raw slices (prefetch distance kStages - 1)
+constexpr int kSK = kTK + 4;
+constexpr int kRawA = (kTM * kSK > kTK * (kTM + 8)) ? kTM * kSK : kTK * (kTM + 8);   // floats
+constexpr int kRawB = (kTN * kSK > kTK * (kTN + 8)) ? kTN * kSK : kTK * (kTN + 8);
+constexpr int kPlaneA = kTM * kTK * 4, kPlaneB = kTN * kTK * 4;                       // bytes
+constexpr int kPlaneBuf = 2 * kPlaneA + 2 * kPlaneB;                                  // one buffer
+constexpr size_t kRawOff = 2 * (size_t)kPlaneBuf;
+constexpr size_t kAdaptSmemBytes = 1024 + kRawOff + sizeof(float) * kStages * (kRawA + kRawB);
+constexpr uint32_t kTmemCols = kNAcc * kTN;   // 256
+constexpr uint32_t kIdesc = umma_idesc_tf32(kTM, kTN);
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
@@ -70,73 +78,94 @@ __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
   big = __uint_as_float(b);
   small = __uint_as_float(sm);
 }
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-               "{%0,%1,%2,%3};"
-               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
 
-// Stage one 64 x kTK slice of an operand: X(mn, k) = base[mn*lmn + k*lk] for mn in [mn0, mn0+64),
-// k in [k0, k0+kTK), zero-filled outside [0, MN) x [k0, kend). 16-byte vectors, kTK/16 per thread.
+// Stage one ROWS x kTK slice of an operand: X(mn, k) = base[mn*lmn + k*lk] for mn in [mn0, mn0+ROWS),
+// k in [k0, k0+kTK), zero-filled outside [0, MN) x [k0, kend). 16-byte vectors.
+template <int ROWS>
 __device__ __forceinline__ void stage_slice(float* dst, const float* base, long long lmn, long long lk, int MN,
                                             int mn0, int k0, int kend) {
+  constexpr int kVec = ROWS * kTK / 4 / kWorkThreads;   // vectors per thread
 #pragma unroll
-  for (int r = 0; r < kTK / 16; ++r) {
-    const int e = threadIdx.x + r * kAdaptThreads;
+  for (int r = 0; r < kVec; ++r) {
+    const int e = threadIdx.x + r * kWorkThreads;
     if (lk == 1) {   // K-contiguous: vector (mn, 4 k)
       const int mn = e / (kTK / 4), kq = (e % (kTK / 4)) * 4;
       const bool v = mn0 + mn < MN && k0 + kq < kend;
       cp_async16(dst + mn * kSK + kq, v ? base + (long long)(mn0 + mn) * lmn + (k0 + kq) : base, v);
     } else {         // MN-contiguous: vector (k, 4 mn)
-      const int k = e >> 4, mq = (e & 15) * 4;
+      const int k = e / (ROWS / 4), mq = (e % (ROWS / 4)) * 4;
       const bool v = k0 + k < kend && mn0 + mq < MN;
-      cp_async16(dst + k * kSM + mq, v ? base + (long long)(k0 + k) * lk + (mn0 + mq) : base, v);
+      cp_async16(dst + k * (ROWS + 8) + mq, v ? base + (long long)(k0 + k) * lk + (mn0 + mq) : base, v);
     }
   }
 }
 
-// Split one raw slice into K-contiguous big / small planes (8 elements per thread). K-contiguous
-// raw: thread -> (mn, 8 consecutive k), LDS.128 / STS.128. MN-contiguous raw: warp w -> k in
-// [4w, 4w+4), lane -> (k = 4w + lane/8, mn = lane%8 + 8j): conflict-free on both the raw read
-// (stride 72) and the transposed plane write (stride 36).
-__device__ __forceinline__ void split_slice(const float* raw, bool kcontig, float* big, float* small) {
-  const int tid = threadIdx.x;
+// Split a raw slice into SW128 K-major big / small planes, one 16-byte chunk (4 k) at a time.
+// K-contiguous raw: thread -> (row, chunk) with the 8 threads of a row covering its 8 chunks.
+// MN-contiguous raw: warp w -> chunk w, lanes -> rows (4 strided LDS per chunk, conflict-free).
+template <int ROWS>
+__device__ __forceinline__ void split_slice(const float* raw, bool kcontig, uint8_t* big, uint8_t* small) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // plain C++ shared-memory accesses (no asm memory clobbers), so the compiler can hoist every
+  // raw load of the slice ahead of the plane stores; ordering against the tensor core comes from
+  // the fence.proxy.async + mbarrier arrive that follow
+  auto store = [&](int r, int j, const float4& v) {
+    float4 b, sm;
+    split_tf32(v.x, b.x, sm.x); split_tf32(v.y, b.y, sm.y);
+    split_tf32(v.z, b.z, sm.z); split_tf32(v.w, b.w, sm.w);
+    const int off = (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4);
+    *reinterpret_cast<float4*>(big + off) = b;
+    *reinterpret_cast<float4*>(small + off) = sm;
+  };
   if (kcontig) {
-    const int mn = tid >> 2, k0 = (tid & 3) * 8;
+    constexpr int kN = ROWS * 8 / kWorkThreads;
+    float4 v[kN];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float4 v = *reinterpret_cast<const float4*>(raw + mn * kSK + k0 + 4 * h);
-      float4 b, sm;
-      split_tf32(v.x, b.x, sm.x); split_tf32(v.y, b.y, sm.y);
-      split_tf32(v.z, b.z, sm.z); split_tf32(v.w, b.w, sm.w);
-      *reinterpret_cast<float4*>(big + mn * kSK + k0 + 4 * h) = b;
-      *reinterpret_cast<float4*>(small + mn * kSK + k0 + 4 * h) = sm;
+    for (int i = 0; i < kN; ++i) {
+      const int e = tid + i * kWorkThreads, r = e >> 3, j = e & 7;
+      v[i] = *reinterpret_cast<const float4*>(raw + r * kSK + 4 * j);
+    }
+#pragma unroll
+    for (int i = 0; i < kN; ++i) {
+      const int e = tid + i * kWorkThreads;
+      store(e >> 3, e & 7, v[i]);
     }
   } else {
-    const int lane = tid & 31, w = tid >> 5;
-    const int k = 4 * w + (lane >> 3);
+    constexpr int kN = ROWS / 32;
+    float4 v[kN];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int mn = (lane & 7) + 8 * j;
-      float b, sm;
-      split_tf32(raw[k * kSM + mn], b, sm);
-      big[mn * kSK + k] = b;
-      small[mn * kSK + k] = sm;
+    for (int i = 0; i < kN; ++i) {
+      const int r = lane + 32 * i, j = w;
+      v[i].x = raw[(4 * j) * (ROWS + 8) + r];
+      v[i].y = raw[(4 * j + 1) * (ROWS + 8) + r];
+      v[i].z = raw[(4 * j + 2) * (ROWS + 8) + r];
+      v[i].w = raw[(4 * j + 3) * (ROWS + 8) + r];
     }
+#pragma unroll
+    for (int i = 0; i < kN; ++i) store(lane + 32 * i, w, v[i]);
   }
 }
 
-// One 64 x 64 output tile (or one K-slice range of it for split-K) on the tensor cores, 3xTF32.
-// 8 warps as 2 (M) x 4 (N), each a 32 x 16 warp tile = 2 x 2 m16n8 fragments; kTK-wide K slices
-// of both operands stream through a kStages-deep cp.async ring and are split once per CTA. The
-// accumulation order is fixed, so the result is deterministic (replicas stay bit-identical).
-__device__ void gemm_tile(const Gemm& g, int work, float* ring) {
+// Per-CTA tensor-core state that persists across tiles and phases (each thread keeps the counters
+// of its own role; mbarrier parities are derived from them).
+struct TcState {
+  uint32_t tmem;         // kTmemCols fp32 accumulator columns
+  uint64_t* full;        // [2]: the 8 worker warps have written plane buffer b
+  uint64_t* empty;       // [2]: the MMAs that read plane buffer b have completed (tcgen05.commit)
+  uint64_t* acc_free;    // the epilogue has read the accumulators of the last MMA tile
+  uint32_t fills[2];     // workers: times buffer b has been filled
+  uint32_t issued[2];    // issuer: fills of buffer b consumed
+  uint32_t tiles;        // issuer: MMA tiles issued
+};
+
+// One 128 x 64 output tile (or one K range of it for split-K) on tcgen05, 3xTF32. Per K slice of
+// 32: the CTA stages the raw fp32 operands (cp.async, kStages deep), splits them once into tf32
+// big/small SW128 planes (double-buffered, so the split of slice i+1 overlaps the MMAs of slice i),
+// and one elected thread issues 4 K-steps x 3 products of M128 N64 K8 into TMEM accumulator
+// (slice % 4); tcgen05.commit frees the plane buffer. The epilogue sums the 4 accumulators in
+// fixed order with IEEE adds (long accumulations inside the tensor core lose ~1e-3 on the
+// gradients) and applies the mode. Deterministic: fixed issue and summation order.
+__device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   const int tiles_n = (g.N + kTN - 1) / kTN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
   const int split = g.ksplit > 1 ? work / tiles_mn : 0;
@@ -148,86 +177,117 @@ __device__ void gemm_tile(const Gemm& g, int work, float* ring) {
     kbeg = split * chunk;
     kend = min(g.K, kbeg + chunk);
   }
-  const bool a_kc = g.lak == 1, b_kc = g.lbk == 1;
   const int nk = kend > kbeg ? (kend - kbeg + kTK - 1) / kTK : 0;
-  auto As = [&](int st) { return ring + st * 2 * kSliceFloats; };
-  auto Bs = [&](int st) { return ring + st * 2 * kSliceFloats + kSliceFloats; };
-  float* planes = ring + kStages * 2 * kSliceFloats;   // A big, A small, B big, B small
+  const uint32_t pbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kIssuerWarp) {
+    // ---------------- MMA issuer: per slice, wait for the split planes, issue 4 K-steps x 3
+    // products into accumulator (slice % 4), commit -> empty[b] frees the buffer
+    if (nk == 0) return;
+    if (ts.tiles > 0) mbar_wait(ts.acc_free, (ts.tiles - 1) & 1);   // previous tile's epilogue has read TMEM
+    for (int it = 0; it < nk; ++it) {
+      const int b = it & 1;
+      mbar_wait(&ts.full[b], ts.issued[b] & 1);
+      ++ts.issued[b];
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t buf = pbase + b * kPlaneBuf;
+        const uint64_t ab = umma_desc_sw128(buf), as = umma_desc_sw128(buf + kPlaneA);
+        const uint64_t bb = umma_desc_sw128(buf + 2 * kPlaneA), bs = umma_desc_sw128(buf + 2 * kPlaneA + kPlaneB);
+        const uint32_t d = ts.tmem + static_cast<uint32_t>((it % kNAcc) * kTN);
+        const uint32_t first = it < kNAcc ? 1u : 0u;   // first slice of this accumulator in the tile
+#pragma unroll
+        for (int ks = 0; ks < kTK / 8; ++ks) {          // K = 8 tf32 = 32 bytes per step
+          const uint64_t o = static_cast<uint64_t>(2 * ks);
+          umma_ss_tf32(d, as + o, bb + o, kIdesc, (first && ks == 0) ? 0u : 1u);   // small terms first
+          umma_ss_tf32(d, ab + o, bs + o, kIdesc, 1u);
+          umma_ss_tf32(d, ab + o, bb + o, kIdesc, 1u);
+        }
+        umma_commit(&ts.empty[b]);
+      }
+      __syncwarp();
+    }
+    ++ts.tiles;
+    return;
+  }
+  // ---------------- workers (warps 0-7): stage raw slices, split into planes, epilogue
+  const bool a_kc = g.lak == 1, b_kc = g.lbk == 1;
+  float* raw = reinterpret_cast<float*>(smem + kRawOff);
+  auto rawA = [&](int st) { return raw + st * (kRawA + kRawB); };
+  auto rawB = [&](int st) { return raw + st * (kRawA + kRawB) + kRawA; };
   auto issue = [&](int it) {
     if (it < nk) {
       const int k0 = kbeg + it * kTK, st = it % kStages;
-      stage_slice(As(st), g.A, g.lam, g.lak, g.M, m0, k0, kend);
-      stage_slice(Bs(st), g.Bm, g.lbn, g.lbk, g.N, n0, k0, kend);
+      stage_slice<kTM>(rawA(st), g.A, g.lam, g.lak, g.M, m0, k0, kend);
+      stage_slice<kTN>(rawB(st), g.Bm, g.lbn, g.lbk, g.N, n0, k0, kend);
     }
     cp_async_commit();   // (empty groups keep the wait arithmetic uniform)
   };
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
-  const int gq = lane >> 2, tq = lane & 3;
-  // ldmatrix lane addresses (bytes, relative to a plane): A matrices (rows 0-7 | 8-15) x (k 0-3 | 4-7),
-  // B matrices (n 0-7, k 0-3 | 4-7) then (n 8-15, ...)
-  const uint32_t pl = smem_u32(planes);
-  const uint32_t a_off = static_cast<uint32_t>(((wm + (lane & 7) + 8 * ((lane >> 3) & 1)) * kSK + 4 * (lane >> 4)) * 4);
-  const uint32_t b_off = static_cast<uint32_t>(((wn + (lane & 7) + 8 * (lane >> 4)) * kSK + 4 * ((lane >> 3) & 1)) * 4);
-  constexpr uint32_t kPlaneBytes = kPlaneFloats * 4;
-  float acc[2][2][4] = {};
-  __syncthreads();       // the ring and planes may still be read by the previous tile
+  named_bar_sync(kWorkBar, kWorkThreads);   // the raw ring may still be read by the previous tile's split
 #pragma unroll
   for (int i = 0; i < kStages - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
+    const int b = it & 1;
     cp_async_wait<kStages - 2>();
-    __syncthreads();     // slice `it` landed for everyone; every warp is past the previous MMAs
+    named_bar_sync(kWorkBar, kWorkThreads);   // slice `it` landed for every worker
     issue(it + kStages - 1);
-    split_slice(As(it % kStages), a_kc, planes, planes + kPlaneFloats);
-    split_slice(Bs(it % kStages), b_kc, planes + 2 * kPlaneFloats, planes + 3 * kPlaneFloats);
-    __syncthreads();
-    // per-slice partial sums start from zero and are added to acc with IEEE fp32 adds: the
-    // tensor core's internal accumulation then only spans 12 products-of-8, not the whole K
-    float part[2][2][4] = {};
-#pragma unroll
-    for (int kk = 0; kk < kTK; kk += 8) {
-      uint32_t ab[2][4], as[2][4], bb[4], bs[4];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t o = a_off + static_cast<uint32_t>((16 * i * kSK + kk) * 4);
-        ldsm_x4(ab[i], pl + o);
-        ldsm_x4(as[i], pl + kPlaneBytes + o);
-      }
-      const uint32_t ob = b_off + static_cast<uint32_t>(kk * 4);
-      ldsm_x4(bb, pl + 2 * kPlaneBytes + ob);
-      ldsm_x4(bs, pl + 3 * kPlaneBytes + ob);
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          mma_tf32(part[i][j], as[i], bb[2 * j], bb[2 * j + 1]);
-          mma_tf32(part[i][j], ab[i], bs[2 * j], bs[2 * j + 1]);
-          mma_tf32(part[i][j], ab[i], bb[2 * j], bb[2 * j + 1]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[i][j][r] += part[i][j][r];
+    if (ts.fills[b] > 0) mbar_wait(&ts.empty[b], (ts.fills[b] - 1) & 1);   // MMAs on buffer b's last fill done
+    uint8_t* buf = smem + b * kPlaneBuf;
+    split_slice<kTM>(rawA(it % kStages), a_kc, buf, buf + kPlaneA);
+    split_slice<kTN>(rawB(it % kStages), b_kc, buf + 2 * kPlaneA, buf + 2 * kPlaneA + kPlaneB);
+    fence_proxy_async_smem();   // generic-proxy plane writes -> visible to the tensor core
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ts.full[b]);
+    ++ts.fills[b];
   }
   cp_async_wait<0>();
+  if (nk > 0) {   // the last commit completes after every MMA of the tile
+    const int bl = (nk - 1) & 1;
+    mbar_wait(&ts.empty[bl], (ts.fills[bl] - 1) & 1);
+  }
+  tc_fence_after();
+  // epilogue: warp w reads TMEM lane quadrant w % 4 (rows) and column half w / 4 of every accumulator
+  const int quad = warp & 3, half = warp >> 2;
+  const int m = m0 + quad * 32 + lane;
+  const int nb = n0 + half * 32;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = 0.f;
+  const int nacc = nk < kNAcc ? nk : kNAcc;
+  for (int a = 0; a < nacc; ++a) {
+    uint32_t r[32];
+    tmem_ld32(ts.tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * kTN + half * 32), r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
+  }
+  if (nk > 0) {   // accumulators read: the issuer may start the next tile
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(ts.acc_free);
+  }
+  // transpose the warp's 32 x 32 block through shared memory (the raw ring is idle now) so that
+  // lanes run along n: bias, mask and C accesses become one coalesced 128-byte row per instruction
+  (void)m;
+  float* tr = raw + warp * (32 * 33);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = v[i];
+  __syncwarp();
+  const int n = nb + lane;
   float* C = g.C + (g.ksplit > 1 ? split * g.cpart : 0);
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int m = m0 + wm + i * 16 + gq + (r >> 1) * 8;
-        const int n = n0 + wn + j * 8 + 2 * tq + (r & 1);
-        if (m >= g.M || n >= g.N) continue;
-        float v = acc[i][j][r];
-        if (g.mode == 0) v = relu(v + g.bias[n]);
-        else if (g.mode == 1) v = g.mask[m * g.ldmask + n] > 0.f ? v : 0.f;
-        C[m * g.ldc + n] = v;
-      }
+  const float bn = (g.mode == 0 && n < g.N) ? g.bias[n] : 0.f;
+  const int mrow0 = m0 + quad * 32;
+  for (int r = 0; r < 32; ++r) {
+    const int mr = mrow0 + r;
+    if (mr >= g.M) break;
+    if (n < g.N) {
+      float x = tr[r * 33 + lane];
+      if (g.mode == 0) x = relu(x + bn);
+      else if (g.mode == 1) x = g.mask[(long long)mr * g.ldmask + n] > 0.f ? x : 0.f;
+      C[(long long)mr * g.ldc + n] = x;
+    }
+  }
+  __syncwarp();
 }
 
 #ifdef AB_STATS
@@ -265,14 +325,15 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
 // fewest GEMM tiles); warp w sums rows w, w+8, ... of the segment (coalesced, 4 loads in flight)
 // and warp 0 adds the 8 warp partials in fixed order.
 __device__ void colsum_split(const float* X, int B, int N, long long ld, float* out, long long stride) {
-  __shared__ float red[kAdaptThreads / 32][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kAdaptThreads / 32;
+  __shared__ float red[kWorkThreads / 32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kWorkThreads / 32;
+  const bool worker = threadIdx.x < kWorkThreads;   // the issuer warp only joins the barriers
   const int groups = (N + 31) / 32, seg = (B + kSplitK - 1) / kSplitK;
   for (int item = gridDim.x - 1 - blockIdx.x; item < groups * kSplitK; item += gridDim.x) {
     const int sgi = item / groups, n = (item % groups) * 32 + lane;
     const int b0 = sgi * seg, b1 = min(B, b0 + seg);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    if (n < N) {
+    if (worker && n < N) {
       int b = b0 + warp;
       for (; b + 3 * nw < b1; b += 4 * nw) {
         a0 += X[(long long)b * ld + n];
@@ -282,7 +343,7 @@ __device__ void colsum_split(const float* X, int B, int N, long long ld, float* 
       }
       for (; b < b1; b += nw) a0 += X[(long long)b * ld + n];
     }
-    red[warp][lane] = (a0 + a1) + (a2 + a3);
+    if (worker) red[warp][lane] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     if (warp == 0 && n < N) {
       float t = red[0][lane];
@@ -303,7 +364,7 @@ __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, cons
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * kAdaptThreads + threadIdx.x) >> 5, nwarps = (gridDim.x * kAdaptThreads) >> 5;
-  for (int b = gwarp; b < B; b += nwarps) {
+  for (int b = gwarp; b < B; b += nwarps) {   // (every warp of the CTA, issuer included)
     float acc[kNMax];
 #pragma unroll
     for (int w = 0; w < kNMax; ++w) acc[w] = 0.f;
@@ -334,6 +395,7 @@ __device__ void update_range(const AdaptParams& p, long long begin, long long en
   const float* Gr = p.grads;
   const long long total = p.off.total;
   const long long gtid = (long long)blockIdx.x * kAdaptThreads + threadIdx.x, gthreads = (long long)gridDim.x * kAdaptThreads;
+  // (all kAdaptThreads threads of every CTA take part: gtid covers [0, gthreads) exactly once)
   if (p.opt == AB_OPT_ADAM) {
     const double t = static_cast<double>(p.t0 + step + 1);
     const float step_size = static_cast<float>(p.lr / (1.0 - pow(static_cast<double>(p.beta1), t)));
@@ -359,8 +421,25 @@ __device__ void update_range(const AdaptParams& p, long long begin, long long en
   }
 }
 
-__global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_constant__ AdaptParams p) {
-  extern __shared__ __align__(16) float ring[];   // kStages x {A, B} slices
+__global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_constant__ AdaptParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // SW128 atoms: 1 KB aligned
+  float* ring = reinterpret_cast<float*>(smem);   // out_rows stages W_o here between GEMM phases
+  __shared__ __align__(8) uint64_t s_bar[5];   // full[2], empty[2], acc_free
+  __shared__ uint32_t s_tmem;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], kWorkThreads / 32);   // full: one arrive per worker warp
+    mbar_init(&s_bar[1], kWorkThreads / 32);
+    mbar_init(&s_bar[2], 1);                   // empty: tcgen05.commit
+    mbar_init(&s_bar[3], 1);
+    mbar_init(&s_bar[4], kWorkThreads / 32);   // acc_free: one arrive per worker warp
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) { tmem_alloc(&s_tmem, kTmemCols); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  TcState ts{s_tmem, &s_bar[0], &s_bar[2], &s_bar[4], {0u, 0u}, {0u, 0u}, 0u};
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   unsigned int gen = 0;
@@ -401,7 +480,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_co
 #ifdef AB_STATS
       const long long tw0 = clock64();
 #endif
-      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, ring);
+      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, smem, ts);
 #ifdef AB_STATS
       if (k == 2 && step == 0 && threadIdx.x == 0 && blockIdx.x < 1024) {
         unsigned smid;
@@ -441,8 +520,8 @@ __global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_co
       Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H};
       const int t1 = gw.tiles(), t2 = gd.tiles();
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, ring);
-        else gemm_tile(gd, t - t1, ring);
+        if (t < t1) gemm_tile(gw, t, smem, ts);
+        else gemm_tile(gd, t - t1, smem, ts);
       }
       colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
       grid_sync(p.barrier, gen);
@@ -461,8 +540,8 @@ __global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_co
         t2 = gd.tiles();
       }
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, ring);
-        else gemm_tile(gd, t - t1, ring);
+        if (t < t1) gemm_tile(gw, t, smem, ts);
+        else gemm_tile(gd, t - t1, smem, ts);
       }
       colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
       // SGD of the layer above, whose gradient partials completed in the previous phase and whose
@@ -475,6 +554,9 @@ __global__ void __launch_bounds__(kAdaptThreads, 2) adapt_kernel(const __grid_co
     update_range(p, p.off.W[1], p.off.b[1] + H, step);
     if (step + 1 < nsteps) grid_sync(p.barrier, gen);
   }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(ts.tmem, kTmemCols);
 }
 
 size_t adapt_ws_floats(int B, int H, int L) {
@@ -489,12 +571,8 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adapt_kernel, kAdaptThreads, kAdaptSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  // Small batches (online adaptation): one CTA per SM — phases have fewer tiles than CTAs and two
-  // co-resident busy CTAs halve each other's speed (B = 1024, 4x512: 0.31 vs 0.35 ms). Large
-  // batches (offline training): two CTAs per SM hide the mma.sync / ldmatrix latency of the other
-  // (B = 32768: 28.1 vs 21.5 TFLOP/s). AUTOBYTE_ADAPT_PER_SM=1|2 overrides.
-  int want = p.B >= 4096 ? 2 : 1;
-  if (const char* env = std::getenv("AUTOBYTE_ADAPT_PER_SM")) want = std::atoi(env) == 2 ? 2 : 1;
+  // one CTA per SM (the tensor-core tile needs ~180 KB of shared memory)
+  const int want = 1;
   int grid = num_sms * (per_sm < want ? per_sm : want);
   *grid_used = grid;
   void* args[] = {const_cast<AdaptParams*>(&p)};

@@ -14,7 +14,7 @@ using namespace ab;
 // NOISE: warps 1..3 store 16 B/thread to a separate smem region in a loop (epilogue-like traffic)
 // K2LIKE: per 4 MMAs a try_wait on an already-complete barrier + fence + commit (no completion wait)
 // NOISE < 0: warp 1 streams 16 KB TMA bulk copies from global memory into its own smem region
-template <int CG, int N, bool TS, int PER_COMMIT, bool WALK = false, int NOISE = 0, bool K2LIKE = false>
+template <int CG, int N, bool TS, int PER_COMMIT, bool WALK = false, int NOISE = 0, bool K2LIKE = false, bool TF32 = false>
 __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long* out, const uint8_t* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ volatile int stop;
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
   tc_fence_after();
   const uint32_t tmem = tmem_base;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
-  constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, N);
+  constexpr uint32_t idesc = TF32 ? umma_idesc_tf32(128 * CG, N) : umma_idesc_bf16(128 * CG, N);
   long long t0 = clock64(), t1 = t0;
   if (warp == 0 && rank == 0) {
     const uint64_t a0 = umma_desc_sw128(smem_u32(smem));
@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
           const uint64_t ad = a0 + (uint64_t)((ks >> 2) * 1024 + 2 * (ks & 3));
           const uint64_t bd = b0 + (uint64_t)(WALK ? ((((it + k) >> 2) & 3) * 1024 + 2 * (ks & 3)) : 2 * (k & 3));
           const uint32_t at = tmem + 256 + ks * 8;
-          if (CG == 2) {
+          if (TF32) {
+            umma_ss_tf32(tmem, ad, bd, idesc, acc);
+          } else if (CG == 2) {
             if (TS) umma_ts2(tmem, at, bd, idesc, acc);
             else umma_ss2(tmem, ad, bd, idesc, acc);
           } else {
@@ -124,13 +126,14 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, unsigned long long
 }
 
 static uint8_t* g_src = nullptr;
-template <int CG, int N, bool TS, int PER_COMMIT, bool WALK = false, int NOISE = 0, bool K2LIKE = false>
+template <int CG, int N, bool TS, int PER_COMMIT, bool WALK = false, int NOISE = 0, bool K2LIKE = false,
+          bool TF32 = false>
 void run(const char* name, int iters) {
   if (!g_src) { cudaMalloc(&g_src, 64 * 16384); cudaMemset(g_src, 0, 64 * 16384); }
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
   cudaMemset(d, 0, 148 * sizeof(unsigned long long));
-  auto k = mma_loop<CG, N, TS, PER_COMMIT, WALK, NOISE, K2LIKE>;
+  auto k = mma_loop<CG, N, TS, PER_COMMIT, WALK, NOISE, K2LIKE, TF32>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608 + 16384 + 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(148);
@@ -155,15 +158,24 @@ void run(const char* name, int iters) {
   double cyc = 0; int n = 0;
   for (int i = 0; i < 148; ++i) if (h[i]) { cyc += h[i]; ++n; }
   cyc /= n;
-  const double flop = 2.0 * 128 * CG * N * 16 * (double)iters * (148 / CG);
+  const int kstep = TF32 ? 8 : 16;
+  const double flop = 2.0 * 128 * CG * N * kstep * (double)iters * (148 / CG);
   printf("%-34s %s  cycles/MMA %7.1f  per-SM FLOP/cycle %7.0f  chip TFLOP/s %7.1f\n", name, cudaGetErrorString(err),
-         cyc / iters, 2.0 * 128 * N * 16 / (cyc / iters), flop / (ms * 1e-3) / 1e12);
+         cyc / iters, 2.0 * 128 * N * kstep / (cyc / iters), flop / (ms * 1e-3) / 1e12);
   fflush(stdout);
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int it = 1 << 16;
+  if (argc > 1) {   // tf32 shapes of the K4 tile (kind::tf32, K = 8 per instruction)
+    run<1, 64, false, 12, true, 0, false, true>("cg1 tf32 M128 N64 (12/commit)", it);
+    run<1, 128, false, 12, true, 0, false, true>("cg1 tf32 M128 N128 (12/commit)", it);
+    run<1, 256, false, 12, true, 0, false, true>("cg1 tf32 M128 N256 (12/commit)", it);
+    run<1, 64, false, 48, true, 0, false, true>("cg1 tf32 M128 N64 (48/commit)", it);
+    run<1, 128, false, 32, true>("cg1 bf16 M128 N128 (32/commit)", it);
+    return 0;
+  }
   run<1, 128, false, 32>("cg1 M128 N128 SS (32/commit)", it);
   run<1, 128, false, 32, true, 0, true>("cg1 K2-like loop", it);
   run<1, 128, false, 32, true, -1, true>("cg1 K2-like loop + TMA stream", it);
