@@ -26,7 +26,7 @@ constexpr int kWorkThreads = 256;                 // warps 0-7: staging, operand
 constexpr int kIssuerWarp = kWorkThreads / 32;    // warp 8: tcgen05.mma issuer
 constexpr int kAdaptThreads = kWorkThreads + 32;
 constexpr uint32_t kWorkBar = 1;                  // named barrier of the 256 worker threads
-constexpr int kTM = 128, kTN = 64, kTK = 32;   // tcgen05 tile: M = 128 TMEM lanes, N = 64, K slices of 32 tf32
+constexpr int kTM = 128, kTK = 32;   // tcgen05 tile: M = 128 TMEM lanes x N (TileCfg), K slices of 32 tf32
 constexpr int kSplitK = kAdaptSplitK;   // K = B splits of the weight-gradient GEMMs (partials in grads[kSplitK][total])
 constexpr int kNAcc = 4;                // TMEM accumulators per tile (K slices round-robin, summed in fp32)
 
@@ -40,24 +40,34 @@ struct Gemm {
   const float* mask; long long ldmask;
   int ksplit;                            // split-K count (mode 2 only): partial s -> C + s*cpart
   long long cpart;
-  __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN) * (ksplit > 1 ? ksplit : 1); }
+  template <int TN>
+  __device__ int tiles() const { return ((M + kTM - 1) / kTM) * ((N + TN - 1) / TN) * (ksplit > 1 ? ksplit : 1); }
 };
 
 // Shared memory (dynamic, 1 KB aligned):
-//   planes  2 buffers x {A big, A small [128][32] tf32, B big, B small [64][32] tf32}, UMMA SW128
+//   planes  2 buffers x {A big, A small [128][32] tf32, B big, B small [128][32] tf32}, UMMA SW128
 //           K-major (row r of an 8-row 1 KB atom at 128 r bytes, 16-byte chunk j at chunk j ^ (r % 8))
 //   raw     kStages x {A, B} fp32 slices as copied from global in their own orientation:
 //           K-contiguous [rows][kTK + 4] or MN-contiguous [kTK][rows + 8]
-constexpr int kStages = 3;   // cp.async depth of the raw slices (prefetch distance kStages - 1)
+// Two tile widths: N = 64 with a 3-deep raw ring for small batches (online adaptation: more tiles
+// per phase, B = 1024 4x512 0.265 ms vs 0.30 ms with N = 128), N = 128 with a 2-deep ring for large
+// batches (offline training: half the MMAs per FLOP, 8.2 vs 7.2 M samples/s at B = 32768).
+template <int TN>
+struct TileCfg {
+  static constexpr int kStages = TN == 64 ? 3 : 2;   // cp.async depth of the raw slices
+  static constexpr int kRawA = (kTM * (kTK + 4) > kTK * (kTM + 8)) ? kTM * (kTK + 4) : kTK * (kTM + 8);   // floats
+  static constexpr int kRawB = (TN * (kTK + 4) > kTK * (TN + 8)) ? TN * (kTK + 4) : kTK * (TN + 8);
+  static constexpr int kPlaneA = kTM * kTK * 4, kPlaneB = TN * kTK * 4;               // bytes
+  static constexpr int kPlaneBuf = 2 * kPlaneA + 2 * kPlaneB;                          // one buffer
+  static constexpr size_t kRawOff = 2 * (size_t)kPlaneBuf;
+  static constexpr size_t kSmem = kRawOff + sizeof(float) * kStages * (kRawA + kRawB);
+  static constexpr uint32_t kIdesc = umma_idesc_tf32(kTM, TN);
+};
 constexpr int kSK = kTK + 4;
-constexpr int kRawA = (kTM * kSK > kTK * (kTM + 8)) ? kTM * kSK : kTK * (kTM + 8);   // floats
-constexpr int kRawB = (kTN * kSK > kTK * (kTN + 8)) ? kTN * kSK : kTK * (kTN + 8);
-constexpr int kPlaneA = kTM * kTK * 4, kPlaneB = kTN * kTK * 4;                       // bytes
-constexpr int kPlaneBuf = 2 * kPlaneA + 2 * kPlaneB;                                  // one buffer
-constexpr size_t kRawOff = 2 * (size_t)kPlaneBuf;
-constexpr size_t kAdaptSmemBytes = 1024 + kRawOff + sizeof(float) * kStages * (kRawA + kRawB);
-constexpr uint32_t kTmemCols = kNAcc * kTN;   // 256
-constexpr uint32_t kIdesc = umma_idesc_tf32(kTM, kTN);
+constexpr size_t kAdaptSmemBytes =
+    1024 + (TileCfg<64>::kSmem > TileCfg<128>::kSmem ? TileCfg<64>::kSmem : TileCfg<128>::kSmem);
+constexpr uint32_t kTmemCols = kNAcc * 128;   // 512: four accumulators of the widest tile
+constexpr int kBigBatch = 4096;               // B >= this: N = 128 tiles
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
@@ -158,19 +168,24 @@ struct TcState {
   uint32_t tiles;        // issuer: MMA tiles issued
 };
 
-// One 128 x 64 output tile (or one K range of it for split-K) on tcgen05, 3xTF32. Per K slice of
+// One 128 x 128 output tile (or one K range of it for split-K) on tcgen05, 3xTF32. Per K slice of
 // 32: the CTA stages the raw fp32 operands (cp.async, kStages deep), splits them once into tf32
 // big/small SW128 planes (double-buffered, so the split of slice i+1 overlaps the MMAs of slice i),
-// and one elected thread issues 4 K-steps x 3 products of M128 N64 K8 into TMEM accumulator
+// and one elected thread issues 4 K-steps x 3 products of M128 N128 K8 into TMEM accumulator
 // (slice % 4); tcgen05.commit frees the plane buffer. The epilogue sums the 4 accumulators in
 // fixed order with IEEE adds (long accumulations inside the tensor core lose ~1e-3 on the
 // gradients) and applies the mode. Deterministic: fixed issue and summation order.
+template <int TN>
 __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
-  const int tiles_n = (g.N + kTN - 1) / kTN;
+  using T = TileCfg<TN>;
+  constexpr int kStages = T::kStages, kRawA = T::kRawA, kRawB = T::kRawB;
+  constexpr int kPlaneA = T::kPlaneA, kPlaneB = T::kPlaneB, kPlaneBuf = T::kPlaneBuf;
+  constexpr uint32_t kIdesc = T::kIdesc;
+  const int tiles_n = (g.N + TN - 1) / TN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
   const int split = g.ksplit > 1 ? work / tiles_mn : 0;
   const int tile = work % tiles_mn;
-  const int m0 = (tile / tiles_n) * kTM, n0 = (tile % tiles_n) * kTN;
+  const int m0 = (tile / tiles_n) * kTM, n0 = (tile % tiles_n) * TN;
   int kbeg = 0, kend = g.K;
   if (g.ksplit > 1) {
     const int chunk = ((g.K + g.ksplit - 1) / g.ksplit + kTK - 1) / kTK * kTK;
@@ -194,7 +209,7 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
         const uint32_t buf = pbase + b * kPlaneBuf;
         const uint64_t ab = umma_desc_sw128(buf), as = umma_desc_sw128(buf + kPlaneA);
         const uint64_t bb = umma_desc_sw128(buf + 2 * kPlaneA), bs = umma_desc_sw128(buf + 2 * kPlaneA + kPlaneB);
-        const uint32_t d = ts.tmem + static_cast<uint32_t>((it % kNAcc) * kTN);
+        const uint32_t d = ts.tmem + static_cast<uint32_t>((it % kNAcc) * TN);
         const uint32_t first = it < kNAcc ? 1u : 0u;   // first slice of this accumulator in the tile
 #pragma unroll
         for (int ks = 0; ks < kTK / 8; ++ks) {          // K = 8 tf32 = 32 bytes per step
@@ -212,14 +227,14 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   }
   // ---------------- workers (warps 0-7): stage raw slices, split into planes, epilogue
   const bool a_kc = g.lak == 1, b_kc = g.lbk == 1;
-  float* raw = reinterpret_cast<float*>(smem + kRawOff);
+  float* raw = reinterpret_cast<float*>(smem + T::kRawOff);
   auto rawA = [&](int st) { return raw + st * (kRawA + kRawB); };
   auto rawB = [&](int st) { return raw + st * (kRawA + kRawB) + kRawA; };
   auto issue = [&](int it) {
     if (it < nk) {
       const int k0 = kbeg + it * kTK, st = it % kStages;
       stage_slice<kTM>(rawA(st), g.A, g.lam, g.lak, g.M, m0, k0, kend);
-      stage_slice<kTN>(rawB(st), g.Bm, g.lbn, g.lbk, g.N, n0, k0, kend);
+      stage_slice<TN>(rawB(st), g.Bm, g.lbn, g.lbk, g.N, n0, k0, kend);
     }
     cp_async_commit();   // (empty groups keep the wait arithmetic uniform)
   };
@@ -234,7 +249,7 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
     if (ts.fills[b] > 0) mbar_wait(&ts.empty[b], (ts.fills[b] - 1) & 1);   // MMAs on buffer b's last fill done
     uint8_t* buf = smem + b * kPlaneBuf;
     split_slice<kTM>(rawA(it % kStages), a_kc, buf, buf + kPlaneA);
-    split_slice<kTN>(rawB(it % kStages), b_kc, buf + 2 * kPlaneA, buf + 2 * kPlaneA + kPlaneB);
+    split_slice<TN>(rawB(it % kStages), b_kc, buf + 2 * kPlaneA, buf + 2 * kPlaneA + kPlaneB);
     fence_proxy_async_smem();   // generic-proxy plane writes -> visible to the tensor core
     __syncwarp();
     if (lane == 0) mbar_arrive(&ts.full[b]);
@@ -246,48 +261,50 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
     mbar_wait(&ts.empty[bl], (ts.fills[bl] - 1) & 1);
   }
   tc_fence_after();
-  // epilogue: warp w reads TMEM lane quadrant w % 4 (rows) and column half w / 4 of every accumulator
-  const int quad = warp & 3, half = warp >> 2;
-  const int m = m0 + quad * 32 + lane;
-  const int nb = n0 + half * 32;
-  float v[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = 0.f;
+  // epilogue: warp w reads TMEM lane quadrant w % 4 (rows) and column groups w / 4, w / 4 + 2 (32
+  // columns each) of every accumulator, sums the accumulators in fixed order, and writes through
+  // a shared-memory transpose (the raw ring is idle now) so that lanes run along n: bias, mask and
+  // C accesses become one coalesced 128-byte row per instruction
+  const int quad = warp & 3;
   const int nacc = nk < kNAcc ? nk : kNAcc;
-  for (int a = 0; a < nacc; ++a) {
-    uint32_t r[32];
-    tmem_ld32(ts.tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * kTN + half * 32), r);
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
-  }
-  if (nk > 0) {   // accumulators read: the issuer may start the next tile
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(ts.acc_free);
-  }
-  // transpose the warp's 32 x 32 block through shared memory (the raw ring is idle now) so that
-  // lanes run along n: bias, mask and C accesses become one coalesced 128-byte row per instruction
-  (void)m;
   float* tr = raw + warp * (32 * 33);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = v[i];
-  __syncwarp();
-  const int n = nb + lane;
   float* C = g.C + (g.ksplit > 1 ? split * g.cpart : 0);
-  const float bn = (g.mode == 0 && n < g.N) ? g.bias[n] : 0.f;
   const int mrow0 = m0 + quad * 32;
-  for (int r = 0; r < 32; ++r) {
-    const int mr = mrow0 + r;
-    if (mr >= g.M) break;
-    if (n < g.N) {
-      float x = tr[r * 33 + lane];
-      if (g.mode == 0) x = relu(x + bn);
-      else if (g.mode == 1) x = g.mask[(long long)mr * g.ldmask + n] > 0.f ? x : 0.f;
-      C[(long long)mr * g.ldc + n] = x;
+#pragma unroll 1
+  for (int t = 0; t < TN / 64; ++t) {
+    const int cg = (warp >> 2) + 2 * t;
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    for (int a = 0; a < nacc; ++a) {
+      uint32_t r[32];
+      tmem_ld32(ts.tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * TN + cg * 32), r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += __uint_as_float(r[i]);
     }
+    if (nk > 0 && t == TN / 64 - 1) {   // accumulators read: the issuer may start the next tile
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ts.acc_free);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tr[lane * 33 + i] = v[i];
+    __syncwarp();
+    const int n = n0 + cg * 32 + lane;
+    const float bn = (g.mode == 0 && n < g.N) ? g.bias[n] : 0.f;
+    for (int rr = 0; rr < 32; ++rr) {
+      const int mr = mrow0 + rr;
+      if (mr >= g.M) break;
+      if (n < g.N) {
+        float x = tr[rr * 33 + lane];
+        if (g.mode == 0) x = relu(x + bn);
+        else if (g.mode == 1) x = g.mask[(long long)mr * g.ldmask + n] > 0.f ? x : 0.f;
+        C[(long long)mr * g.ldc + n] = x;
+      }
+    }
+    __syncwarp();
   }
-  __syncwarp();
 }
 
 #ifdef AB_STATS
@@ -440,6 +457,12 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   TcState ts{s_tmem, &s_bar[0], &s_bar[2], &s_bar[4], {0u, 0u}, {0u, 0u}, 0u};
+  const bool big = p.B >= kBigBatch;   // uniform: every CTA takes the same tile width
+  auto tiles = [&](const Gemm& g) { return big ? g.tiles<128>() : g.tiles<64>(); };
+  auto gemm = [&](const Gemm& g, int t) {
+    if (big) gemm_tile<128>(g, t, smem, ts);
+    else gemm_tile<64>(g, t, smem, ts);
+  };
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
   unsigned int gen = 0;
@@ -480,7 +503,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
 #ifdef AB_STATS
       const long long tw0 = clock64();
 #endif
-      for (int t = blockIdx.x; t < g.tiles(); t += gridDim.x) gemm_tile(g, t, smem, ts);
+      for (int t = blockIdx.x; t < tiles(g); t += gridDim.x) gemm(g, t);
 #ifdef AB_STATS
       if (k == 2 && step == 0 && threadIdx.x == 0 && blockIdx.x < 1024) {
         unsigned smid;
@@ -518,10 +541,10 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
     {
       Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
       Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H};
-      const int t1 = gw.tiles(), t2 = gd.tiles();
+      const int t1 = tiles(gw), t2 = tiles(gd);
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, smem, ts);
-        else gemm_tile(gd, t - t1, smem, ts);
+        if (t < t1) gemm(gw, t);
+        else gemm(gd, t - t1);
       }
       colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
       grid_sync(p.barrier, gen);
@@ -532,16 +555,16 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       const float* in = k == 1 ? Z : Hk(k - 1);
       const float* Dk = D[k & 1];
       Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
-      const int t1 = gw.tiles();
+      const int t1 = tiles(gw);
       int t2 = 0;
       Gemm gd{};
       if (k > 1) {
         gd = Gemm{B, H, H, Dk, H, 1, P + p.off.W[k], H, 1, D[(k - 1) & 1], H, 1, nullptr, Hk(k - 1), H};
-        t2 = gd.tiles();
+        t2 = tiles(gd);
       }
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm_tile(gw, t, smem, ts);
-        else gemm_tile(gd, t - t1, smem, ts);
+        if (t < t1) gemm(gw, t);
+        else gemm(gd, t - t1);
       }
       colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
       // SGD of the layer above, whose gradient partials completed in the previous phase and whose
