@@ -16,6 +16,6 @@ example of the meta-network); only computation-given-weights is pinned.
 from .metanet import (  # noqa: F401
     encode_candidate, encode_grid, encode_job, encode_jobs, lstm_step, head_forward,
     speed, score_matrix, score_pairs, argmax_rows, loss_norm, adapt, head_loss_and_grad,
-    HEAD_PARAMS, train, topk_rows,
+    HEAD_PARAMS, train, topk_rows, encoder_grad, ENCODER_PARAMS,
 )
 from .trigger import trigger_decide, KEEP, RECONFIGURE, ADAPT  # noqa: F401,E402

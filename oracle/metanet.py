@@ -210,7 +210,69 @@ def HEAD_PARAMS(W):
     return names + ["W_o", "b_o"]
 
 
-def head_loss_and_grad(W, Z_in: np.ndarray, V_bar: np.ndarray, n: np.ndarray):
+ENCODER_PARAMS = ["E_m", "E_arc", "W_e", "b_e", "lstm1_Wx", "lstm1_Wh", "lstm1_b", "lstm2_Wx", "lstm2_Wh", "lstm2_b"]
+
+
+def encoder_grad(W, jobs, dX: np.ndarray):
+    """Gradients of the encoder parameters given dX[b] = d objective / d x_b (SURVEY NEXT 4
+    "encoder fine-tuning"; R#20): back-propagation through time of the two-layer LSTM of
+    encode_job (P:402, R#5), the per-layer embedding W_e, b_e (R#4) and the type tables E_m, E_arc
+    (R#6); the bandwidth / n / l features carry no parameters. Written step by step in reverse
+    time order from the forward's stashed gates and states."""
+    g = {k: np.zeros_like(_f64(W[k])) for k in ENCODER_PARAMS}
+    Wx1, Wh1, b1 = _f64(W["lstm1_Wx"]), _f64(W["lstm1_Wh"]), _f64(W["lstm1_b"])
+    Wx2, Wh2, b2 = _f64(W["lstm2_Wx"]), _f64(W["lstm2_Wh"]), _f64(W["lstm2_b"])
+    We, be = _f64(W["W_e"]), _f64(W["b_e"])
+    hd = Wh1.shape[1]
+
+    def gates(Wx, Wh, b, x, h, c):
+        z = Wx @ x + Wh @ h + b
+        i, f = _sigmoid(z[:hd]), _sigmoid(z[hd:2 * hd])
+        gg, o = np.tanh(z[2 * hd:3 * hd]), _sigmoid(z[3 * hd:])
+        c_new = f * c + i * gg
+        return (i, f, gg, o), c_new, o * np.tanh(c_new)
+
+    def back(acts, c_prev, c_new, dh, dc, x, h_prev, Wx, Wh, kx, kh, kb):
+        i, f, gg, o = acts
+        tc = np.tanh(c_new)
+        do = dh * tc
+        dc = dc + dh * o * (1.0 - tc * tc)
+        dz = np.concatenate([dc * gg * i * (1.0 - i), dc * c_prev * f * (1.0 - f),
+                             dc * i * (1.0 - gg * gg), do * o * (1.0 - o)])
+        g[kx] += np.outer(dz, x)
+        g[kh] += np.outer(dz, h_prev)
+        g[kb] += dz
+        return Wx.T @ dz, Wh.T @ dz, dc * f          # d input, d h_prev, d c_prev
+
+    for bi in range(jobs.J):
+        n, l = int(jobs.n[bi]), int(jobs.l[bi])
+        valid = np.arange(N_MAX) < n
+        T = _f64(jobs.T[bi])
+        h1 = np.zeros(hd); c1 = np.zeros(hd); h2 = np.zeros(hd); c2 = np.zeros(hd)
+        st = []
+        for i in range(l):                           # forward with stash (as encode_job)
+            t_feat = np.where(valid, np.log2(1.0 + np.where(valid, T[i], 0.0) / 1.0), 0.0)
+            e = We @ t_feat + be
+            a1, c1n, h1n = gates(Wx1, Wh1, b1, e, h1, c1)
+            a2, c2n, h2n = gates(Wx2, Wh2, b2, h1n, h2, c2)
+            st.append((t_feat, e, h1, c1, a1, c1n, h1n, h2, c2, a2, c2n))
+            h1, c1, h2, c2 = h1n, c1n, h2n, c2n
+        dx = _f64(dX[bi])
+        dh2, dc2 = dx[:hd].copy(), np.zeros(hd)
+        dh1, dc1 = np.zeros(hd), np.zeros(hd)
+        for i in range(l - 1, -1, -1):               # BPTT
+            t_feat, e, h1p, c1p, a1, c1n, h1n, h2p, c2p, a2, c2n = st[i]
+            dx2, dh2, dc2 = back(a2, c2p, c2n, dh2, dc2, h1n, h2p, Wx2, Wh2, "lstm2_Wx", "lstm2_Wh", "lstm2_b")
+            de, dh1, dc1 = back(a1, c1p, c1n, dh1 + dx2, dc1, e, h1p, Wx1, Wh1, "lstm1_Wx", "lstm1_Wh", "lstm1_b")
+            g["W_e"] += np.outer(de, t_feat)
+            g["b_e"] += de
+        te = W["E_m"].shape[1]
+        g["E_m"][int(jobs.m[bi])] += dx[hd + 2 * N_MAX + 2: hd + 2 * N_MAX + 2 + te]
+        g["E_arc"][int(jobs.arc[bi])] += dx[hd + 2 * N_MAX + 2 + te:]
+    return g
+
+
+def head_loss_and_grad(W, Z_in: np.ndarray, V_bar: np.ndarray, n: np.ndarray, want_dz: bool = False):
     """Objective (R#12): (1/B) sum_b 1/2 ||r_b||^2 with r_b = (V_hat_b - V_bar_b) masked to
     the n_b valid workers; its gradient w.r.t. every head parameter by the chain rule (the
     encoder is frozen, R#13). Returns (objective, mean Eq.2 norm, grads)."""
@@ -231,6 +293,8 @@ def head_loss_and_grad(W, Z_in: np.ndarray, V_bar: np.ndarray, n: np.ndarray):
         g[f"b{k}"] = delta.sum(axis=0)
         if k > 1:
             delta = (delta @ _f64(W[f"W{k}"])) * (zs[k - 2] > 0)   # uses the pre-update W_k
+    if want_dz:                                   # d obj / d [x | u], the input of layer 1
+        return obj, float(norms.mean()), g, delta @ _f64(W["W1"])
     return obj, float(norms.mean()), g
 
 
@@ -257,7 +321,7 @@ def adapt(W, batch, lr: float, steps: int):
 
 
 def train(W, batch, steps: int, optimizer: str = "adam", lr: float = 1e-3, beta1: float = 0.9,
-          beta2: float = 0.999, eps: float = 1e-8, state=None):
+          beta2: float = 0.999, eps: float = 1e-8, state=None, scope: str = "head"):
     """Offline training of the head on one minibatch (P:418 "Offline training online adapting";
     P:415 the meta-network trained on collected runtime samples; optimiser R#18): `steps` updates
     of every head parameter (encoder frozen, as in adapt) on the objective of R#12.
@@ -265,22 +329,29 @@ def train(W, batch, steps: int, optimizer: str = "adam", lr: float = 1e-3, beta1
       "adam": t <- t + 1; m <- b1 m + (1 - b1) g; v <- b2 v + (1 - b2) g^2;
               theta <- theta - lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
     `state` = {"t": int, "m": {name: array}, "v": {name: array}} carries the Adam moments across
-    calls (None = fresh, all zero). Returns (new weights, new state, [mean Eq.2 norm before each
-    step])."""
+    calls (None = fresh, all zero). scope = "all" also trains the encoder (NEXT 4 "encoder
+    fine-tuning", R#20) with the BPTT gradients of encoder_grad. Returns (new weights, new state,
+    [mean Eq.2 norm before each step])."""
     Wn = {k: _f64(v).copy() for k, v in W.items()}
-    names = HEAD_PARAMS(Wn)
+    names = HEAD_PARAMS(Wn) + (ENCODER_PARAMS if scope == "all" else [])
     if state is None:
         state = {"t": 0, "m": {k: np.zeros_like(Wn[k]) for k in names}, "v": {k: np.zeros_like(Wn[k]) for k in names}}
     else:
         state = {"t": int(state["t"]), "m": {k: _f64(a).copy() for k, a in state["m"].items()},
                  "v": {k: _f64(a).copy() for k, a in state["v"].items()}}
     jobs = batch.jobs
-    X = encode_jobs(Wn, jobs)
     U = np.stack([encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(jobs.J)])
-    Z_in = np.concatenate([X, U], axis=1)
+    X = encode_jobs(Wn, jobs)
     losses = []
     for _ in range(int(steps)):
-        _, norm_mean, g = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
+        if scope == "all":                        # the encoder moves: re-encode every step
+            X = encode_jobs(Wn, jobs)
+        Z_in = np.concatenate([X, U], axis=1)
+        if scope == "all":
+            _, norm_mean, g, dZ = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n, want_dz=True)
+            g.update(encoder_grad(Wn, jobs, dZ[:, :X.shape[1]]))
+        else:
+            _, norm_mean, g = head_loss_and_grad(Wn, Z_in, batch.V_bar, jobs.n)
         losses.append(norm_mean)
         if optimizer == "sgd":
             for k in names:

@@ -400,3 +400,77 @@ def test_topk_closed_forms():
     assert np.array_equal(oracle.topk_rows(s, 3)[0][0], [9, 8, 7])
     assert np.array_equal(oracle.topk_rows(-s, 3)[0][0], [0, 1, 2])
     assert np.array_equal(oracle.topk_rows(np.zeros((1, 5)), 7)[0][0], [0, 1, 2, 3, 4, -1, -1])
+
+
+# ---------------------------------------------------------------- encoder fine-tuning (NEXT 4)
+def _torch_full_model_grads(W, batch, L):
+    """Objective of R#12 through torch.nn.LSTM / Linear / autograd in float64 (gate order i,f,g,o;
+    bias_hh = 0 so bias_ih plays the single LSTM bias); returns every parameter's gradient."""
+    d = torch.float64
+    P = {k: torch.tensor(np.asarray(W[k], np.float64), requires_grad=True) for k in W}
+    lstm = torch.nn.LSTM(16, 32, num_layers=2, batch_first=True).double()
+    with torch.no_grad():
+        for layer in (0, 1):
+            getattr(lstm, f"bias_hh_l{layer}").zero_()
+    params = dict(lstm.named_parameters())
+    jobs = batch.jobs
+    loss = 0.0
+    for b in range(jobs.J):
+        n, l = int(jobs.n[b]), int(jobs.l[b])
+        valid = torch.arange(16) < n
+        Tt = torch.tensor(np.asarray(jobs.T[b][:l], np.float64))
+        feat = torch.where(valid, torch.log2(1.0 + torch.where(valid, Tt, torch.zeros_like(Tt))), torch.zeros_like(Tt))
+        e = feat @ P["W_e"].T + P["b_e"]
+        h = torch.zeros(2, 1, 32, dtype=d); c = torch.zeros(2, 1, 32, dtype=d)
+        out, (hn, cn) = torch.func.functional_call(
+            lstm, {"weight_ih_l0": P["lstm1_Wx"], "weight_hh_l0": P["lstm1_Wh"], "bias_ih_l0": P["lstm1_b"],
+                   "bias_hh_l0": params["bias_hh_l0"], "weight_ih_l1": P["lstm2_Wx"], "weight_hh_l1": P["lstm2_Wh"],
+                   "bias_ih_l1": P["lstm2_b"], "bias_hh_l1": params["bias_hh_l1"]}, (e[None], (h, c)))
+        bd = torch.where(valid, torch.log2(torch.where(valid, torch.tensor(np.asarray(jobs.B_d[b], np.float64)),
+                                                        torch.ones(16, dtype=d))), torch.zeros(16, dtype=d))
+        bu = torch.where(valid, torch.log2(torch.where(valid, torch.tensor(np.asarray(jobs.B_u[b], np.float64)),
+                                                        torch.ones(16, dtype=d))), torch.zeros(16, dtype=d))
+        x = torch.cat([hn[1, 0], bd, bu, torch.tensor([n / 16.0, l / 64.0], dtype=d),
+                       P["E_m"][int(jobs.m[b])], P["E_arc"][int(jobs.arc[b])]])
+        u = torch.tensor(oracle.encode_candidate(batch.S_p[b], batch.S_c[b]))
+        z = torch.cat([x, u])
+        for k in range(1, L + 1):
+            z = torch.relu(P[f"W{k}"] @ z + P[f"b{k}"])
+        V = P["W_o"] @ z + P["b_o"]
+        r = (V - torch.tensor(np.asarray(batch.V_bar[b], np.float64))) * (torch.arange(16) < n)
+        loss = loss + 0.5 * (r * r).sum() / jobs.J
+    loss.backward()
+    return {k: P[k].grad.numpy() for k in P if P[k].grad is not None}
+
+
+@pytest.mark.parametrize("L", [1, 3])
+def test_encoder_bptt_matches_torch_autograd(L):
+    """encoder_grad (hand-written BPTT) + head_loss_and_grad(want_dz) == torch autograd through
+    torch.nn.LSTM for every parameter of the network, on jobs of different lengths and widths."""
+    desc = synth.NetDesc(L, 12)
+    W = synth.make_weights(desc, seed=60 + L)
+    batch = _tiny_batch(61 + L, J=4)
+    batch.jobs.l[:] = [3, 1, 5, 2]
+    X = oracle.encode_jobs(W, batch.jobs)
+    U = np.stack([oracle.encode_candidate(batch.S_p[b], batch.S_c[b]) for b in range(batch.jobs.J)])
+    _, _, g, dZ = oracle.head_loss_and_grad(W, np.concatenate([X, U], 1), batch.V_bar, batch.jobs.n, want_dz=True)
+    g.update(oracle.encoder_grad(W, batch.jobs, dZ[:, :82]))
+    ref = _torch_full_model_grads(W, batch, L)
+    for k in oracle.HEAD_PARAMS(W) + oracle.ENCODER_PARAMS:
+        np.testing.assert_allclose(g[k], ref[k], rtol=1e-9, atol=1e-13, err_msg=k)
+
+
+def test_train_scope_all_moves_the_encoder_and_descends():
+    desc = synth.NetDesc(2, 16)
+    W = synth.make_weights(desc, seed=9)
+    batch = _tiny_batch(71, J=6)
+    Wh, _, lh = oracle.train(W, batch, 1, "sgd", lr=1e-2)
+    Wa, _, la = oracle.train(W, batch, 1, "sgd", lr=1e-2, scope="all")
+    assert lh[0] == la[0]
+    for k in oracle.HEAD_PARAMS(W):          # same head update (the encoder gradient is separate)
+        np.testing.assert_allclose(Wa[k], Wh[k], rtol=1e-13, atol=0)
+    for k in oracle.ENCODER_PARAMS:
+        assert np.array_equal(Wh[k], W[k].astype(np.float64)), k
+    assert any(not np.array_equal(Wa[k], W[k].astype(np.float64)) for k in oracle.ENCODER_PARAMS)
+    _, _, l2 = oracle.train(Wa, batch, 1, "sgd", lr=0.0, scope="all")
+    assert l2[0] < la[0]
