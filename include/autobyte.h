@@ -210,12 +210,16 @@ autobyte_status autobyte_adapt(autobyte_ctx* ctx, const autobyte_job_stats* samp
  * no launch. Deterministic (fixed summation order); the bf16 shadows are refreshed in stream
  * order. */
 typedef enum { AB_OPT_SGD = 0, AB_OPT_ADAM = 1 } autobyte_opt_kind;
+typedef enum { AB_SCOPE_HEAD = 0, AB_SCOPE_ALL = 1 } autobyte_train_scope;
 typedef struct {
   int32_t kind;    /* autobyte_opt_kind */
   float lr;
   float beta1;     /* Adam only; typical 0.9 */
   float beta2;     /* Adam only; typical 0.999 */
   float eps;       /* Adam only; typical 1e-8 */
+  int32_t scope;   /* autobyte_train_scope: AB_SCOPE_ALL also fine-tunes the encoder (SURVEY NEXT 4,
+                      R#20) by back-propagation through time of the LSTM; the samples are then
+                      re-encoded every step (single-rank semantics; replicas stay identical) */
 } autobyte_optimizer;
 autobyte_status autobyte_train(autobyte_ctx* ctx, const autobyte_job_stats* samples,
                                const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,

@@ -48,9 +48,9 @@ class Grid(ctypes.Structure):
 
 
 class Optimizer(ctypes.Structure):
-    """autobyte_optimizer: kind 0 = SGD, 1 = Adam (R#18)."""
+    """autobyte_optimizer: kind 0 = SGD, 1 = Adam (R#18); scope 0 = head, 1 = encoder too (R#20)."""
     _fields_ = [("kind", ctypes.c_int32), ("lr", ctypes.c_float), ("beta1", ctypes.c_float),
-                ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("scope", ctypes.c_int32)]
 
 
 OPT_SGD, OPT_ADAM = 0, 1
@@ -332,12 +332,13 @@ class AutoByte:
         return idx, score
 
     def train(self, samples: DeviceJobs, S_p, S_c, V_bar, steps: int, optimizer: str = "adam", lr: float = 1e-3,
-              beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, want_losses: bool = True):
+              beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, want_losses: bool = True,
+              scope: str = "head"):
         """Offline training of the head on one minibatch (autobyte_train): `steps` SGD or Adam
         updates; returns the per-step mean Eq. 2 norms before each update (device tensor)."""
         import torch
         kind = {"sgd": OPT_SGD, "adam": OPT_ADAM}[optimizer]
-        opt = Optimizer(kind, lr, beta1, beta2, eps)
+        opt = Optimizer(kind, lr, beta1, beta2, eps, {"head": 0, "all": 1}[scope])
         losses = torch.empty(max(int(steps), 1), dtype=torch.float32, device=self.torch_device) if want_losses else None
         js = samples.struct()
         self._check(self.lib.autobyte_train(self.ctx, ctypes.byref(js), S_p.data_ptr(), S_c.data_ptr(),

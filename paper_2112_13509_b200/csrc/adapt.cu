@@ -561,6 +561,9 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       if (k > 1) {
         gd = Gemm{B, H, H, Dk, H, 1, P + p.off.W[k], H, 1, D[(k - 1) & 1], H, 1, nullptr, Hk(k - 1), H};
         t2 = tiles(gd);
+      } else if (p.dz_out) {   // encoder fine-tuning: d obj / d [x | u] = D_1 W1 (pre-update W1)
+        gd = Gemm{B, kZDim, H, Dk, H, 1, P + p.off.W[1], kZDim, 1, p.dz_out, kZDim, 2, nullptr, nullptr, 0, 1, 0};
+        t2 = tiles(gd);
       }
       for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
         if (t < t1) gemm(gw, t);

@@ -80,6 +80,7 @@ struct autobyte_ctx {
   DevBuf<float> jobvec, x, adapt_ws, loss_tmp;
   DevBuf<float> opt_m, opt_v;        // Adam moments (autobyte_train), blob layout
   DevBuf<float> topk_scores;         // [J][shard] score matrix of autobyte_topk
+  DevBuf<float> enc_stash, enc_dz, enc_part;   // encoder fine-tuning: K1a stash, dX [B][84], K8 partials
   DevBuf<unsigned long long> topk_keys;   // [G][J][k] per-rank top-k keys
   long long opt_t = 0;               // Adam step count
   DevBuf<float2> u;                  // [shard] candidate encodings (K0)
@@ -403,6 +404,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
   c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
   c->opt_m.release(); c->opt_v.release(); c->topk_scores.release(); c->topk_keys.release();
+  c->enc_stash.release(); c->enc_dz.release(); c->enc_part.release();
   c->loss_tmp.release(); c->keys.release();
   c->sT.release(); c->sBd.release(); c->sBu.release(); c->sSc.release(); c->sV.release();
   c->rScore.release(); c->rCur.release();
@@ -607,11 +609,59 @@ autobyte_status autobyte_train(autobyte_ctx* c, const autobyte_job_stats* sample
   if (opt->kind == AB_OPT_ADAM && !(opt->beta1 >= 0.f && opt->beta1 < 1.f && opt->beta2 >= 0.f && opt->beta2 < 1.f &&
                                     opt->eps > 0.f && std::isfinite(opt->eps)))
     return fail(c, AB_E_INVALID, "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
+  if (opt->scope != AB_SCOPE_HEAD && opt->scope != AB_SCOPE_ALL) return fail(c, AB_E_INVALID, "unknown train scope");
   DeviceGuard guard(c->device);
   if ((s = device_checks(c, samples, nullptr)) != AB_OK) return s;
   if (steps == 0) return AB_OK;
-  return run_head_update(c, samples, sp_bytes, sc_mult, v_obs, opt->kind, opt->lr, opt->beta1, opt->beta2, opt->eps,
-                         steps, nullptr, losses);
+  if (opt->scope == AB_SCOPE_HEAD)
+    return run_head_update(c, samples, sp_bytes, sc_mult, v_obs, opt->kind, opt->lr, opt->beta1, opt->beta2,
+                           opt->eps, steps, nullptr, losses);
+  // AB_SCOPE_ALL (R#20): per step K1a with stash -> K4 (1 step, dX out, head update) -> K8 BPTT
+  // partials -> K9 encoder update; the samples are re-encoded with the updated encoder each step
+  const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
+  AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
+  AB_CUDA(c, c->x.ensure((size_t)B * kXDim));
+  AB_CUDA(c, c->enc_stash.ensure((size_t)B * samples->l_max * kEncStash));
+  AB_CUDA(c, c->enc_dz.ensure((size_t)B * kZDim));
+  AB_CUDA(c, c->enc_part.ensure((size_t)encoder_bwd_parts(B, c->num_sms) * c->off.W[1]));
+  if (opt->kind == AB_OPT_ADAM && !c->opt_m.ptr) {
+    AB_CUDA(c, c->opt_m.ensure(c->off.total));
+    AB_CUDA(c, c->opt_v.ensure(c->off.total));
+    AB_CUDA(c, cudaMemsetAsync(c->opt_m.ptr, 0, c->off.total * sizeof(float), c->stream));
+    AB_CUDA(c, cudaMemsetAsync(c->opt_v.ptr, 0, c->off.total * sizeof(float), c->stream));
+  }
+  for (int32_t st = 0; st < steps; ++st) {
+    EncodeParams ep = encode_params(c, samples);
+    ep.x_out = c->x.ptr;
+    ep.j_begin = 0; ep.j_end = B;
+    ep.stash = c->enc_stash.ptr;
+    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
+    AdaptParams ap{};
+    ap.B = B; ap.H = H; ap.L = L; ap.steps = 1; ap.lr = opt->lr;
+    ap.x = c->x.ptr; ap.S_p = reinterpret_cast<const long long*>(sp_bytes); ap.S_c = sc_mult; ap.v_obs = v_obs;
+    ap.n = samples->n_workers;
+    ap.params = c->params.ptr; ap.off = c->off; ap.ws = c->adapt_ws.ptr; ap.grads = c->grads.ptr;
+    ap.losses = losses ? losses + st : nullptr; ap.barrier = c->barrier.ptr;
+    ap.opt = opt->kind; ap.beta1 = opt->beta1; ap.beta2 = opt->beta2; ap.eps = opt->eps;
+    ap.m = c->opt_m.ptr; ap.v = c->opt_v.ptr; ap.t0 = c->opt_t;
+    ap.dz_out = c->enc_dz.ptr;
+    int grid_used = 0;
+    AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
+    int nparts = 0;
+    AB_CUDA(c, timed(c, K_ADAPT, [&] {
+              return launch_encoder_bwd(ep, c->enc_dz.ptr, kZDim, c->enc_part.ptr, c->num_sms, &nparts, c->stream);
+            }));
+    AB_CUDA(c, timed(c, K_ADAPT, [&] {
+              return launch_encoder_update(ep, c->enc_dz.ptr, kZDim, B, c->enc_part.ptr, nparts, opt->kind, opt->lr,
+                                           opt->beta1, opt->beta2, opt->eps, c->opt_t + 1, c->opt_m.ptr,
+                                           c->opt_v.ptr, c->stream);
+            }));
+    if (opt->kind == AB_OPT_ADAM) c->opt_t += 1;
+  }
+  AB_CUDA(c, timed(c, K_PACK, [&] {
+            return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
+          }));
+  return AB_OK;
 }
 
 autobyte_status autobyte_reset_optimizer(autobyte_ctx* c) {

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   for (int k = 0; k < C::NJ; ++k) lmax = max(lmax, sL[k]);
 
   // gates of one layer for the HJ jobs of this half: z = b + Wx in + Wh h  (4 partial sums)
-  auto cell_update = [&](float (*sHout)[kLstm], float* cst, int step) {
+  // (stash, for encoder fine-tuning: per job and step [e | i f g o c h of layer 1 | of layer 2])
+  auto cell_update = [&](float (*sHout)[kLstm], float* cst, int step, int soff) {
 #pragma unroll
     for (int r = 0; r < C::RC; ++r) {
       const int e = tid + r * kEncThreads;
@@ -102,7 +103,13 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
           const float ig = sigmoidf_acc(sG[jj][u]), fg = sigmoidf_acc(sG[jj][kLstm + u]);
           const float gg = tanh_acc(sG[jj][2 * kLstm + u]), og = sigmoidf_acc(sG[jj][3 * kLstm + u]);
           cst[r] = fmaf(fg, cst[r], ig * gg);
-          sHout[jj][u] = og * tanh_acc(cst[r]);
+          const float h = og * tanh_acc(cst[r]);
+          sHout[jj][u] = h;
+          if (p.stash) {
+            float* st = p.stash + ((size_t)(j0 + jj) * p.l_max + step) * kEncStash + soff;
+            st[u] = ig; st[kLstm + u] = fg; st[2 * kLstm + u] = gg; st[3 * kLstm + u] = og;
+            st[4 * kLstm + u] = cst[r]; st[5 * kLstm + u] = h;
+          }
         }
       }
     }
@@ -126,6 +133,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 #pragma unroll
       for (int w = 0; w < kNMax; ++w) acc = fmaf(P[p.off.W_e + d * kNMax + w], sTl[jj][i][w], acc);
       sE[jj][i][d] = acc;
+      if (p.stash && jj < nj && i0 + i < sL[jj]) p.stash[((size_t)(j0 + jj) * p.l_max + i0 + i) * kEncStash + d] = acc;
     }
     __syncthreads();
     for (int i = 0; i < len; ++i) {
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 #pragma unroll
       for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
       __syncthreads();
-      cell_update(sH1, c1, i0 + i);
+      cell_update(sH1, c1, i0 + i, kEmbed);
       __syncthreads();
       // ---- layer 2 gates
 #pragma unroll
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 #pragma unroll
       for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
       __syncthreads();
-      cell_update(sH2, c2, i0 + i);
+      cell_update(sH2, c2, i0 + i, kEmbed + 6 * kLstm);
       __syncthreads();
     }
   }

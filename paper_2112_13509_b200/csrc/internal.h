@@ -19,6 +19,7 @@ constexpr int kXDim = AUTOBYTE_X_DIM;          // 82
 constexpr int kZDim = AUTOBYTE_X_DIM + 2;      // 84 = [x | u]
 constexpr int kMaxHidden = 8;
 constexpr int kTileM = 128;                    // candidates per tcgen05 tile (TMEM lanes)
+constexpr int kEncStash = kEmbed + 12 * kLstm; // floats stashed per job and layer step (e, 2 x [i f g o c h])
 
 // Offsets (in floats) of every parameter inside the fp32 master buffer (= blob payload order).
 struct ParamOffsets {
@@ -46,6 +47,7 @@ struct EncodeParams {
   float* beta_out;     // [J][jv]: mean of the first n entries of b_o, or null
   unsigned long long* keys;      // [J] reset to 0, or null
   unsigned long long* cur_keys;  // [J] reset to 0, or null
+  float* stash;        // [J][l_max][kEncStash] forward states for encoder fine-tuning, or null
 };
 
 struct alignas(64) ScoreParams {
@@ -91,6 +93,7 @@ struct AdaptParams {
   long long t0;            // Adam steps taken before this launch
   float* m;                // Adam first moments (blob layout, head part used) or null
   float* v;                // Adam second moments
+  float* dz_out;           // [B][84] d objective / d [x | u] (encoder fine-tuning) or null
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)
@@ -107,6 +110,12 @@ cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
+cudaError_t launch_encoder_bwd(const EncodeParams& p, const float* dX, int ldx, float* partial, int num_sms,
+                               int* nparts, cudaStream_t s);                                   // K8
+cudaError_t launch_encoder_update(const EncodeParams& p, const float* dX, int ldx, int B, const float* partial,
+                                  int nparts, int opt, float lr, float beta1, float beta2, float eps, long long t,
+                                  float* m, float* v, cudaStream_t s);                          // K9
+int encoder_bwd_parts(int B, int num_sms);
 cudaError_t launch_topk(int J, long long C, const float* scores, long long c_begin, int k, unsigned long long* out,
                         cudaStream_t s);                                                       // K6
 cudaError_t launch_topk_merge(int J, int G, int k, const unsigned long long* lists, int32_t* idx, float* score,

@@ -1,7 +1,7 @@
 """Throughput of offline head training (autobyte_train, Adam) at large minibatches: samples/s
 and algorithmic TFLOP/s of K4 (forward + weight-gradient + input-gradient GEMMs of the head,
 3 x 2 x (84 H + (L-1) H^2 + 16 H) FLOP per sample per step), timed with the library's CUDA
-events. Usage: python tools/train_bench.py [L] [H] [B,B,...] [steps]"""
+events. Usage: python tools/train_bench.py [L] [H] [B,B,...] [steps] [head|all]   (all: encoder fine-tuning too)"""
 import json
 import os
 import sys
@@ -20,6 +20,7 @@ def main():
     H = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     Bs = [int(b) for b in (sys.argv[3] if len(sys.argv) > 3 else "1024,8192,32768").split(",")]
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else 10
+    scope = sys.argv[5] if len(sys.argv) > 5 else "head"
     net = AutoByte(L, H, synth.make_weights(synth.NetDesc(L, H)), device=0)
     flop_per_sample = 3 * 2.0 * (84 * H + (L - 1) * H * H + 16 * H)
     for B in Bs:
@@ -28,17 +29,17 @@ def main():
         sp = torch.as_tensor(batch.S_p, device="cuda")
         sc = torch.as_tensor(batch.S_c, device="cuda")
         vb = torch.as_tensor(batch.V_bar, device="cuda")
-        net.train(dj, sp, sc, vb, 2, "adam", lr=1e-4)
+        net.train(dj, sp, sc, vb, 2, "adam", lr=1e-4, scope=scope)
         torch.cuda.synchronize()
         net.reset_profile()
         net.set_profiling(True)
-        losses = net.train(dj, sp, sc, vb, steps, "adam", lr=1e-4)
+        losses = net.train(dj, sp, sc, vb, steps, "adam", lr=1e-4, scope=scope)
         torch.cuda.synchronize()
         p = net.profile()
         net.set_profiling(False)
-        k4 = p["adapt_ms"] / max(p["adapt_launches"], 1)
-        step_ms = k4 / steps
-        print(json.dumps({"L": L, "H": H, "B": B, "steps": steps, "k4_ms_per_step": step_ms,
+        # head scope: one K4 launch runs all steps; all: per step K1a + K4 + K8 + K9 (+ one pack)
+        step_ms = (p["adapt_ms"] + (p["encode_ms"] if scope == "all" else 0.0)) / steps
+        print(json.dumps({"L": L, "H": H, "B": B, "scope": scope, "steps": steps, "ms_per_step": step_ms,
                           "samples_per_s": B / step_ms * 1e3, "tflops": flop_per_sample * B / step_ms / 1e9,
                           "encode_ms": p["encode_ms"], "loss_first": float(losses[0]), "loss_last": float(losses[-1])}),
               flush=True)
