@@ -595,3 +595,42 @@ def test_fp32_path_after_adapt():
     jobs, grid = synth.small_fleet(3, 9), synth.log_grid(6, 7)
     # the adapted fp32 masters differ from the oracle's float64 ones by ~1e-7; scores stay within 1e-4
     check_scores(gpu_scores(net, jobs, grid), oracle.score_matrix(W_ora, jobs, grid), RTOL32)
+
+
+# ------------------------------------------------------------------------------------- AUTOBYTE_CHECK
+def test_device_checks_reject_out_of_range_inputs():
+    """AUTOBYTE_CHECK=1 validates device data before any launch (include/autobyte.h): worker count,
+    layer count, type ids, positive bandwidths, non-negative times; grids with S_p >= 4 KB and
+    S_c >= 1, both strictly ascending. Valid inputs pass; each violation is AB_E_INVALID."""
+    import os
+    from paper_2112_13509_b200.autobyte import AB_E_INVALID, AutoByte, AutoByteError
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H))
+    os.environ["AUTOBYTE_CHECK"] = "1"
+    try:
+        net = AutoByte(L, H, W, device=0)
+    finally:
+        os.environ.pop("AUTOBYTE_CHECK", None)
+    jobs, grid = synth.small_fleet(5, 3), synth.log_grid(8, 8)
+    gpu_argmax(net, jobs, grid)   # valid: no error
+
+    def bad_jobs(mut):
+        j = jobs.subset(np.arange(5))
+        mut(j)
+        return j
+
+    cases = [lambda j: j.n.__setitem__(1, 0), lambda j: j.n.__setitem__(1, 17), lambda j: j.l.__setitem__(2, 0),
+             lambda j: j.l.__setitem__(2, j.T.shape[1] + 1), lambda j: j.m.__setitem__(0, 99),
+             lambda j: j.arc.__setitem__(0, 2), lambda j: j.B_d.__setitem__((3, 0), 0.0),
+             lambda j: j.T.__setitem__((4, 0, 0), -1.0)]
+    for mut in cases:
+        with pytest.raises(AutoByteError) as ei:
+            gpu_argmax(net, bad_jobs(mut), grid)
+        assert ei.value.status == AB_E_INVALID
+    g_small = synth.Grid(np.array([1024, 8192], np.int64), grid.S_c.copy())
+    g_desc = synth.Grid(grid.S_p[::-1].copy(), grid.S_c.copy())
+    g_sc = synth.Grid(grid.S_p.copy(), np.array([0.5, 2.0], np.float32))
+    for g in (g_small, g_desc, g_sc):
+        with pytest.raises(AutoByteError) as ei:
+            gpu_argmax(net, jobs, g)
+        assert ei.value.status == AB_E_INVALID
