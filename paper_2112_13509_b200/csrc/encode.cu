@@ -41,8 +41,9 @@ struct EncCfg {
   static constexpr int TL_OFF = E_OFF + NJ * CH * kEmbed;  // sTl [NJ][CH][16]; sX [NJ][XS] aliases it
   static constexpr int H1_OFF = TL_OFF + NJ * CH * kNMax;  // sH1 [NJ][32]
   static constexpr int H2_OFF = H1_OFF + NJ * kLstm;       // sH2 [NJ][32]
-  static constexpr int G_OFF = H2_OFF + NJ * kLstm;        // sG [NJ][128]
-  static constexpr int N_OFF = G_OFF + NJ * 4 * kLstm;     // int sN[NJ], sL[NJ]
+  static constexpr int G_OFF = H2_OFF + NJ * kLstm;        // sG [NJ][128]: layer-1 gates
+  static constexpr int G2_OFF = G_OFF + NJ * 4 * kLstm;    // sG2 [NJ][128]: layer-2 gates
+  static constexpr int N_OFF = G2_OFF + NJ * 4 * kLstm;    // int sN[NJ], sL[NJ]
   static constexpr int FLOATS = N_OFF + 2 * NJ;
   static constexpr size_t BYTES = sizeof(float) * FLOATS;
   static_assert(CH * kNMax >= XS, "sX must fit in the sTl chunk it aliases");
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   float (*sH1)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H1_OFF);
   float (*sH2)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H2_OFF);
   float (*sG)[4 * kLstm] = reinterpret_cast<float (*)[4 * kLstm]>(smem + C::G_OFF);
+  float (*sG2)[4 * kLstm] = reinterpret_cast<float (*)[4 * kLstm]>(smem + C::G2_OFF);
   int* sN = reinterpret_cast<int*>(smem + C::N_OFF);
   int* sL = sN + C::NJ;
   const int tid = threadIdx.x;
@@ -93,15 +95,15 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 
   // gates of one layer for the HJ jobs of this half: z = b + Wx in + Wh h  (4 partial sums)
   // (stash, for encoder fine-tuning: per job and step [e | i f g o c h of layer 1 | of layer 2])
-  auto cell_update = [&](float (*sHout)[kLstm], float* cst, int step, int soff) {
+  auto cell_update = [&](float (*sGin)[4 * kLstm], float (*sHout)[kLstm], float* cst, int step, int soff) {
 #pragma unroll
     for (int r = 0; r < C::RC; ++r) {
       const int e = tid + r * kEncThreads;
       if (e < C::NJ * kLstm) {
         const int jj = e >> 5, u = e & (kLstm - 1);
         if (step < sL[jj]) {
-          const float ig = sigmoidf_acc(sG[jj][u]), fg = sigmoidf_acc(sG[jj][kLstm + u]);
-          const float gg = tanh_acc(sG[jj][2 * kLstm + u]), og = sigmoidf_acc(sG[jj][3 * kLstm + u]);
+          const float ig = sigmoidf_acc(sGin[jj][u]), fg = sigmoidf_acc(sGin[jj][kLstm + u]);
+          const float gg = tanh_acc(sGin[jj][2 * kLstm + u]), og = sigmoidf_acc(sGin[jj][3 * kLstm + u]);
           cst[r] = fmaf(fg, cst[r], ig * gg);
           const float h = og * tanh_acc(cst[r]);
           sHout[jj][u] = h;
@@ -115,8 +117,13 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     }
   };
 
-  for (int i0 = 0; i0 < lmax; i0 += C::CH) {
-    const int len = min(C::CH, lmax - i0);
+  // Layer wavefront: layer 1 of step t and layer 2 of step t-1 both need only h1(t-1), so their
+  // gates are formed in one phase and their cells updated in the next (2 barriers per step
+  // instead of 4); the loop runs one step past lmax for the last layer-2 step. Each value is
+  // computed with the same operations as in the sequential order.
+  for (int i0 = 0; i0 <= lmax && lmax > 0; i0 += C::CH) {
+    const int len = min(C::CH, lmax - i0);   // 0 for a tail-only chunk
+    const int iend = i0 + C::CH > lmax ? lmax - i0 + 1 : C::CH;
     __syncthreads();
     // t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers, 0 on padding (R#7, R#8)
     for (int e = tid; e < C::NJ * len * kNMax; e += kEncThreads) {
@@ -136,55 +143,57 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
       if (p.stash && jj < nj && i0 + i < sL[jj]) p.stash[((size_t)(j0 + jj) * p.l_max + i0 + i) * kEncStash + d] = acc;
     }
     __syncthreads();
-    for (int i = 0; i < len; ++i) {
-      // ---- layer 1 gates for the HJ jobs of this half
-      float z[HJ];
+    for (int i = 0; i < iend; ++i) {
+      const int t = i0 + i;
+      if (t < lmax) {   // ---- layer-1 gates of step t (input e_t, h1(t-1)) -> sG
+        float z[HJ];
 #pragma unroll
-      for (int k = 0; k < HJ; ++k) {
-        const int jj = half * HJ + k;
-        const float4* e4 = reinterpret_cast<const float4*>(sE[jj][i]);
-        const float4* h4 = reinterpret_cast<const float4*>(sH1[jj]);
-        float a0 = bg1, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        for (int k = 0; k < HJ; ++k) {
+          const int jj = half * HJ + k;
+          const float4* e4 = reinterpret_cast<const float4*>(sE[jj][i]);
+          const float4* h4 = reinterpret_cast<const float4*>(sH1[jj]);
+          float a0 = bg1, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int q = 0; q < kEmbed / 4; ++q) {
-          const float4 v = e4[q];
-          a0 = fmaf(wx1[4 * q], v.x, a0); a1 = fmaf(wx1[4 * q + 1], v.y, a1);
-          a2 = fmaf(wx1[4 * q + 2], v.z, a2); a3 = fmaf(wx1[4 * q + 3], v.w, a3);
+          for (int q = 0; q < kEmbed / 4; ++q) {
+            const float4 v = e4[q];
+            a0 = fmaf(wx1[4 * q], v.x, a0); a1 = fmaf(wx1[4 * q + 1], v.y, a1);
+            a2 = fmaf(wx1[4 * q + 2], v.z, a2); a3 = fmaf(wx1[4 * q + 3], v.w, a3);
+          }
+#pragma unroll
+          for (int q = 0; q < kLstm / 4; ++q) {
+            const float4 v = h4[q];
+            a0 = fmaf(wh1[4 * q], v.x, a0); a1 = fmaf(wh1[4 * q + 1], v.y, a1);
+            a2 = fmaf(wh1[4 * q + 2], v.z, a2); a3 = fmaf(wh1[4 * q + 3], v.w, a3);
+          }
+          z[k] = (a0 + a1) + (a2 + a3);
         }
 #pragma unroll
-        for (int q = 0; q < kLstm / 4; ++q) {
-          const float4 v = h4[q];
-          a0 = fmaf(wh1[4 * q], v.x, a0); a1 = fmaf(wh1[4 * q + 1], v.y, a1);
-          a2 = fmaf(wh1[4 * q + 2], v.z, a2); a3 = fmaf(wh1[4 * q + 3], v.w, a3);
-        }
-        z[k] = (a0 + a1) + (a2 + a3);
+        for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
       }
+      if (t > 0) {      // ---- layer-2 gates of step t-1 (input h1(t-1), h2(t-2)) -> sG2
+        float z[HJ];
 #pragma unroll
-      for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
-      __syncthreads();
-      cell_update(sH1, c1, i0 + i, kEmbed);
-      __syncthreads();
-      // ---- layer 2 gates
+        for (int k = 0; k < HJ; ++k) {
+          const int jj = half * HJ + k;
+          const float4* x4 = reinterpret_cast<const float4*>(sH1[jj]);
+          const float4* h4 = reinterpret_cast<const float4*>(sH2[jj]);
+          float a0 = bg2, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-      for (int k = 0; k < HJ; ++k) {
-        const int jj = half * HJ + k;
-        const float4* x4 = reinterpret_cast<const float4*>(sH1[jj]);
-        const float4* h4 = reinterpret_cast<const float4*>(sH2[jj]);
-        float a0 = bg2, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-        for (int q = 0; q < kLstm / 4; ++q) {
-          const float4 v = x4[q], w = h4[q];
-          a0 = fmaf(wx2[4 * q], v.x, a0); a1 = fmaf(wx2[4 * q + 1], v.y, a1);
-          a2 = fmaf(wx2[4 * q + 2], v.z, a2); a3 = fmaf(wx2[4 * q + 3], v.w, a3);
-          a0 = fmaf(wh2[4 * q], w.x, a0); a1 = fmaf(wh2[4 * q + 1], w.y, a1);
-          a2 = fmaf(wh2[4 * q + 2], w.z, a2); a3 = fmaf(wh2[4 * q + 3], w.w, a3);
+          for (int q = 0; q < kLstm / 4; ++q) {
+            const float4 v = x4[q], w = h4[q];
+            a0 = fmaf(wx2[4 * q], v.x, a0); a1 = fmaf(wx2[4 * q + 1], v.y, a1);
+            a2 = fmaf(wx2[4 * q + 2], v.z, a2); a3 = fmaf(wx2[4 * q + 3], v.w, a3);
+            a0 = fmaf(wh2[4 * q], w.x, a0); a1 = fmaf(wh2[4 * q + 1], w.y, a1);
+            a2 = fmaf(wh2[4 * q + 2], w.z, a2); a3 = fmaf(wh2[4 * q + 3], w.w, a3);
+          }
+          z[k] = (a0 + a1) + (a2 + a3);
         }
-        z[k] = (a0 + a1) + (a2 + a3);
-      }
 #pragma unroll
-      for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
+        for (int k = 0; k < HJ; ++k) sG2[half * HJ + k][g] = z[k];
+      }
       __syncthreads();
-      cell_update(sH2, c2, i0 + i, kEmbed + 6 * kLstm);
+      if (t < lmax) cell_update(sG, sH1, c1, t, kEmbed);
+      if (t > 0) cell_update(sG2, sH2, c2, t - 1, kEmbed + 6 * kLstm);
       __syncthreads();
     }
   }
