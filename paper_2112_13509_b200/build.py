@@ -36,19 +36,24 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False, stats: bool = False, exp: int = 0) -> str:
+def build(force: bool = False, verbose: bool = False, stats: bool = False, exp: int = 0,
+          defines: tuple = (), name: str = "") -> str:
     """exp > 0 builds libautobyte_exp<exp>.so with -DAB_EXP=<exp>: timing experiments of K2 that
-    deliberately skip work (wrong results; tools only, never loaded by the package)."""
+    deliberately skip work (wrong results; tools only, never loaded by the package).
+    defines / name build a tuning variant libautobyte_<name>.so (e.g. AB_NS_MAX=4) for tools."""
     lib_path = STATS_LIB if stats else LIB
     if exp:
         lib_path = os.path.join(PKG, f"libautobyte_exp{exp}.so")
-    if not force and not stats and not exp and up_to_date():
+    if name:
+        lib_path = os.path.join(PKG, f"libautobyte_{name}.so")
+    if not force and not stats and not exp and not name and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *(["-DAB_STATS"] if stats else []), *([f"-DAB_EXP={exp}"] if exp else []), *sources(), "-o", lib_path + ".tmp",
+           *(["-DAB_STATS"] if stats else []), *([f"-DAB_EXP={exp}"] if exp else []),
+           *[f"-D{d}" for d in defines], *sources(), "-o", lib_path + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -60,4 +65,7 @@ def build(force: bool = False, verbose: bool = False, stats: bool = False, exp: 
 
 if __name__ == "__main__":
     exp = int(sys.argv[sys.argv.index("--exp") + 1]) if "--exp" in sys.argv else 0
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, stats="--stats" in sys.argv, exp=exp))
+    defs = tuple(a.split("=", 1)[1] for a in sys.argv if a.startswith("-D="))
+    name = sys.argv[sys.argv.index("--name") + 1] if "--name" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, stats="--stats" in sys.argv, exp=exp,
+                defines=defs, name=name))

@@ -89,7 +89,11 @@ struct ScoreCfg {
   static constexpr int FIXED = A_BYTES + AW_BYTES + WHAT_BYTES + BIAS_BYTES + PART_BYTES + MISC_BYTES;
   static constexpr int BUDGET = 232448 - 1024;    // opt-in maximum minus the 1 KB alignment slack
   static constexpr int NS_FIT = (BUDGET - FIXED) / CTA_STAGE_BYTES;
+#ifdef AB_NS_MAX
+  static constexpr int NS = NS_FIT > AB_NS_MAX ? AB_NS_MAX : NS_FIT;   // pipeline-depth experiments
+#else
   static constexpr int NS = NS_FIT > 12 ? 12 : NS_FIT;
+#endif
   static constexpr int SMEM = 1024 + FIXED + NS * CTA_STAGE_BYTES;
   static constexpr uint32_t IDESC = umma_idesc_bf16(128 * CG, NCH);
   static constexpr uint32_t TMEM_COLS = 512;

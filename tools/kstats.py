@@ -22,7 +22,7 @@ def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     H = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     J = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
-    lib = ab.load_library(STATS_LIB)
+    lib = ab.load_library(os.environ.get("AUTOBYTE_LIB") or STATS_LIB)
     fn = lib.ab_debug_stats
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     buf = (ctypes.c_ulonglong * 16)()
