@@ -289,9 +289,9 @@ def run_ours(args):
         hg.S_p, hg.S_c = pin(c.grid.S_p), pin(c.grid.S_c)
         hcur, hsp, hsc, hv = pin(cur), pin(ad.S_p), pin(ad.S_c), pin(ad.V_bar)
         hout = (pin(np.empty(J, np.int32)), pin(np.empty(J, np.float32)), pin(np.empty(J, np.float32)))
-        h2d = sum(getattr(hj, f).nbytes for f in ("T", "B_d", "B_u", "n", "l", "m", "arc")) + hg.S_p.nbytes + \
-            hg.S_c.nbytes + hcur.nbytes + sum(getattr(ha, f).nbytes for f in ("T", "B_d", "B_u", "n", "l", "m", "arc")) + \
-            hsp.nbytes + hsc.nbytes + hv.nbytes
+        # job statistics: only this rank's encoder shard crosses PCIe (the library reports the bytes)
+        h2d = net.staged_job_bytes(J, hj.T.shape[1]) + hg.S_p.nbytes + hg.S_c.nbytes + hcur.nbytes + \
+            net.staged_job_bytes(ha.T.shape[0], ha.T.shape[1]) + hsp.nbytes + hsc.nbytes + hv.nbytes
         d2h = sum(o.nbytes for o in hout) + 4
 
         def e2e_step():

@@ -246,7 +246,15 @@ autobyte_status autobyte_trigger(autobyte_ctx* ctx, int32_t J, const int32_t* be
 /* ---- end-to-end entry points (HOST pointers; copies inside; synchronising) ---------- */
 /* Same contracts as above with every array pointer in HOST memory. The library stages the
  * inputs into its own device workspace with cudaMemcpyAsync, runs the device path, copies
- * the [J] results back and synchronises the ctx stream. */
+ * the [J] results back and synchronises the ctx stream. With a communicator attached
+ * (world > 1) every rank still passes the full job arrays, but only the statistics of the
+ * jobs its own encoder shard reads (T, B_down, B_up, n_layers, model_type, arch_type of
+ * ceil(J/world) jobs) are copied; n_workers is copied for all jobs. AUTOBYTE_CHECK=1 copies
+ * everything (the range checks read every job). */
+
+/* Host-to-device bytes the staging above moves for the job statistics of J jobs with
+ * l_max layers on this rank (the e2e accounting of bench.py). Returns 0 for a NULL ctx. */
+size_t autobyte_staged_job_bytes(const autobyte_ctx* ctx, int32_t J, int32_t l_max);
 autobyte_status autobyte_argmax_host(autobyte_ctx* ctx, const autobyte_job_stats* jobs,
                                      const autobyte_grid* grid, const int32_t* cur_idx,
                                      int32_t* best_idx, float* best_score, float* cur_score);

@@ -15,6 +15,7 @@
 // Every GEMM runs on the legacy mma.sync tensor path with 3xTF32 split operands (big*big +
 // big*small + small*big, ~fp32 accuracy), which keeps the gradient well inside the parity
 // tolerance (K4) at a fraction of the SIMT instruction count.
+#include <climits>
 #include <cstdlib>
 
 #include "internal.h"
@@ -54,7 +55,12 @@ struct Gemm {
 // batches (offline training: half the MMAs per FLOP, 8.2 vs 7.2 M samples/s at B = 32768).
 template <int TN>
 struct TileCfg {
-  static constexpr int kStages = TN == 64 ? 3 : 2;   // cp.async depth of the raw slices
+#ifndef AB_ADAPT_STAGES64
+#define AB_ADAPT_STAGES64 4
+#endif
+  // cp.async depth of the raw slices: a slice costs ~2k cycles, mostly L2 latency over the
+  // prefetch distance (kStages - 1 slices), so N = 64 tiles take the deepest ring that fits
+  static constexpr int kStages = TN == 64 ? AB_ADAPT_STAGES64 : 2;
   static constexpr int kRawA = (kTM * (kTK + 4) > kTK * (kTM + 8)) ? kTM * (kTK + 4) : kTK * (kTM + 8);   // floats
   static constexpr int kRawB = (TN * (kTK + 4) > kTK * (TN + 8)) ? TN * (kTK + 4) : kTK * (TN + 8);
   static constexpr int kPlaneA = kTM * kTK * 4, kPlaneB = TN * kTK * 4;               // bytes
@@ -311,6 +317,10 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
 __device__ unsigned long long g_adapt_phase[64];   // block 0: clock at entry of each grid barrier
 __device__ int g_adapt_nphase;
 __device__ long long g_adapt_blk[1024][3];   // per block: smid, clock at F2 tile start, at F2 tile end
+__device__ long long g_adapt_sub[1024][5];   // per block, phase B_{L-1}: start, GEMMs, colsum, update, after sync
+#define AB_SUB(i) do { if (k == L - 1 && step == 0 && threadIdx.x == 0 && blockIdx.x < 1024) g_adapt_sub[blockIdx.x][i] = clock64(); } while (0)
+#else
+#define AB_SUB(i) do { } while (0)
 #endif
 __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) {
 #ifdef AB_STATS
@@ -377,7 +387,24 @@ __device__ void colsum_split(const float* X, int B, int N, long long ld, float* 
 // the 16 sums are reduced with a fixed xor butterfly (deterministic).
 __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, const float* vbar, const int32_t* nvalid,
                          float scale, int B, int H, float* R, float* sW) {
-  for (int e = threadIdx.x; e < kNMax * H; e += kAdaptThreads) sW[e] = Wo[e];
+  {   // W_o -> shared memory with 8 independent 16-byte loads in flight per thread (H % 4 == 0)
+    const float4* src = reinterpret_cast<const float4*>(Wo);
+    float4* dst = reinterpret_cast<float4*>(sW);
+    const int n4 = kNMax * H / 4;
+    for (int e0 = threadIdx.x; e0 < n4; e0 += 8 * kAdaptThreads) {
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + i * kAdaptThreads;
+        if (e < n4) v[i] = src[e];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + i * kAdaptThreads;
+        if (e < n4) dst[e] = v[i];
+      }
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * kAdaptThreads + threadIdx.x) >> 5, nwarps = (gridDim.x * kAdaptThreads) >> 5;
@@ -385,10 +412,17 @@ __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, cons
     float acc[kNMax];
 #pragma unroll
     for (int w = 0; w < kNMax; ++w) acc[w] = 0.f;
-    for (int k = lane; k < H; k += 32) {
-      const float h = Hl[(long long)b * H + k];
+    for (int k0 = lane; k0 < H; k0 += 32 * 8) {   // the row's loads issued 8 at a time
+      float h[8];
 #pragma unroll
-      for (int w = 0; w < kNMax; ++w) acc[w] = fmaf(h, sW[w * H + k], acc[w]);
+      for (int i = 0; i < 8; ++i) h[i] = k0 + 32 * i < H ? Hl[(long long)b * H + k0 + 32 * i] : 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (k0 + 32 * i < H) {
+#pragma unroll
+          for (int w = 0; w < kNMax; ++w) acc[w] = fmaf(h[i], sW[w * H + k0 + 32 * i], acc[w]);
+        }
+      }
     }
     float mine = 0.f;
 #pragma unroll
@@ -462,6 +496,37 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   auto gemm = [&](const Gemm& g, int t) {
     if (big) gemm_tile<128>(g, t, smem, ts);
     else gemm_tile<64>(g, t, smem, ts);
+  };
+  // Two independent GEMMs in one phase (t1 tiles of g1, t2 of g2; every thread takes the same
+  // decision). Round-robin over the concatenated tile list can stack a long tile and a short one
+  // on the same CTA (backward at B = 1024: 64 K = 512 input-gradient tiles + 128 K = 256 split-K
+  // weight-gradient tiles on 148 CTAs); when it is shorter, the g2 tiles get dedicated CTAs
+  // [0, t2) and the g1 tiles are dealt round-robin over the rest. Costs are K slices per tile.
+  // Tile arithmetic does not depend on the CTA that runs it, so results are unchanged.
+  auto gemm_pair = [&](const Gemm& g1, const Gemm& g2) {
+    const int t1 = tiles(g1), t2 = tiles(g2), G = gridDim.x;
+    auto slices = [&](const Gemm& g) {
+      const int kk = g.ksplit > 1 ? (g.K + g.ksplit - 1) / g.ksplit : g.K;
+      return (kk + kTK - 1) / kTK;
+    };
+    const int c1 = slices(g1), c2 = slices(g2);
+    int rr = 0;   // round-robin makespan (in slices) over CTAs b < G
+    for (int b = 0; b < G && b < t1 + t2; ++b) {
+      int c = 0;
+      for (int t = b; t < t1 + t2; t += G) c += t < t1 ? c1 : c2;
+      rr = c > rr ? c : rr;
+    }
+    const int rest = G - t2;
+    const int ded = (t2 > 0 && rest > 0) ? max(c2, ((t1 + rest - 1) / rest) * c1) : INT_MAX;
+    if (ded < rr) {
+      if (blockIdx.x < t2) gemm(g2, blockIdx.x);
+      else for (int t = blockIdx.x - t2; t < t1; t += rest) gemm(g1, t);
+    } else {
+      for (int t = blockIdx.x; t < t1 + t2; t += G) {
+        if (t < t1) gemm(g1, t);
+        else gemm(g2, t - t1);
+      }
+    }
   };
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
@@ -541,11 +606,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
     {
       Gemm gw{kNMax, H, B, R, 1, kNMax, Hk(L), H, 1, Gr + p.off.W_o, H, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
       Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H};
-      const int t1 = tiles(gw), t2 = tiles(gd);
-      for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm(gw, t);
-        else gemm(gd, t - t1);
-      }
+      gemm_pair(gw, gd);
       colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
       grid_sync(p.barrier, gen);
     }
@@ -555,26 +616,24 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       const float* in = k == 1 ? Z : Hk(k - 1);
       const float* Dk = D[k & 1];
       Gemm gw{H, Kin, B, Dk, 1, H, in, Kin, 1, Gr + p.off.W[k], Kin, 2, nullptr, nullptr, 0, kSplitK, p.off.total};
-      const int t1 = tiles(gw);
-      int t2 = 0;
-      Gemm gd{};
+      Gemm gd{};   // M = 0: no tiles
       if (k > 1) {
         gd = Gemm{B, H, H, Dk, H, 1, P + p.off.W[k], H, 1, D[(k - 1) & 1], H, 1, nullptr, Hk(k - 1), H};
-        t2 = tiles(gd);
       } else if (p.dz_out) {   // encoder fine-tuning: d obj / d [x | u] = D_1 W1 (pre-update W1)
         gd = Gemm{B, kZDim, H, Dk, H, 1, P + p.off.W[1], kZDim, 1, p.dz_out, kZDim, 2, nullptr, nullptr, 0, 1, 0};
-        t2 = tiles(gd);
       }
-      for (int t = blockIdx.x; t < t1 + t2; t += gridDim.x) {
-        if (t < t1) gemm(gw, t);
-        else gemm(gd, t - t1);
-      }
+      AB_SUB(0);
+      gemm_pair(gw, gd);
+      AB_SUB(1);
       colsum_split(Dk, B, H, H, Gr + p.off.b[k], p.off.total);
+      AB_SUB(2);
       // SGD of the layer above, whose gradient partials completed in the previous phase and whose
       // weights no phase reads any more this step (W_o after BO; W_{k+1} after B_{k+1})
       if (k == L) update_range(p, p.off.W_o, p.off.total, step);
       else update_range(p, p.off.W[k + 1], p.off.b[k + 1] + H, step);
+      AB_SUB(3);
       grid_sync(p.barrier, gen);
+      AB_SUB(4);
     }
     // ---------------- SGD of layer 1 (W1, b1); the kernel exit orders it after the last step
     update_range(p, p.off.W[1], p.off.b[1] + H, step);
@@ -612,6 +671,10 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
 extern "C" int ab_debug_adapt_blocks(long long* out, int n) {
   cudaDeviceSynchronize();
   return cudaMemcpyFromSymbol(out, ab::g_adapt_blk, sizeof(long long) * 3 * (n < 1024 ? n : 1024)) == cudaSuccess;
+}
+extern "C" int ab_debug_adapt_sub(long long* out, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ab::g_adapt_sub, sizeof(long long) * 5 * (n < 1024 ? n : 1024)) == cudaSuccess;
 }
 extern "C" int ab_debug_adapt_phases(unsigned long long* out) {
   cudaDeviceSynchronize();

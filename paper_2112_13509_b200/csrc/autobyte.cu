@@ -190,16 +190,27 @@ EncodeParams encode_params(autobyte_ctx* c, const autobyte_job_stats* j) {
 // its 1/G slice of the jobs and the x rows are all-gathered in place over NCCL: K1a's per-job
 // arithmetic does not depend on how jobs are grouped, so x (and every key after it) is
 // bit-identical to the single-rank result.
+// The jobs [*jb, *je) whose statistics this rank's K1a reads (all of them at G = 1).
+bool encode_range(const autobyte_ctx* c, int J, int* jb, int* je) {
+  const bool shard = c->shard_encode && c->comm && c->world > 1;
+  const int G = shard ? c->world : 1;
+  const int Jp = (J + G - 1) / G;
+  *jb = shard ? std::min(J, c->rank * Jp) : 0;
+  *je = shard ? std::min(J, (c->rank + 1) * Jp) : J;
+  return shard;
+}
+
 autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, EncodeParams* out) {
   const int J = jobs->J;
-  const bool shard = c->shard_encode && c->comm && c->world > 1;
+  int jb = 0, je = J;
+  const bool shard = encode_range(c, J, &jb, &je);
   const int G = shard ? c->world : 1;
   const int Jp = (J + G - 1) / G;
   AB_CUDA(c, c->x.ensure((size_t)Jp * G * kXDim));
   EncodeParams ep = encode_params(c, jobs);
   ep.x_out = c->x.ptr;
-  ep.j_begin = shard ? std::min(J, c->rank * Jp) : 0;
-  ep.j_end = shard ? std::min(J, (c->rank + 1) * Jp) : J;
+  ep.j_begin = jb;
+  ep.j_end = je;
   if (ep.j_end > ep.j_begin)
     AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
   if (shard) {
@@ -213,6 +224,38 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
   }
   *out = ep;
   return AB_OK;
+}
+
+// Host staging of job statistics for the *_host entry points. Only this rank's K1a job range
+// reads T, B_d, B_u, l, m and arc (every rank encodes 1/G of the jobs and all-gathers x), so only
+// that slice crosses PCIe, copied to its global offset; n is read for every job (K1b's worker
+// mean, K4's mask). With AUTOBYTE_CHECK=1 everything is copied (the range checks read all jobs).
+cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs) {
+  const int J = jobs->J;
+  int jb = 0, je = J;
+  encode_range(c, J, &jb, &je);
+  if (c->check) { jb = 0; je = J; }
+  const size_t nj = (size_t)(je - jb), lt = (size_t)jobs->l_max * kNMax;
+  auto h2d = [&](void* d, const void* h, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream) : cudaSuccess;
+  };
+  cudaError_t e;
+  if ((e = h2d(c->sT.ptr + jb * lt, jobs->T + jb * lt, nj * lt * 4)) != cudaSuccess) return e;
+  if ((e = h2d(c->sBd.ptr + (size_t)jb * kNMax, jobs->B_down + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
+  if ((e = h2d(c->sBu.ptr + (size_t)jb * kNMax, jobs->B_up + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
+  if ((e = h2d(c->sN.ptr, jobs->n_workers, (size_t)J * 4)) != cudaSuccess) return e;
+  if ((e = h2d(c->sL.ptr + jb, jobs->n_layers + jb, nj * 4)) != cudaSuccess) return e;
+  if ((e = h2d(c->sM.ptr + jb, jobs->model_type + jb, nj * 4)) != cudaSuccess) return e;
+  return h2d(c->sArc.ptr + jb, jobs->arch_type + jb, nj * 4);
+}
+
+// Bytes the *_host staging above moves for J jobs on this rank (for the e2e accounting).
+size_t staged_job_bytes(const autobyte_ctx* c, int J, int l_max) {
+  int jb = 0, je = J;
+  encode_range(c, J, &jb, &je);
+  if (c->check) { jb = 0; je = J; }
+  const size_t nj = (size_t)(je - jb);
+  return nj * ((size_t)l_max * kNMax * 4 + 2 * kNMax * 4 + 3 * 4) + (size_t)J * 4;
 }
 
 autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
@@ -693,6 +736,10 @@ autobyte_status autobyte_trigger(autobyte_ctx* c, int32_t J, const int32_t* best
   return AB_OK;
 }
 
+size_t autobyte_staged_job_bytes(const autobyte_ctx* c, int32_t J, int32_t l_max) {
+  return c && J > 0 && l_max > 0 ? staged_job_bytes(c, J, l_max) : 0;
+}
+
 autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                      const int32_t* cur_idx, int32_t* best_idx, float* best_score,
                                      float* cur_score) {
@@ -710,13 +757,7 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
   AB_CUDA(c, c->rIdx.ensure(J)); AB_CUDA(c, c->rScore.ensure(J)); AB_CUDA(c, c->rCur.ensure(J));
   if (cur_idx) AB_CUDA(c, c->sCur.ensure(J));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  AB_CUDA(c, h2d(c->sT.ptr, jobs->T, nT * 4));
-  AB_CUDA(c, h2d(c->sBd.ptr, jobs->B_down, (size_t)J * kNMax * 4));
-  AB_CUDA(c, h2d(c->sBu.ptr, jobs->B_up, (size_t)J * kNMax * 4));
-  AB_CUDA(c, h2d(c->sN.ptr, jobs->n_workers, (size_t)J * 4));
-  AB_CUDA(c, h2d(c->sL.ptr, jobs->n_layers, (size_t)J * 4));
-  AB_CUDA(c, h2d(c->sM.ptr, jobs->model_type, (size_t)J * 4));
-  AB_CUDA(c, h2d(c->sArc.ptr, jobs->arch_type, (size_t)J * 4));
+  AB_CUDA(c, stage_jobs_host(c, jobs));
   AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
   if (cur_idx) AB_CUDA(c, h2d(c->sCur.ptr, cur_idx, (size_t)J * 4));
@@ -751,13 +792,7 @@ autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* s
   AB_CUDA(c, c->sSp.ensure(B)); AB_CUDA(c, c->sSc.ensure(B)); AB_CUDA(c, c->sV.ensure((size_t)B * kNMax));
   AB_CUDA(c, c->loss_tmp.ensure(1));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  AB_CUDA(c, h2d(c->sT.ptr, samples->T, nT * 4));
-  AB_CUDA(c, h2d(c->sBd.ptr, samples->B_down, (size_t)B * kNMax * 4));
-  AB_CUDA(c, h2d(c->sBu.ptr, samples->B_up, (size_t)B * kNMax * 4));
-  AB_CUDA(c, h2d(c->sN.ptr, samples->n_workers, (size_t)B * 4));
-  AB_CUDA(c, h2d(c->sL.ptr, samples->n_layers, (size_t)B * 4));
-  AB_CUDA(c, h2d(c->sM.ptr, samples->model_type, (size_t)B * 4));
-  AB_CUDA(c, h2d(c->sArc.ptr, samples->arch_type, (size_t)B * 4));
+  AB_CUDA(c, stage_jobs_host(c, samples));
   AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
   AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));

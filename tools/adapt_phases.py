@@ -20,7 +20,7 @@ batch = synth.make_adapt_batch(synth.small_fleet(B, 1), synth.log_grid(64, 64), 
 for _ in range(2):
     net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, 1e-3, 1)
     n = fn(buf)
-names = ["Z"] + [f"F{k}" for k in range(1, L + 1)] + ["OUT", "BO"] + [f"B{k}" for k in range(L, 0, -1)] + ["SGD"]
+names = [f"F{k}" for k in range(1, L + 1)] + ["OUT", "BO"] + [f"B{k}" for k in range(L, 0, -1)] + ["SGD"]
 prev = buf[0]
 for i in range(1, n):
     print(f"{names[i - 1] if i - 1 < len(names) else i:5s} {buf[i] - prev:8d} cycles")
@@ -45,3 +45,15 @@ if durs:
     durs.sort()
     print("F2 tile cycles min/med/max", durs[0], durs[len(durs) // 2], durs[-1])
 print("block->smid first 8:", [blk[3 * b] for b in range(8)])
+
+# phase B_{L-1} per block: GEMM tiles, column sums, optimiser update, grid barrier (cycles)
+fs = lib.ab_debug_adapt_sub
+fs.argtypes = [ctypes.c_void_p, ctypes.c_int]
+sub = (ctypes.c_longlong * (5 * 1024))()
+fs(sub, 1024)
+rows = [[sub[5 * b + i] for i in range(5)] for b in range(148)]
+t0 = min(r[0] for r in rows)
+for name, i in (("gemm", 1), ("colsum", 2), ("update", 3), ("sync", 4)):
+    d = sorted(r[i] - r[i - 1] for r in rows)
+    print(f"B{L - 1} {name:7s} per-block cycles min/med/max {d[0]} {d[len(d) // 2]} {d[-1]}")
+print(f"B{L - 1} start skew {max(r[0] for r in rows) - t0}, last block done with update at +{max(r[3] for r in rows) - t0}")

@@ -35,6 +35,14 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
     dist.all_gather(allp, packed)
     same_all_ranks = all(torch.equal(allp[0], x) for x in allp)
     res = {"config": name, "world": world, "cta_group": cg, "same_on_all_ranks": same_all_ranks}
+    # host entry point: each rank copies only its encoder shard of the statistics -> same results
+    hb, hs, hc = net.argmax_host(jobs, grid, cur.cpu().numpy(), b, e)
+    res["host_same_as_device"] = bool(np.array_equal(hb, bi.cpu().numpy())
+                                      and np.array_equal(hs.view(np.int32), bs.cpu().numpy().view(np.int32))
+                                      and np.array_equal(np.nan_to_num(hc), np.nan_to_num(cs.cpu().numpy())))
+    full = jobs.T.nbytes + jobs.B_d.nbytes + jobs.B_u.nbytes + 4 * 4 * jobs.J
+    res["host_staged_bytes"] = net.staged_job_bytes(jobs.J, jobs.T.shape[1])
+    res["host_staged_fraction"] = res["host_staged_bytes"] / full
     # top-k (NEXT 4): per-rank lists all-gathered and merged -> identical everywhere and to 1 GPU
     ti, ts = net.topk(dj, dg, 8, b, e)
     torch.cuda.synchronize(dev)
@@ -67,6 +75,11 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
     allb = [torch.empty_like(blob) for _ in range(world)]
     dist.all_gather(allb, blob)
     res["adapt_same_on_all_ranks"] = all(torch.equal(allb[0], x) for x in allb)
+    hnet = AutoByte(desc.hidden_layers, desc.hidden_width, W, device=dev.index)
+    abd.attach(hnet)
+    hloss = hnet.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=1e-3, steps=1)
+    res["adapt_host_same_as_device"] = hnet.get_weights_blob() == net.get_weights_blob() and hloss == float(loss.item())
+    hnet.close()
     if rank == 0:
         loss1 = single.adapt(dj, sp, sc, vb, lr=1e-3, steps=1)
         torch.cuda.synchronize(dev)
@@ -96,7 +109,8 @@ def main():
         if rank == 0:
             print(json.dumps(r), flush=True)
             ok &= (r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
-                   and r["topk_same_on_all_ranks"] and r["topk_g_invariant"])
+                   and r["topk_same_on_all_ranks"] and r["topk_g_invariant"] and r["host_same_as_device"]
+                   and r["adapt_host_same_as_device"] and (world == 1 or r["host_staged_fraction"] < 0.75))
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
