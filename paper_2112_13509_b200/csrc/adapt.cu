@@ -23,6 +23,13 @@
 
 namespace ab {
 
+#ifdef AB_STATS
+__device__ long long g_adapt_trace[2][64][4];   // [worker t0 | issuer][slice][stamp] of one traced tile
+__device__ int g_adapt_trace_on;
+#define AB_TR(who, it, i) do { if (trace && (it) < 64) g_adapt_trace[who][it][i] = clock64(); } while (0)
+#else
+#define AB_TR(who, it, i) do { } while (0)
+#endif
 constexpr int kWorkThreads = 256;                 // warps 0-7: staging, operand split, epilogue, SIMT phases
 constexpr int kIssuerWarp = kWorkThreads / 32;    // warp 8: tcgen05.mma issuer
 constexpr int kAdaptThreads = kWorkThreads + 32;
@@ -56,7 +63,7 @@ struct Gemm {
 template <int TN>
 struct TileCfg {
 #ifndef AB_ADAPT_STAGES64
-#define AB_ADAPT_STAGES64 4
+#define AB_ADAPT_STAGES64 2
 #endif
   // cp.async depth of the raw slices: a slice costs ~2k cycles, mostly L2 latency over the
   // prefetch distance (kStages - 1 slices), so N = 64 tiles take the deepest ring that fits
@@ -65,13 +72,21 @@ struct TileCfg {
   static constexpr int kRawB = (TN * (kTK + 4) > kTK * (TN + 8)) ? TN * (kTK + 4) : kTK * (TN + 8);
   static constexpr int kPlaneA = kTM * kTK * 4, kPlaneB = TN * kTK * 4;               // bytes
   static constexpr int kPlaneBuf = 2 * kPlaneA + 2 * kPlaneB;                          // one buffer
-  static constexpr size_t kRawOff = 2 * (size_t)kPlaneBuf;
+#ifndef AB_ADAPT_BUFS64
+#define AB_ADAPT_BUFS64 3
+#endif
+  // plane buffers: with two, splitting slice i+1 waited for the MMAs of slice i-1 to COMPLETE and
+  // the split and the MMA chain ran back to back (~1.6k cycles per slice); a third buffer lets the
+  // split run one slice further ahead (N = 64 only: three N = 128 buffers do not fit)
+  static constexpr int kBufs = TN == 64 ? AB_ADAPT_BUFS64 : 2;
+  static constexpr size_t kRawOff = kBufs * (size_t)kPlaneBuf;
   static constexpr size_t kSmem = kRawOff + sizeof(float) * kStages * (kRawA + kRawB);
   static constexpr uint32_t kIdesc = umma_idesc_tf32(kTM, TN);
 };
 constexpr int kSK = kTK + 4;
 constexpr size_t kAdaptSmemBytes =
     1024 + (TileCfg<64>::kSmem > TileCfg<128>::kSmem ? TileCfg<64>::kSmem : TileCfg<128>::kSmem);
+static_assert(kAdaptSmemBytes + 4096 <= 232448, "dynamic + static shared memory of K4 exceeds 227 KB");
 constexpr uint32_t kTmemCols = kNAcc * 128;   // 512: four accumulators of the widest tile
 constexpr int kBigBatch = 4096;               // B >= this: N = 128 tiles
 
@@ -84,8 +99,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// x = big + small with both parts tf32 (10-bit mantissa each): the 3xTF32 product
-// big*big + big*small + small*big carries ~fp32 accuracy (the dropped small*small is ~2^-22 relative).
+// x ~ big + small with both parts exact tf32 values (10 explicit mantissa bits): big = x with its
+// low 13 mantissa bits cleared (truncation), small = the exact fp32 remainder x - big, truncated the
+// same way. The 3xTF32 product big*big + big*small + small*big then carries ~2^-20 relative error
+// (|small| < 2^-10 |x|, small's own truncation < 2^-10 |small|; small*small is dropped). Two LOP3 and
+// one FADD per element: cvt.rna.tf32 runs at a fraction of the ALU rate, and with it the split was
+// ~60 % of every K slice (tools/adapt_phases.py slice trace: ~900 of ~1600 cycles).
+#ifndef AB_TF32_CVT
+__device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
+  const float b = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  big = b;
+  small = __uint_as_float(__float_as_uint(x - b) & 0xFFFFE000u);
+}
+#else   // the round-to-nearest split (timing comparison)
 __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
   uint32_t b, sm;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
@@ -94,6 +120,7 @@ __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
   big = __uint_as_float(b);
   small = __uint_as_float(sm);
 }
+#endif
 
 // Stage one ROWS x kTK slice of an operand: X(mn, k) = base[mn*lmn + k*lk] for mn in [mn0, mn0+ROWS),
 // k in [k0, k0+kTK), zero-filled outside [0, MN) x [k0, kend). 16-byte vectors.
@@ -166,11 +193,11 @@ __device__ __forceinline__ void split_slice(const float* raw, bool kcontig, uint
 // of its own role; mbarrier parities are derived from them).
 struct TcState {
   uint32_t tmem;         // kTmemCols fp32 accumulator columns
-  uint64_t* full;        // [2]: the 8 worker warps have written plane buffer b
-  uint64_t* empty;       // [2]: the MMAs that read plane buffer b have completed (tcgen05.commit)
+  uint64_t* full;        // [kMaxBufs]: the 8 worker warps have written plane buffer b
+  uint64_t* empty;       // [kMaxBufs]: the MMAs that read plane buffer b have completed (tcgen05.commit)
   uint64_t* acc_free;    // the epilogue has read the accumulators of the last MMA tile
-  uint32_t fills[2];     // workers: times buffer b has been filled
-  uint32_t issued[2];    // issuer: fills of buffer b consumed
+  uint32_t fills[3];     // workers: times buffer b has been filled
+  uint32_t issued[3];    // issuer: fills of buffer b consumed
   uint32_t tiles;        // issuer: MMA tiles issued
 };
 
@@ -185,7 +212,7 @@ template <int TN>
 __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   using T = TileCfg<TN>;
   constexpr int kStages = T::kStages, kRawA = T::kRawA, kRawB = T::kRawB;
-  constexpr int kPlaneA = T::kPlaneA, kPlaneB = T::kPlaneB, kPlaneBuf = T::kPlaneBuf;
+  constexpr int kPlaneA = T::kPlaneA, kPlaneB = T::kPlaneB, kPlaneBuf = T::kPlaneBuf, kBufs = T::kBufs;
   constexpr uint32_t kIdesc = T::kIdesc;
   const int tiles_n = (g.N + TN - 1) / TN;
   const int tiles_mn = ((g.M + kTM - 1) / kTM) * tiles_n;
@@ -201,14 +228,21 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   const int nk = kend > kbeg ? (kend - kbeg + kTK - 1) / kTK : 0;
   const uint32_t pbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef AB_STATS
+  const bool trace_tile = g_adapt_trace_on && blockIdx.x == 0 && nk >= 8 && g.mode == 0 && g.K > 256;
+  if (trace_tile && threadIdx.x == 0) g_adapt_trace_on = 0;
+  const bool trace = trace_tile && (threadIdx.x == 0 || (warp == kIssuerWarp && lane == 0));
+#endif
   if (warp == kIssuerWarp) {
     // ---------------- MMA issuer: per slice, wait for the split planes, issue 4 K-steps x 3
     // products into accumulator (slice % 4), commit -> empty[b] frees the buffer
     if (nk == 0) return;
     if (ts.tiles > 0) mbar_wait(ts.acc_free, (ts.tiles - 1) & 1);   // previous tile's epilogue has read TMEM
     for (int it = 0; it < nk; ++it) {
-      const int b = it & 1;
+      const int b = it % kBufs;
+      AB_TR(1, it, 0);
       mbar_wait(&ts.full[b], ts.issued[b] & 1);
+      AB_TR(1, it, 1);
       ++ts.issued[b];
       tc_fence_after();
       if (elect_one()) {
@@ -227,6 +261,7 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
         umma_commit(&ts.empty[b]);
       }
       __syncwarp();
+      AB_TR(1, it, 2);
     }
     ++ts.tiles;
     return;
@@ -248,11 +283,15 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
 #pragma unroll
   for (int i = 0; i < kStages - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
-    const int b = it & 1;
+    const int b = it % kBufs;
+    AB_TR(0, it, 0);
     cp_async_wait<kStages - 2>();
+    AB_TR(0, it, 1);
     named_bar_sync(kWorkBar, kWorkThreads);   // slice `it` landed for every worker
+    AB_TR(0, it, 2);
     issue(it + kStages - 1);
     if (ts.fills[b] > 0) mbar_wait(&ts.empty[b], (ts.fills[b] - 1) & 1);   // MMAs on buffer b's last fill done
+    AB_TR(0, it, 3);
     uint8_t* buf = smem + b * kPlaneBuf;
     split_slice<kTM>(rawA(it % kStages), a_kc, buf, buf + kPlaneA);
     split_slice<TN>(rawB(it % kStages), b_kc, buf + 2 * kPlaneA, buf + 2 * kPlaneA + kPlaneB);
@@ -263,7 +302,7 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   }
   cp_async_wait<0>();
   if (nk > 0) {   // the last commit completes after every MMA of the tile
-    const int bl = (nk - 1) & 1;
+    const int bl = (nk - 1) % kBufs;
     mbar_wait(&ts.empty[bl], (ts.fills[bl] - 1) & 1);
   }
   tc_fence_after();
@@ -476,21 +515,21 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // SW128 atoms: 1 KB aligned
   float* ring = reinterpret_cast<float*>(smem);   // out_rows stages W_o here between GEMM phases
-  __shared__ __align__(8) uint64_t s_bar[5];   // full[2], empty[2], acc_free
+  __shared__ __align__(8) uint64_t s_bar[7];   // full[3], empty[3], acc_free
   __shared__ uint32_t s_tmem;
   if (threadIdx.x == 0) {
-    mbar_init(&s_bar[0], kWorkThreads / 32);   // full: one arrive per worker warp
-    mbar_init(&s_bar[1], kWorkThreads / 32);
-    mbar_init(&s_bar[2], 1);                   // empty: tcgen05.commit
-    mbar_init(&s_bar[3], 1);
-    mbar_init(&s_bar[4], kWorkThreads / 32);   // acc_free: one arrive per worker warp
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&s_bar[b], kWorkThreads / 32);   // full: one arrive per worker warp
+      mbar_init(&s_bar[3 + b], 1);               // empty: tcgen05.commit
+    }
+    mbar_init(&s_bar[6], kWorkThreads / 32);     // acc_free: one arrive per worker warp
     fence_barrier_init();
   }
   if (threadIdx.x < 32) { tmem_alloc(&s_tmem, kTmemCols); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  TcState ts{s_tmem, &s_bar[0], &s_bar[2], &s_bar[4], {0u, 0u}, {0u, 0u}, 0u};
+  TcState ts{s_tmem, &s_bar[0], &s_bar[3], &s_bar[6], {0u, 0u, 0u}, {0u, 0u, 0u}, 0u};
   const bool big = p.B >= kBigBatch;   // uniform: every CTA takes the same tile width
   auto tiles = [&](const Gemm& g) { return big ? g.tiles<128>() : g.tiles<64>(); };
   auto gemm = [&](const Gemm& g, int t) {
@@ -671,6 +710,14 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
 extern "C" int ab_debug_adapt_blocks(long long* out, int n) {
   cudaDeviceSynchronize();
   return cudaMemcpyFromSymbol(out, ab::g_adapt_blk, sizeof(long long) * 3 * (n < 1024 ? n : 1024)) == cudaSuccess;
+}
+extern "C" int ab_debug_adapt_trace(long long* out, int arm) {
+  cudaDeviceSynchronize();
+  if (arm) {
+    const int one = 1;
+    return cudaMemcpyToSymbol(ab::g_adapt_trace_on, &one, sizeof(int)) == cudaSuccess;
+  }
+  return cudaMemcpyFromSymbol(out, ab::g_adapt_trace, sizeof(long long) * 2 * 64 * 4) == cudaSuccess;
 }
 extern "C" int ab_debug_adapt_sub(long long* out, int n) {
   cudaDeviceSynchronize();

@@ -85,6 +85,8 @@ struct autobyte_ctx {
   long long opt_t = 0;               // Adam step count
   DevBuf<float2> u;                  // [shard] candidate encodings (K0)
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
+  DevBuf<unsigned long long> keys_all;   // [G][2J]: every rank's keys (all-gather exchange)
+  bool exchange_allreduce = false;   // AUTOBYTE_EXCHANGE=allreduce: ncclAllReduce(max) instead
   // staging for the *_host entry points
   DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
   DevBuf<int32_t> sN, sL, sM, sArc, sCur, rIdx;
@@ -394,6 +396,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   c->stream = static_cast<cudaStream_t>(cuda_stream);
   const char* se = std::getenv("AUTOBYTE_SHARD_ENCODE");
   c->shard_encode = !(se && se[0] == '0');
+  const char* ex = std::getenv("AUTOBYTE_EXCHANGE");
+  c->exchange_allreduce = ex && std::strcmp(ex, "allreduce") == 0;
   const char* chk = std::getenv("AUTOBYTE_CHECK");
   c->check = chk && chk[0] == '1';
   auto bail = [&](cudaError_t e, const char* what) {
@@ -533,16 +537,28 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
   if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
   if ((s = run_encode_and_score(c, jobs, grid, cur_idx, nullptr)) != AB_OK) return s;
   const int J = jobs->J;
+  // K3 (§8(a) a-7): the per-rank (score, index) keys are all-gathered over NVLink (one pass; the
+  // per-job max is folded into K5), or with AUTOBYTE_EXCHANGE=allreduce reduced by ncclAllReduce(max)
+  const unsigned long long* kin = c->keys.ptr;
+  int G = 1;
   if (c->comm && c->world > 1) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
-    ncclResult_t r = ncclAllReduce(c->keys.ptr, c->keys.ptr, (size_t)2 * J, ncclUint64, ncclMax, c->comm, c->stream);
+    ncclResult_t r;
+    if (c->exchange_allreduce) {
+      r = ncclAllReduce(c->keys.ptr, c->keys.ptr, (size_t)2 * J, ncclUint64, ncclMax, c->comm, c->stream);
+    } else {
+      AB_CUDA(c, c->keys_all.ensure((size_t)2 * J * c->world));
+      r = ncclAllGather(c->keys.ptr, c->keys_all.ptr, (size_t)2 * J, ncclUint64, c->comm, c->stream);
+      kin = c->keys_all.ptr;
+      G = c->world;
+    }
     if (c->profiling) { cudaEventRecord(b, c->stream); c->pending.push_back({K_EXCHANGE, {a, b}}); }
-    if (r != ncclSuccess) return fail(c, AB_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    if (r != ncclSuccess) return fail(c, AB_E_NCCL, std::string("nccl key exchange: ") + ncclGetErrorString(r));
     c->launches[K_EXCHANGE] += 1;
   }
   AB_CUDA(c, timed(c, K_FINALIZE, [&] {
-            return launch_finalize(J, c->keys.ptr, c->keys.ptr + J, best_idx, best_score, cur_score, c->stream);
+            return launch_finalize(J, G, 2LL * J, kin, kin + J, best_idx, best_score, cur_score, c->stream);
           }));
   return AB_OK;
 }

@@ -104,8 +104,9 @@ cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s
 cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_score, const int32_t* cur_idx,
                            const float* cur_score, const float* v_obs, float gain, float drift, int32_t* action,
                            cudaStream_t s);
-cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigned long long* cur_keys,
-                            int32_t* best_idx, float* best_score, float* cur_score, cudaStream_t s);
+cudaError_t launch_finalize(int J, int G, long long stride, const unsigned long long* keys,
+                            const unsigned long long* cur_keys, int32_t* best_idx, float* best_score,
+                            float* cur_score, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);

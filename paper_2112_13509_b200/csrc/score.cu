@@ -687,12 +687,16 @@ cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- K5: decode per-job keys
-__global__ void finalize_kernel(int J, const unsigned long long* __restrict__ keys,
+// K5: keys -> (best index, best score, current score). G > 1 with the all-gather exchange: the
+// keys arrive as G rank blocks of [2J] (best keys, then current-config keys) and the per-job max
+// is taken here (max is order-free, so the result is the same for any G and shard layout).
+__global__ void finalize_kernel(int J, int G, long long stride, const unsigned long long* __restrict__ keys,
                                 const unsigned long long* __restrict__ cur_keys, int32_t* best_idx,
                                 float* best_score, float* cur_score) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= J) return;
-  const unsigned long long k = keys[j];
+  unsigned long long k = keys[j];
+  for (int g = 1; g < G; ++g) k = max(k, keys[g * stride + j]);
   if (k == 0ull) {
     best_idx[j] = -1;
     best_score[j] = __uint_as_float(0x7FC00000u);
@@ -701,14 +705,16 @@ __global__ void finalize_kernel(int J, const unsigned long long* __restrict__ ke
     best_score[j] = unord32(static_cast<uint32_t>(k >> 32));
   }
   if (cur_score) {
-    const unsigned long long ck = cur_keys[j];
+    unsigned long long ck = cur_keys[j];
+    for (int g = 1; g < G; ++g) ck = max(ck, cur_keys[g * stride + j]);
     cur_score[j] = ck ? unord32(static_cast<uint32_t>(ck >> 32)) : __uint_as_float(0x7FC00000u);
   }
 }
 
-cudaError_t launch_finalize(int J, const unsigned long long* keys, const unsigned long long* cur_keys,
-                            int32_t* best_idx, float* best_score, float* cur_score, cudaStream_t s) {
-  finalize_kernel<<<(J + 255) / 256, 256, 0, s>>>(J, keys, cur_keys, best_idx, best_score, cur_score);
+cudaError_t launch_finalize(int J, int G, long long stride, const unsigned long long* keys,
+                            const unsigned long long* cur_keys, int32_t* best_idx, float* best_score,
+                            float* cur_score, cudaStream_t s) {
+  finalize_kernel<<<(J + 255) / 256, 256, 0, s>>>(J, G, stride, keys, cur_keys, best_idx, best_score, cur_score);
   return cudaGetLastError();
 }
 

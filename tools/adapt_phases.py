@@ -17,9 +17,24 @@ fn.argtypes = [ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 64)()
 net = ab.AutoByte(L, H, synth.make_weights(synth.NetDesc(L, H)), device=0)
 batch = synth.make_adapt_batch(synth.small_fleet(B, 1), synth.log_grid(64, 64), 2)
+ft = lib.ab_debug_adapt_trace
+ft.argtypes = [ctypes.c_void_p, ctypes.c_int]
+tr = (ctypes.c_longlong * (2 * 64 * 4))()
 for _ in range(2):
+    ft(tr, 1)   # trace the first long forward tile of block 0 in this call
     net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, 1e-3, 1)
     n = fn(buf)
+ft(tr, 0)
+w = [[tr[(0 * 64 + i) * 4 + k] for k in range(4)] for i in range(64)]
+m = [[tr[(1 * 64 + i) * 4 + k] for k in range(4)] for i in range(64)]
+t0 = w[0][0]
+print("slice  W:wait_cp  W:bar  W:empty(+issue)  W:to_next | M:wait_full  M:issue   (cycles; worker t0, issuer lane 0)")
+for i in range(16):
+    if w[i][0] == 0:
+        break
+    nxt = w[i + 1][0] if w[i + 1][0] else 0
+    print(f"{i:5d} {w[i][1] - w[i][0]:9d} {w[i][2] - w[i][1]:6d} {w[i][3] - w[i][2]:9d} {nxt - w[i][3] if nxt else 0:9d} |"
+          f" {m[i][1] - m[i][0]:9d} {m[i][2] - m[i][1]:8d}   M start at {m[i][0] - t0}")
 names = [f"F{k}" for k in range(1, L + 1)] + ["OUT", "BO"] + [f"B{k}" for k in range(L, 0, -1)] + ["SGD"]
 prev = buf[0]
 for i in range(1, n):
