@@ -86,7 +86,8 @@ typedef struct {
   int32_t J;                 /* number of jobs, >= 1 */
   int32_t l_max;             /* layer stride of T, >= 1 */
   const float*   T;          /* [J][l_max][n_max] layer-wise BP time in ms; entries of
-                                layers >= n_layers[j] or workers >= n_workers[j] are ignored */
+                                layers >= n_layers[j] or workers >= n_workers[j] are ignored;
+                                16-byte aligned (else AB_E_INVALID, no launch) */
   const float*   B_down;     /* [J][n_max] download Gbps (> 0 for valid workers) */
   const float*   B_up;       /* [J][n_max] upload Gbps (> 0 for valid workers) */
   const int32_t* n_workers;  /* [J] in 1..n_max */

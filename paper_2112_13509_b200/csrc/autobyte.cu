@@ -142,6 +142,8 @@ autobyte_status check_jobs_host(autobyte_ctx* c, const autobyte_job_stats* j) {
   if (j->l_max < 1) return fail(c, AB_E_SHAPE, "l_max must be >= 1");
   if (!j->T || !j->B_down || !j->B_up || !j->n_workers || !j->n_layers || !j->model_type || !j->arch_type)
     return fail(c, AB_E_INVALID, "job stats array pointer is NULL");
+  if (reinterpret_cast<uintptr_t>(j->T) & 15u)   // K1a stages T rows with 16-byte cp.async
+    return fail(c, AB_E_INVALID, "T must be 16-byte aligned");
   return AB_OK;
 }
 

@@ -38,12 +38,13 @@ struct EncCfg {
   static constexpr int RC = (NJ * kLstm + kEncThreads - 1) / kEncThreads;   // cells per thread
   static constexpr int XS = kXDim + 2;
   static constexpr int E_OFF = 0;                         // sE [NJ][CH][16]
-  static constexpr int TL_OFF = E_OFF + NJ * CH * kEmbed;  // sTl [NJ][CH][16]; sX [NJ][XS] aliases it
-  static constexpr int H1_OFF = TL_OFF + NJ * CH * kNMax;  // sH1 [NJ][32]
+  static constexpr int TL_OFF = E_OFF + NJ * CH * kEmbed;  // sTl [2][NJ][CH][16] (T chunk ring); sX [NJ][XS] aliases it
+  static constexpr int H1_OFF = TL_OFF + 2 * NJ * CH * kNMax;  // sH1 [NJ][32]
   static constexpr int H2_OFF = H1_OFF + NJ * kLstm;       // sH2 [NJ][32]
   static constexpr int G_OFF = H2_OFF + NJ * kLstm;        // sG [NJ][128]: layer-1 gates
   static constexpr int G2_OFF = G_OFF + NJ * 4 * kLstm;    // sG2 [NJ][128]: layer-2 gates
-  static constexpr int N_OFF = G2_OFF + NJ * 4 * kLstm;    // int sN[NJ], sL[NJ]
+  static constexpr int WE_OFF = G2_OFF + NJ * 4 * kLstm;   // sWe [16][16], sBe [16]
+  static constexpr int N_OFF = WE_OFF + kEmbed * kNMax + kEmbed;   // int sN[NJ], sL[NJ]
   static constexpr int FLOATS = N_OFF + 2 * NJ;
   static constexpr size_t BYTES = sizeof(float) * FLOATS;
   static_assert(CH * kNMax >= XS, "sX must fit in the sTl chunk it aliases");
@@ -54,7 +55,9 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   using C = EncCfg<HJ>;
   extern __shared__ __align__(16) float smem[];
   float (*sE)[C::CH][kEmbed] = reinterpret_cast<float (*)[C::CH][kEmbed]>(smem + C::E_OFF);
-  float (*sTl)[C::CH][kNMax] = reinterpret_cast<float (*)[C::CH][kNMax]>(smem + C::TL_OFF);
+  float* sTring = smem + C::TL_OFF;   // two [NJ][CH][16] chunk buffers
+  float* sWe = smem + C::WE_OFF;
+  float* sBe = sWe + kEmbed * kNMax;
   float (*sX)[C::XS] = reinterpret_cast<float (*)[C::XS]>(smem + C::TL_OFF);   // after the LSTM
   float (*sH1)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H1_OFF);
   float (*sH2)[kLstm] = reinterpret_cast<float (*)[kLstm]>(smem + C::H2_OFF);
@@ -71,6 +74,8 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     sN[tid] = tid < nj ? p.n[j0 + tid] : 1;
     sL[tid] = tid < nj ? p.l[j0 + tid] : 0;
   }
+  for (int e = tid; e < kEmbed * kNMax + kEmbed; e += kEncThreads)
+    sWe[e] = e < kEmbed * kNMax ? P[p.off.W_e + e] : P[p.off.b_e + e - kEmbed * kNMax];
   for (int e = tid; e < C::NJ * kLstm; e += kEncThreads) {
     (&sH1[0][0])[e] = 0.f;
     (&sH2[0][0])[e] = 0.f;
@@ -117,6 +122,29 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     }
   };
 
+  // Raw T of one chunk (layers i0 .. i0+CH-1 of the CTA's jobs) -> ring buffer `buf` with 16-byte
+  // cp.async; padding workers (w >= n), layers (>= l) and jobs are zero-filled, and log2(1 + 0) = 0
+  // is exactly the padding value of t' (R#7), so the log pass needs no masks. The copy of chunk
+  // c+1 is in flight while chunk c's LSTM steps run.
+  auto prefetch_T = [&](int i0, int buf) {
+    float* dst = sTring + buf * (C::NJ * C::CH * kNMax);
+    for (int e = tid; e < C::NJ * C::CH * (kNMax / 4); e += kEncThreads) {
+      const int jj = e / (C::CH * (kNMax / 4)), r = e % (C::CH * (kNMax / 4)), i = r / (kNMax / 4), w0 = 4 * (r % (kNMax / 4));
+      int bytes = 0;
+      const float* src = p.T;
+      if (jj < nj && i0 + i < sL[jj]) {
+        const int left = sN[jj] - w0;
+        bytes = left >= 4 ? 16 : (left > 0 ? 4 * left : 0);
+        src = p.T + ((size_t)(j0 + jj) * p.l_max + i0 + i) * kNMax + w0;
+      }
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + e * 4)), "l"(src), "r"(bytes)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (lmax > 0) prefetch_T(0, 0);   // (sN, sL, sWe were published by the barrier above)
+  int ring = 0;
+
   // Layer wavefront: layer 1 of step t and layer 2 of step t-1 both need only h1(t-1), so their
   // gates are formed in one phase and their cells updated in the next (2 barriers per step
   // instead of 4); the loop runs one step past lmax for the last layer-2 step. Each value is
@@ -124,21 +152,22 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   for (int i0 = 0; i0 <= lmax && lmax > 0; i0 += C::CH) {
     const int len = min(C::CH, lmax - i0);   // 0 for a tail-only chunk
     const int iend = i0 + C::CH > lmax ? lmax - i0 + 1 : C::CH;
-    __syncthreads();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();   // chunk i0 landed; the previous chunk's steps are done with the other buffer
+    float (*sTl)[C::CH][kNMax] = reinterpret_cast<float (*)[C::CH][kNMax]>(sTring + ring * (C::NJ * C::CH * kNMax));
+    if (len > 0 && i0 + C::CH < lmax) prefetch_T(i0 + C::CH, ring ^ 1);
     // t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers, 0 on padding (R#7, R#8)
     for (int e = tid; e < C::NJ * len * kNMax; e += kEncThreads) {
       const int jj = e / (len * kNMax), r = e % (len * kNMax), i = r / kNMax, w = r % kNMax;
-      float v = 0.f;
-      if (jj < nj && i0 + i < sL[jj] && w < sN[jj]) v = log2f(1.0f + p.T[((size_t)(j0 + jj) * p.l_max + i0 + i) * kNMax + w]);
-      sTl[jj][i][w] = v;
+      sTl[jj][i][w] = log2f(1.0f + sTl[jj][i][w]);
     }
     __syncthreads();
     // e_i = W_e t'_i + b_e (R#4)
     for (int e = tid; e < C::NJ * len * kEmbed; e += kEncThreads) {
       const int jj = e / (len * kEmbed), r = e % (len * kEmbed), i = r / kEmbed, d = r % kEmbed;
-      float acc = P[p.off.b_e + d];
+      float acc = sBe[d];
 #pragma unroll
-      for (int w = 0; w < kNMax; ++w) acc = fmaf(P[p.off.W_e + d * kNMax + w], sTl[jj][i][w], acc);
+      for (int w = 0; w < kNMax; ++w) acc = fmaf(sWe[d * kNMax + w], sTl[jj][i][w], acc);
       sE[jj][i][d] = acc;
       if (p.stash && jj < nj && i0 + i < sL[jj]) p.stash[((size_t)(j0 + jj) * p.l_max + i0 + i) * kEncStash + d] = acc;
     }
@@ -196,6 +225,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
       if (t > 0) cell_update(sG2, sH2, c2, t - 1, kEmbed + 6 * kLstm);
       __syncthreads();
     }
+    ring ^= 1;
   }
   // ---- feature vectors x_j (Table 2; R#6-R#8)
   for (int e = tid; e < nj * kXDim; e += kEncThreads) {
