@@ -174,7 +174,44 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     __syncthreads();
     for (int i = 0; i < iend; ++i) {
       const int t = i0 + i;
-      if (t < lmax) {   // ---- layer-1 gates of step t (input e_t, h1(t-1)) -> sG
+      if (t > 0 && t < lmax) {
+        // both layers (the common case): one pass per job reads h1(t-1) once for the layer-1
+        // recurrent term and the layer-2 input, and runs 8 independent FMA chains; each gate's
+        // operation order is the one of the single-layer loops below (bit-identical results)
+        float z1[HJ], z2[HJ];
+#pragma unroll
+        for (int k = 0; k < HJ; ++k) {
+          const int jj = half * HJ + k;
+          const float4* e4 = reinterpret_cast<const float4*>(sE[jj][i]);
+          const float4* h14 = reinterpret_cast<const float4*>(sH1[jj]);
+          const float4* h24 = reinterpret_cast<const float4*>(sH2[jj]);
+          float a0 = bg1, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          float b0 = bg2, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+#pragma unroll
+          for (int q = 0; q < kEmbed / 4; ++q) {
+            const float4 v = e4[q];
+            a0 = fmaf(wx1[4 * q], v.x, a0); a1 = fmaf(wx1[4 * q + 1], v.y, a1);
+            a2 = fmaf(wx1[4 * q + 2], v.z, a2); a3 = fmaf(wx1[4 * q + 3], v.w, a3);
+          }
+#pragma unroll
+          for (int q = 0; q < kLstm / 4; ++q) {
+            const float4 v = h14[q], w = h24[q];
+            a0 = fmaf(wh1[4 * q], v.x, a0); a1 = fmaf(wh1[4 * q + 1], v.y, a1);
+            a2 = fmaf(wh1[4 * q + 2], v.z, a2); a3 = fmaf(wh1[4 * q + 3], v.w, a3);
+            b0 = fmaf(wx2[4 * q], v.x, b0); b1 = fmaf(wx2[4 * q + 1], v.y, b1);
+            b2 = fmaf(wx2[4 * q + 2], v.z, b2); b3 = fmaf(wx2[4 * q + 3], v.w, b3);
+            b0 = fmaf(wh2[4 * q], w.x, b0); b1 = fmaf(wh2[4 * q + 1], w.y, b1);
+            b2 = fmaf(wh2[4 * q + 2], w.z, b2); b3 = fmaf(wh2[4 * q + 3], w.w, b3);
+          }
+          z1[k] = (a0 + a1) + (a2 + a3);
+          z2[k] = (b0 + b1) + (b2 + b3);
+        }
+#pragma unroll
+        for (int k = 0; k < HJ; ++k) {
+          sG[half * HJ + k][g] = z1[k];
+          sG2[half * HJ + k][g] = z2[k];
+        }
+      } else if (t < lmax) {   // ---- layer-1 gates of step t (input e_t, h1(t-1)) -> sG
         float z[HJ];
 #pragma unroll
         for (int k = 0; k < HJ; ++k) {
@@ -198,8 +235,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
         }
 #pragma unroll
         for (int k = 0; k < HJ; ++k) sG[half * HJ + k][g] = z[k];
-      }
-      if (t > 0) {      // ---- layer-2 gates of step t-1 (input h1(t-1), h2(t-2)) -> sG2
+      } else if (t > 0) {      // ---- layer-2 gates of step t-1 (input h1(t-1), h2(t-2)) -> sG2
         float z[HJ];
 #pragma unroll
         for (int k = 0; k < HJ; ++k) {
