@@ -174,7 +174,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"per step 1 of {c.jobs.J} jobs x all {c.grid.C} candidates + 16-sample adapt"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -342,14 +342,27 @@ def run_ours(args):
             "per_kernel_ms": {k: prof[k] / args.steps for k in
                               ("encode_ms", "score_ms", "finalize_ms", "exchange_ms", "adapt_ms", "pack_ms")},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     net.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The bench line goes to the original stdout; everything else (NCCL's version banner when
+    NCCL_DEBUG is set, library or torch chatter) was redirected to stderr in main()."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)   # keep stdout for the one JSON line
+    os.dup2(2, 1)          # C-level printf (NCCL) and Python prints -> stderr
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
