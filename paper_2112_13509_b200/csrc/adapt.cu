@@ -229,7 +229,10 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
   const uint32_t pbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef AB_STATS
-  const bool trace_tile = g_adapt_trace_on && blockIdx.x == 0 && nk >= 8 && g.mode == 0 && g.K > 256;
+  // armed with (mode + 1) | (block << 8): the first tile of that mode with >= 8 slices on that block
+  const int arm = g_adapt_trace_on;
+  const bool trace_tile = arm && blockIdx.x == (arm >> 8) && nk >= 8 && g.mode == (arm & 255) - 1;
+  __syncthreads();   // every thread has read the arm word before thread 0 clears it
   if (trace_tile && threadIdx.x == 0) g_adapt_trace_on = 0;
   const bool trace = trace_tile && (threadIdx.x == 0 || (warp == kIssuerWarp && lane == 0));
 #endif
@@ -714,8 +717,7 @@ extern "C" int ab_debug_adapt_blocks(long long* out, int n) {
 extern "C" int ab_debug_adapt_trace(long long* out, int arm) {
   cudaDeviceSynchronize();
   if (arm) {
-    const int one = 1;
-    return cudaMemcpyToSymbol(ab::g_adapt_trace_on, &one, sizeof(int)) == cudaSuccess;
+    return cudaMemcpyToSymbol(ab::g_adapt_trace_on, &arm, sizeof(int)) == cudaSuccess;
   }
   return cudaMemcpyFromSymbol(out, ab::g_adapt_trace, sizeof(long long) * 2 * 64 * 4) == cudaSuccess;
 }

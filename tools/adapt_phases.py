@@ -20,11 +20,14 @@ batch = synth.make_adapt_batch(synth.small_fleet(B, 1), synth.log_grid(64, 64), 
 ft = lib.ab_debug_adapt_trace
 ft.argtypes = [ctypes.c_void_p, ctypes.c_int]
 tr = (ctypes.c_longlong * (2 * 64 * 4))()
+# traced tile: TRACE="mode,block" (mode 0 forward / 1 input gradient / 2 weight gradient)
+tmode, tblock = (int(v) for v in os.environ.get("TRACE", "0,0").split(","))
 for _ in range(2):
-    ft(tr, 1)   # trace the first long forward tile of block 0 in this call
+    ft(tr, (tmode + 1) | (tblock << 8))   # trace the first long tile of that mode on that block
     net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, 1e-3, 1)
     n = fn(buf)
 ft(tr, 0)
+print(f"traced tile: mode {tmode} on block {tblock}")
 w = [[tr[(0 * 64 + i) * 4 + k] for k in range(4)] for i in range(64)]
 m = [[tr[(1 * 64 + i) * 4 + k] for k in range(4)] for i in range(64)]
 t0 = w[0][0]
