@@ -35,7 +35,7 @@ template <int HJ>
 struct EncCfg {
   static constexpr int NJ = 2 * HJ;                       // jobs per CTA
   static constexpr int CH = HJ <= 8 ? 16 : 8;             // layers staged per chunk
-  static constexpr int RC = (NJ * kLstm + kEncThreads - 1) / kEncThreads;   // cells per thread
+  static constexpr int RC = (2 * NJ * kLstm + kEncThreads - 1) / kEncThreads;   // cells per thread (both layers)
   static constexpr int XS = kXDim + 2;
   static constexpr int E_OFF = 0;                         // sE [NJ][CH][16]
   static constexpr int TL_OFF = E_OFF + NJ * CH * kEmbed;  // sTl [2][NJ][CH][16] (T chunk ring); sX [NJ][XS] aliases it
@@ -90,32 +90,40 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     wh2[d] = P[p.off.l2Wh + g * kLstm + d];
   }
   const float bg1 = P[p.off.l1b + g], bg2 = P[p.off.l2b + g];
-  // cell states: thread owns cells e = tid + 256 r (job e / 32, unit e % 32) of each layer
-  float c1[C::RC], c2[C::RC];
+  // cell states: thread owns cells e = tid + 256 r of the 2·NJ·32 cells, layer 1 first (job
+  // (e mod NJ·32) / 32, unit e % 32), so the two layers' updates of a step run on different warps
+  float cst[C::RC];
 #pragma unroll
-  for (int r = 0; r < C::RC; ++r) c1[r] = c2[r] = 0.f;
+  for (int r = 0; r < C::RC; ++r) cst[r] = 0.f;
   __syncthreads();
   int lmax = 0;
   for (int k = 0; k < C::NJ; ++k) lmax = max(lmax, sL[k]);
 
-  // gates of one layer for the HJ jobs of this half: z = b + Wx in + Wh h  (4 partial sums)
+  // Cell updates of one wavefront step: layer-1 cells of step t (gates sG, t < lmax) and layer-2
+  // cells of step t-1 (gates sG2, t > 0); warp-uniform layer (NJ·32 is a multiple of 32).
   // (stash, for encoder fine-tuning: per job and step [e | i f g o c h of layer 1 | of layer 2])
-  auto cell_update = [&](float (*sGin)[4 * kLstm], float (*sHout)[kLstm], float* cst, int step, int soff) {
+  auto cell_phase = [&](int t) {
 #pragma unroll
     for (int r = 0; r < C::RC; ++r) {
       const int e = tid + r * kEncThreads;
-      if (e < C::NJ * kLstm) {
-        const int jj = e >> 5, u = e & (kLstm - 1);
-        if (step < sL[jj]) {
-          const float ig = sigmoidf_acc(sGin[jj][u]), fg = sigmoidf_acc(sGin[jj][kLstm + u]);
-          const float gg = tanh_acc(sGin[jj][2 * kLstm + u]), og = sigmoidf_acc(sGin[jj][3 * kLstm + u]);
-          cst[r] = fmaf(fg, cst[r], ig * gg);
-          const float h = og * tanh_acc(cst[r]);
-          sHout[jj][u] = h;
-          if (p.stash) {
-            float* st = p.stash + ((size_t)(j0 + jj) * p.l_max + step) * kEncStash + soff;
-            st[u] = ig; st[kLstm + u] = fg; st[2 * kLstm + u] = gg; st[3 * kLstm + u] = og;
-            st[4 * kLstm + u] = cst[r]; st[5 * kLstm + u] = h;
+      if (e < 2 * C::NJ * kLstm) {
+        const bool l2 = e >= C::NJ * kLstm;
+        const int idx = l2 ? e - C::NJ * kLstm : e, step = l2 ? t - 1 : t;
+        if (l2 ? t > 0 : t < lmax) {
+          float (*sGin)[4 * kLstm] = l2 ? sG2 : sG;
+          float (*sHout)[kLstm] = l2 ? sH2 : sH1;
+          const int jj = idx >> 5, u = idx & (kLstm - 1);
+          if (step < sL[jj]) {
+            const float ig = sigmoidf_acc(sGin[jj][u]), fg = sigmoidf_acc(sGin[jj][kLstm + u]);
+            const float gg = tanh_acc(sGin[jj][2 * kLstm + u]), og = sigmoidf_acc(sGin[jj][3 * kLstm + u]);
+            cst[r] = fmaf(fg, cst[r], ig * gg);
+            const float h = og * tanh_acc(cst[r]);
+            sHout[jj][u] = h;
+            if (p.stash) {
+              float* st = p.stash + ((size_t)(j0 + jj) * p.l_max + step) * kEncStash + (l2 ? kEmbed + 6 * kLstm : kEmbed);
+              st[u] = ig; st[kLstm + u] = fg; st[2 * kLstm + u] = gg; st[3 * kLstm + u] = og;
+              st[4 * kLstm + u] = cst[r]; st[5 * kLstm + u] = h;
+            }
           }
         }
       }
@@ -257,8 +265,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
         for (int k = 0; k < HJ; ++k) sG2[half * HJ + k][g] = z[k];
       }
       __syncthreads();
-      if (t < lmax) cell_update(sG, sH1, c1, t, kEmbed);
-      if (t > 0) cell_update(sG2, sH2, c2, t - 1, kEmbed + 6 * kLstm);
+      cell_phase(t);
       __syncthreads();
     }
     ring ^= 1;
