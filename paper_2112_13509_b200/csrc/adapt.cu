@@ -551,13 +551,17 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       const int kk = g.ksplit > 1 ? (g.K + g.ksplit - 1) / g.ksplit : g.K;
       return (kk + kTK - 1) / kTK;
     };
-    const int c1 = slices(g1), c2 = slices(g2);
-    int rr = 0;   // round-robin makespan (in slices) over CTAs b < G
-    for (int b = 0; b < G && b < t1 + t2; ++b) {
-      int c = 0;
-      for (int t = b; t < t1 + t2; t += G) c += t < t1 ? c1 : c2;
-      rr = c > rr ? c : rr;
-    }
+    const int c1 = slices(g1), c2 = slices(g2), n = t1 + t2, lim = min(G, n);
+    // round-robin makespan (in slices): CTA b holds ceil((n-b)/G) tiles, ceil((t1-b)/G) of them
+    // from g1; both counts step down once in [0, G) (at t1 % G and n % G), so the maximum over b
+    // is attained at b = 0, t1 % G or n % G (closed form: the per-CTA loop cost ~7 % of K4)
+    auto rr_cost = [&](int b) {
+      const int n1 = b < t1 ? (t1 - b + G - 1) / G : 0, k = (n - b + G - 1) / G;
+      return c1 * n1 + c2 * (k - n1);
+    };
+    int rr = lim > 0 ? rr_cost(0) : 0;
+    if (t1 % G < lim) rr = max(rr, rr_cost(t1 % G));
+    if (n % G < lim) rr = max(rr, rr_cost(n % G));
     const int rest = G - t2;
     const int ded = (t2 > 0 && rest > 0) ? max(c2, ((t1 + rest - 1) / rest) * c1) : INT_MAX;
     if (ded < rr) {
