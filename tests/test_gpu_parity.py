@@ -538,6 +538,27 @@ def test_host_entry_point_matches_device():
     check_argmax(bi_h[sample], s_ora, RTOL)
 
 
+def test_host_staging_bytes_and_alignment_check():
+    """G = 1: the host entry points stage every job's statistics (T, B_d, B_u, l, m, arc, n); a T
+    pointer that is not 16-byte aligned (K1a's cp.async rows) is refused on the host, no launch."""
+    import ctypes
+    from paper_2112_13509_b200 import autobyte as ab
+    c = synth.config("C3")
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, synth.make_weights(c.desc))
+    J, lmax = c.jobs.J, c.jobs.T.shape[1]
+    full = c.jobs.T.nbytes + c.jobs.B_d.nbytes + c.jobs.B_u.nbytes + 4 * 4 * J
+    assert net.staged_job_bytes(J, lmax) == full
+    dj, dg = dev(c.jobs, c.grid)
+    js = dj.struct()
+    js.T = js.T + 4   # misaligned by one float
+    out = [torch.empty(J, dtype=t, device="cuda") for t in (torch.int32, torch.float32, torch.float32)]
+    g = dg.struct(0, dg.C)
+    st = net.lib.autobyte_argmax(net.ctx, ctypes.byref(js), ctypes.byref(g), None, out[0].data_ptr(),
+                                 out[1].data_ptr(), out[2].data_ptr())
+    assert st == ab.AB_E_INVALID and b"16-byte" in net.lib.autobyte_last_error(net.ctx)
+    net.close()
+
+
 # ------------------------------------------------------------------------------------- fp32 path
 def make_fp32(L, H, W):
     from paper_2112_13509_b200.autobyte import AutoByte
