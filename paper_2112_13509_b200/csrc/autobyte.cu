@@ -417,7 +417,7 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
     return bail(e, "copy blob");
   c->planes = precision == AB_PREC_FP32 ? 2 : 1;
   const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers, c->planes);
-  if ((e = c->wpack.ensure(wp ? wp : 1)) != cudaSuccess) return bail(e, "alloc wpack");
+  if ((e = c->wpack.ensure(wp ? wp * kWeightReplicas : 1)) != cudaSuccess) return bail(e, "alloc wpack");
   if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
   // K2 variant: CTA pairs win when the head is deep and wide (4x512: 1158 vs 1133 TFLOP/s),
   // CTA pairs win from H = 256 up (C4 4x512: 1416 vs 1119 TFLOP/s; 3x256: 808 vs 757); single

@@ -109,7 +109,11 @@ cudaError_t launch_finalize(int J, int G, long long stride, const unsigned long 
                             float* cur_score, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
-__host__ __device__ size_t packed_weight_elems(int H, int L, int planes);
+__host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica
+#ifndef AB_WREP
+#define AB_WREP 1   // L2 replicas of the packed bf16 weights (CTA pair i streams replica i % AB_WREP)
+#endif
+constexpr int kWeightReplicas = AB_WREP;
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
 cudaError_t launch_encoder_bwd(const EncodeParams& p, const float* dX, int ldx, float* partial, int num_sms,
                                int* nparts, cudaStream_t s);                                   // K8

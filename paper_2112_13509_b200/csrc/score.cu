@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       const uint64_t pol = l2_policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
+      // this pair's (CTA's) replica of the packed weights (same bytes, different L2 lines)
+      const int rep = static_cast<int>((CG == 2 ? (blockIdx.x >> 1) : blockIdx.x) % kWeightReplicas);
+      const int rep_rows = G * C::NQ * C::NKB * C::NCH * C::NP;   // 64-element rows per replica
       for (long long u = first; u < n_units; u += stride)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
@@ -265,10 +268,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #pragma unroll
                   for (int a = 0; a < C::KBS; ++a)
                     tma_load_2d_pair(sStage + s * C::CTA_STAGE_BYTES + a * C::ATOM_BYTES, &p.wmap, 0,
-                                     (ti + a) * C::NCH + static_cast<int>(rank) * (C::NCH / 2), &full[s], pol);
+                                     rep * rep_rows + (ti + a) * C::NCH + static_cast<int>(rank) * (C::NCH / 2),
+                                     &full[s], pol);
                 } else {
                   mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-                  bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)ti * (C::NCH * 64 * C::NP),
+                  bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)rep * rep_rows * 64 + (size_t)ti * (C::NCH * 64 * C::NP),
                            C::STAGE_BYTES, &full[s], pol);
                 }
               }
@@ -771,7 +775,9 @@ __global__ void pack_kernel(const float* __restrict__ params, ParamOffsets off, 
     const int n = q * NCH + nl, k = b * 64 + kl;
     const float w = params[off.W[g + 2] + (size_t)n * H + k];
     const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-    wpack[e] = plane == 0 ? hi : __float2bfloat16_rn(w - __bfloat162float(hi));
+    const __nv_bfloat16 v = plane == 0 ? hi : __float2bfloat16_rn(w - __bfloat162float(hi));
+#pragma unroll
+    for (int r = 0; r < kWeightReplicas; ++r) wpack[e + r * total] = v;
   }
 }
 
@@ -820,7 +826,7 @@ bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const int NCH = H >= 128 ? 128 : H;
-  const size_t rows = packed_weight_elems(H, L, 1) / 64;
+  const size_t rows = packed_weight_elems(H, L, 1) / 64 * kWeightReplicas;
   if (rows == 0) { std::memset(map, 0, sizeof(*map)); return true; }
   cuuint64_t dims[2] = {64, rows};
   cuuint64_t strides[1] = {128};
