@@ -19,6 +19,17 @@ namespace ab {
 
 constexpr int kEncThreads = 256;   // 128 LSTM gate rows x 2 job halves
 
+#ifdef AB_STATS
+// K1a phase cycles of block 0 / thread 0, per launch size class: [prologue, chunk staging, gates,
+// cells, epilogue] accumulated over launches (tools/enc_phases.py)
+__device__ unsigned long long g_enc_phase[5];
+#define ENC_T(v) const long long v = clock64()
+#define ENC_ACC(i, v) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_enc_phase[i] += clock64() - (v); } while (0)
+#else
+#define ENC_T(v)
+#define ENC_ACC(i, v)
+#endif
+
 // logistic and tanh from the ex2 unit: |error| ~ 1e-7 absolute, well inside the 1e-4 / 2e-5
 // tolerance the encoder is held to against the float64 oracle (tests/test_gpu_parity.py)
 __device__ __forceinline__ float sigmoidf_acc(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
@@ -52,6 +63,7 @@ struct EncCfg {
 
 template <int HJ>
 __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_constant__ EncodeParams p) {
+  ENC_T(t_kernel);
   using C = EncCfg<HJ>;
   extern __shared__ __align__(16) float smem[];
   float (*sE)[C::CH][kEmbed] = reinterpret_cast<float (*)[C::CH][kEmbed]>(smem + C::E_OFF);
@@ -81,13 +93,36 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     (&sH2[0][0])[e] = 0.f;
   }
   float wx1[kEmbed], wh1[kLstm], wx2[kLstm], wh2[kLstm];
+  // gate row g of the four matrices: 16-byte loads when the blob offsets allow (they do for the
+  // standard layout; one branch for the whole grid). Scalar loads of a row are 64-128 bytes apart
+  // across the warp, so each one touched 32 sectors and the 112 of them cost ~27k cycles per launch
+  // (tools/enc_phases.py: half of K1a at J = 512)
+  if (((p.off.l1Wx | p.off.l1Wh | p.off.l2Wx | p.off.l2Wh) & 3) == 0) {
+    const float4* a = reinterpret_cast<const float4*>(P + p.off.l1Wx + g * kEmbed);
+    const float4* b = reinterpret_cast<const float4*>(P + p.off.l1Wh + g * kLstm);
+    const float4* c = reinterpret_cast<const float4*>(P + p.off.l2Wx + g * kLstm);
+    const float4* d4 = reinterpret_cast<const float4*>(P + p.off.l2Wh + g * kLstm);
 #pragma unroll
-  for (int d = 0; d < kEmbed; ++d) wx1[d] = P[p.off.l1Wx + g * kEmbed + d];
+    for (int q = 0; q < kEmbed / 4; ++q) {
+      const float4 v = __ldg(a + q);
+      wx1[4 * q] = v.x; wx1[4 * q + 1] = v.y; wx1[4 * q + 2] = v.z; wx1[4 * q + 3] = v.w;
+    }
 #pragma unroll
-  for (int d = 0; d < kLstm; ++d) {
-    wh1[d] = P[p.off.l1Wh + g * kLstm + d];
-    wx2[d] = P[p.off.l2Wx + g * kLstm + d];
-    wh2[d] = P[p.off.l2Wh + g * kLstm + d];
+    for (int q = 0; q < kLstm / 4; ++q) {
+      const float4 u = __ldg(b + q), v = __ldg(c + q), w = __ldg(d4 + q);
+      wh1[4 * q] = u.x; wh1[4 * q + 1] = u.y; wh1[4 * q + 2] = u.z; wh1[4 * q + 3] = u.w;
+      wx2[4 * q] = v.x; wx2[4 * q + 1] = v.y; wx2[4 * q + 2] = v.z; wx2[4 * q + 3] = v.w;
+      wh2[4 * q] = w.x; wh2[4 * q + 1] = w.y; wh2[4 * q + 2] = w.z; wh2[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < kEmbed; ++d) wx1[d] = P[p.off.l1Wx + g * kEmbed + d];
+#pragma unroll
+    for (int d = 0; d < kLstm; ++d) {
+      wh1[d] = P[p.off.l1Wh + g * kLstm + d];
+      wx2[d] = P[p.off.l2Wx + g * kLstm + d];
+      wh2[d] = P[p.off.l2Wh + g * kLstm + d];
+    }
   }
   const float bg1 = P[p.off.l1b + g], bg2 = P[p.off.l2b + g];
   // cell states: thread owns cells e = tid + 256 r of the 2·NJ·32 cells, layer 1 first (job
@@ -150,6 +185,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  ENC_ACC(0, t_kernel);
   if (lmax > 0) prefetch_T(0, 0);   // (sN, sL, sWe were published by the barrier above)
   int ring = 0;
 
@@ -160,6 +196,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   for (int i0 = 0; i0 <= lmax && lmax > 0; i0 += C::CH) {
     const int len = min(C::CH, lmax - i0);   // 0 for a tail-only chunk
     const int iend = i0 + C::CH > lmax ? lmax - i0 + 1 : C::CH;
+    ENC_T(t_chunk);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();   // chunk i0 landed; the previous chunk's steps are done with the other buffer
     float (*sTl)[C::CH][kNMax] = reinterpret_cast<float (*)[C::CH][kNMax]>(sTring + ring * (C::NJ * C::CH * kNMax));
@@ -180,8 +217,10 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
       if (p.stash && jj < nj && i0 + i < sL[jj]) p.stash[((size_t)(j0 + jj) * p.l_max + i0 + i) * kEncStash + d] = acc;
     }
     __syncthreads();
+    ENC_ACC(1, t_chunk);
     for (int i = 0; i < iend; ++i) {
       const int t = i0 + i;
+      ENC_T(t_gates);
       if (t > 0 && t < lmax) {
         // both layers (the common case): one pass per job reads h1(t-1) once for the layer-1
         // recurrent term and the layer-2 input, and runs 8 independent FMA chains; each gate's
@@ -265,11 +304,15 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
         for (int k = 0; k < HJ; ++k) sG2[half * HJ + k][g] = z[k];
       }
       __syncthreads();
+      ENC_ACC(2, t_gates);
+      ENC_T(t_cells);
       cell_phase(t);
       __syncthreads();
+      ENC_ACC(3, t_cells);
     }
     ring ^= 1;
   }
+  ENC_T(t_epi);
   // ---- feature vectors x_j (Table 2; R#6-R#8)
   for (int e = tid; e < nj * kXDim; e += kEncThreads) {
     const int jj = e / kXDim, i = e % kXDim, j = j0 + jj, n = sN[jj];
@@ -286,6 +329,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
   __syncthreads();
   for (int e = tid; e < nj * kXDim; e += kEncThreads)
     p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
+  ENC_ACC(4, t_epi);
 }
 
 // K1b: per-job projections for K2, 32 jobs per CTA, one output column per thread per pass:
@@ -488,3 +532,15 @@ cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s)
 }
 
 }  // namespace ab
+
+#ifdef AB_STATS
+extern "C" int ab_debug_enc_phases(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, ab::g_enc_phase, sizeof(unsigned long long) * 5) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[5] = {};
+    cudaMemcpyToSymbol(ab::g_enc_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
