@@ -336,16 +336,14 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 //   a[j][c]    = b1[c] + sum_i W1[c][i] x[j][i]            (job half of layer 1)
 //   what[j][c] = sum_{w < n_j} W_o[w][c] / n_j             (worker-mean fold of the output layer)
 //   beta[j]    = sum_{w < n_j} b_o[w] / n_j, and the job's arg-max keys reset to 0.
-// W1's job columns stream through shared memory in 16-wide K slices (coalesced row segments), so
-// every weight is fetched once per CTA and read conflict-free; each x_j is a broadcast LDS.128.
+// Thread c holds row c of W1's job columns in registers (16-byte loads) and W_o's column c; each
+// x_j is a broadcast LDS.128 of the transposed job block.
 constexpr int kProjJobs = 32;
 constexpr int kProjThreads = 256;
-constexpr int kProjK = 16;
 
 __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ EncodeParams p) {
   __shared__ __align__(16) float sXt[kXDim][kProjJobs];    // transposed: 4 jobs per LDS.128
   __shared__ __align__(16) float sM[kNMax][kProjJobs];     // mask / n
-  __shared__ float sW[kProjK][kProjThreads + 1];          // W1[cb + c][i0 + k] at sW[k][c]
   const int j0 = blockIdx.x * kProjJobs, tid = threadIdx.x;
   const float* P = p.params;
   const int jn = min(kProjJobs, p.J - j0);
@@ -369,45 +367,56 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
     if (p.cur_keys) p.cur_keys[j] = 0ull;
   }
   const int H = p.H;
+  __syncthreads();   // sXt / sM staged
+  const bool vec = (p.off.W[1] & 3) == 0;   // rows of W1 (84 floats) are 16-byte aligned
   for (int cb = 0; cb < H; cb += kProjThreads) {
     const int col = cb + tid;
+    if (col >= H) continue;
+    // row `col` of W1 (its 82 job columns; the last two are the candidate columns, used by K2)
+    // straight into registers with 16-byte loads: all 21 are in flight at once, no per-slice
+    // barriers (the shared-memory slice staging waited out ~12 L2 round trips per pass)
+    float w[kZDim];
+    const float* wr = P + p.off.W[1] + (size_t)col * kZDim;
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < kZDim / 4; ++q) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(wr) + q);
+        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kZDim; ++k) w[k] = wr[k];
+    }
+    float wo[kNMax];
+#pragma unroll
+    for (int ww = 0; ww < kNMax; ++ww) wo[ww] = P[p.off.W_o + (size_t)ww * H + col];
+    const float b1 = P[p.off.b[1] + col];
     float acc[kProjJobs];
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
-    for (int i0 = 0; i0 < kXDim; i0 += kProjK) {
-      const int len = min(kProjK, kXDim - i0);
-      __syncthreads();   // previous slice consumed (and sXt / sM staged on the first pass)
-      for (int e = tid; e < kProjThreads * kProjK; e += kProjThreads) {
-        const int c = e / kProjK, k = e % kProjK;
-        sW[k][c] = (cb + c < H && k < len) ? P[p.off.W[1] + (size_t)(cb + c) * kZDim + i0 + k] : 0.f;
-      }
-      __syncthreads();
-      for (int k = 0; k < len; ++k) {
-        const float w = sW[k][tid];
-        const float4* xv = reinterpret_cast<const float4*>(sXt[i0 + k]);
 #pragma unroll
-        for (int q = 0; q < kProjJobs / 4; ++q) {
-          const float4 v = xv[q];
-          acc[4 * q] = fmaf(w, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(w, v.y, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(w, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(w, v.w, acc[4 * q + 3]);
-        }
+    for (int k = 0; k < kXDim; ++k) {   // same k order as a plain dot product
+      const float4* xv = reinterpret_cast<const float4*>(sXt[k]);
+#pragma unroll
+      for (int q = 0; q < kProjJobs / 4; ++q) {
+        const float4 v = xv[q];
+        acc[4 * q] = fmaf(w[k], v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(w[k], v.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(w[k], v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(w[k], v.w, acc[4 * q + 3]);
       }
     }
-    if (col >= H) continue;
-    const float b1 = P[p.off.b[1] + col];
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj)
       if (jj < jn) p.a_out[(size_t)(j0 + jj) * p.jv + col] = acc[jj] + b1;
 #pragma unroll
     for (int jj = 0; jj < kProjJobs; ++jj) acc[jj] = 0.f;
-    for (int w = 0; w < kNMax; ++w) {
-      const float wo = P[p.off.W_o + (size_t)w * H + col];
-      const float4* mv = reinterpret_cast<const float4*>(sM[w]);
+#pragma unroll
+    for (int ww = 0; ww < kNMax; ++ww) {
+      const float4* mv = reinterpret_cast<const float4*>(sM[ww]);
 #pragma unroll
       for (int q = 0; q < kProjJobs / 4; ++q) {
         const float4 v = mv[q];
-        acc[4 * q] = fmaf(wo, v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(wo, v.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(wo, v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(wo, v.w, acc[4 * q + 3]);
+        acc[4 * q] = fmaf(wo[ww], v.x, acc[4 * q]); acc[4 * q + 1] = fmaf(wo[ww], v.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(wo[ww], v.z, acc[4 * q + 2]); acc[4 * q + 3] = fmaf(wo[ww], v.w, acc[4 * q + 3]);
       }
     }
 #pragma unroll
