@@ -150,10 +150,19 @@ autobyte_status autobyte_synchronize(autobyte_ctx* ctx);
 /* ---- multi-GPU (candidate-axis sharding) ----------------------------- */
 /* Fill 128 bytes with a fresh NCCL unique id (rank 0 calls it and broadcasts the bytes). */
 autobyte_status autobyte_get_unique_id(void* out_128_bytes);
-/* Join a world of `world` ranks (one per GPU). After this, autobyte_argmax all-reduces the
- * per-job best keys with ncclAllReduce(max, uint64) so every rank returns the global
- * result; shards must partition [0, C) across ranks. world == 1 detaches. */
+/* Join a world of `world` ranks (one per GPU; collective: every rank calls it). After this,
+ * autobyte_argmax exchanges the per-job best keys so every rank returns the global result;
+ * shards must partition [0, C) across ranks. world == 1 detaches.
+ * Exchange (§8(a) a-7): by default every rank maps the other ranks' key windows through CUDA
+ * IPC and ONE kernel stores its keys into all windows over NVLink, raises an epoch flag in each,
+ * waits for every rank's flag and takes the per-job max (exchange.cu); jobs beyond the window
+ * capacity (AUTOBYTE_PEER_JOBS, default 65536) or AUTOBYTE_EXCHANGE=nccl use ncclAllGather + a
+ * max kernel, AUTOBYTE_EXCHANGE=allreduce uses ncclAllReduce(max). The ranks agree on the mode
+ * (all mappings must succeed). Results are bit-identical in every mode and for any world. */
 autobyte_status autobyte_attach_comm(autobyte_ctx* ctx, const void* unique_id_128, int rank, int world);
+/* 1 if the NVLink peer-memory key exchange is active for this ctx, 0 otherwise (no comm, world 1,
+ * NCCL mode, or a rank could not map a peer window). */
+int32_t autobyte_peer_exchange(const autobyte_ctx* ctx);
 
 /* ---- the hot path (DEVICE pointers, asynchronous) ---------------------------------- */
 /* Encoder only: x[J][82] fp32 job feature vectors (P:402 components 1-3; "turn

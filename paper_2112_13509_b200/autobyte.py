@@ -73,7 +73,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_validate_blob", "autobyte_create", "autobyte_destroy", "autobyte_last_error",
            "autobyte_synchronize", "autobyte_get_unique_id", "autobyte_attach_comm", "autobyte_encode",
            "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
-           "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
+           "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile"]
 
 _lib = None
@@ -110,6 +110,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_argmax_host": (I32, [P, P, P, P, P, P, P]),
         "autobyte_adapt_host": (I32, [P, P, P, P, P, F32, I32, P]),
         "autobyte_staged_job_bytes": (SZ, [P, I32, I32]),
+        "autobyte_peer_exchange": (I32, [P]),
         "autobyte_topk": (I32, [P, P, P, I32, P, P]),
         "autobyte_train": (I32, [P, P, P, P, P, P, I32, P]),
         "autobyte_reset_optimizer": (I32, [P]),
@@ -382,6 +383,10 @@ class AutoByte:
                                                   cur.ctypes.data if cur is not None else None,
                                                   _ptr(out[0]), _ptr(out[1]), _ptr(out[2])), "argmax_host")
         return out
+
+    def peer_exchange(self) -> bool:
+        """True when argmax exchanges keys through the NVLink peer-memory kernel (exchange.cu)."""
+        return bool(self.lib.autobyte_peer_exchange(self.ctx))
 
     def staged_job_bytes(self, J: int, l_max: int) -> int:
         """Host-to-device bytes the *_host calls copy for J jobs' statistics on this rank."""

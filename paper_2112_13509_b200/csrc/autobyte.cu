@@ -53,6 +53,10 @@ struct DevBuf {
     ptr = nullptr;
     n = 0;
   }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
 };
 
 }  // namespace
@@ -87,6 +91,14 @@ struct autobyte_ctx {
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
   DevBuf<unsigned long long> keys_all;   // [G][2J]: every rank's keys (all-gather exchange)
   bool exchange_allreduce = false;   // AUTOBYTE_EXCHANGE=allreduce: ncclAllReduce(max) instead
+  bool exchange_nccl = false;        // AUTOBYTE_EXCHANGE=nccl|allreduce: no peer-memory window
+  // peer-memory exchange (exchange.cu): own window + IPC mappings of the other ranks' windows
+  bool peer = false;
+  DevBuf<unsigned long long> win;
+  DevBuf<unsigned int> win_counter;
+  unsigned long long* peer_win[kMaxPeers] = {};
+  long long win_cap2 = 0;            // slot stride in u64 (2 x job capacity)
+  unsigned long long epoch = 0;
   // staging for the *_host entry points
   DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
   DevBuf<int32_t> sN, sL, sM, sArc, sCur, rIdx;
@@ -228,6 +240,57 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
   }
   *out = ep;
   return AB_OK;
+}
+
+// Peer-memory window for the fused exchange (exchange.cu). Every rank allocates a window, its CUDA
+// IPC handle is all-gathered over NCCL and the other ranks' windows are mapped; the ranks then agree
+// (NCCL min) that every mapping succeeded, else all of them keep the NCCL all-gather path.
+void close_peer_window(autobyte_ctx* c) {
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (c->peer_win[r] && r != c->rank) cudaIpcCloseMemHandle(c->peer_win[r]);
+    c->peer_win[r] = nullptr;
+  }
+  c->win.release();
+  c->win_counter.release();
+  c->peer = false;
+  c->win_cap2 = 0;
+}
+
+bool setup_peer_window(autobyte_ctx* c) {
+  const int G = c->world;
+  if (G < 2 || G > kMaxPeers || c->exchange_nccl) return false;
+  const char* capenv = std::getenv("AUTOBYTE_PEER_JOBS");
+  const long long cap_jobs = capenv ? std::atoll(capenv) : 65536;
+  c->win_cap2 = 2 * (cap_jobs > 0 ? cap_jobs : 65536);
+  const size_t words = kPeerFlagWords + 2 * (size_t)G * c->win_cap2;
+  int ok = c->win.ensure(words) == cudaSuccess && c->win_counter.ensure(1) == cudaSuccess &&
+           cudaMemsetAsync(c->win.ptr, 0, words * 8, c->stream) == cudaSuccess &&
+           cudaMemsetAsync(c->win_counter.ptr, 0, sizeof(unsigned int), c->stream) == cudaSuccess;
+  cudaIpcMemHandle_t mine{};
+  if (ok) ok = cudaIpcGetMemHandle(&mine, c->win.ptr) == cudaSuccess;
+  DevBuf<uint8_t> hbuf;
+  DevBuf<int> okbuf;
+  std::vector<cudaIpcMemHandle_t> all(G);
+  if (hbuf.ensure(sizeof(cudaIpcMemHandle_t) * G) != cudaSuccess || okbuf.ensure(1) != cudaSuccess) return false;
+  cudaMemcpyAsync(hbuf.ptr + sizeof(cudaIpcMemHandle_t) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream);
+  if (ncclAllGather(hbuf.ptr + sizeof(cudaIpcMemHandle_t) * c->rank, hbuf.ptr, sizeof(cudaIpcMemHandle_t), ncclChar,
+                    c->comm, c->stream) != ncclSuccess)
+    return false;
+  cudaMemcpyAsync(all.data(), hbuf.ptr, sizeof(cudaIpcMemHandle_t) * G, cudaMemcpyDeviceToHost, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
+  for (int r = 0; r < G && ok; ++r) {
+    if (r == c->rank) { c->peer_win[r] = c->win.ptr; continue; }
+    void* ptr = nullptr;
+    ok = cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    c->peer_win[r] = static_cast<unsigned long long*>(ptr);
+  }
+  if (!ok) cudaGetLastError();   // clear a failed mapping's error before agreeing
+  cudaMemcpyAsync(okbuf.ptr, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  if (ncclAllReduce(okbuf.ptr, okbuf.ptr, 1, ncclInt, ncclMin, c->comm, c->stream) != ncclSuccess) return false;
+  int all_ok = 0;
+  cudaMemcpyAsync(&all_ok, okbuf.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
+  return all_ok == 1;
 }
 
 // Host staging of job statistics for the *_host entry points. Only this rank's K1a job range
@@ -400,6 +463,7 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   c->shard_encode = !(se && se[0] == '0');
   const char* ex = std::getenv("AUTOBYTE_EXCHANGE");
   c->exchange_allreduce = ex && std::strcmp(ex, "allreduce") == 0;
+  c->exchange_nccl = ex && (std::strcmp(ex, "nccl") == 0 || c->exchange_allreduce);
   const char* chk = std::getenv("AUTOBYTE_CHECK");
   c->check = chk && chk[0] == '1';
   auto bail = [&](cudaError_t e, const char* what) {
@@ -449,6 +513,7 @@ void autobyte_destroy(autobyte_ctx* c) {
     cudaEventDestroy(p.second.first);
     cudaEventDestroy(p.second.second);
   }
+  close_peer_window(c);
   if (c->comm) ncclCommDestroy(c->comm);
   c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
   c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
@@ -485,6 +550,7 @@ autobyte_status autobyte_attach_comm(autobyte_ctx* c, const void* uid, int rank,
   if (world < 1 || rank < 0 || rank >= world) return fail(c, AB_E_INVALID, "bad rank/world");
   DeviceGuard guard(c->device);
   if (c->comm) {
+    close_peer_window(c);
     ncclCommDestroy(c->comm);
     c->comm = nullptr;
   }
@@ -499,8 +565,12 @@ autobyte_status autobyte_attach_comm(autobyte_ctx* c, const void* uid, int rank,
     c->comm = nullptr;
     return fail(c, AB_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
+  c->peer = setup_peer_window(c);
+  if (!c->peer) close_peer_window(c);
   return AB_OK;
 }
+
+int32_t autobyte_peer_exchange(const autobyte_ctx* c) { return c && c->peer ? 1 : 0; }
 
 autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs, float* x_out) {
   if (!c) return AB_E_INVALID;
@@ -543,6 +613,16 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
   // per-job max is folded into K5), or with AUTOBYTE_EXCHANGE=allreduce reduced by ncclAllReduce(max)
   const unsigned long long* kin = c->keys.ptr;
   int G = 1;
+  if (c->comm && c->world > 1 && c->peer && 2LL * J <= c->win_cap2) {
+    // fused K3 + K5 over NVLink peer memory (exchange.cu)
+    PeerExchangeParams xp{};
+    for (int r = 0; r < c->world; ++r) xp.win[r] = c->peer_win[r];
+    xp.keys = c->keys.ptr; xp.counter = c->win_counter.ptr;
+    xp.best_idx = best_idx; xp.best_score = best_score; xp.cur_score = cur_score;
+    xp.epoch = ++c->epoch; xp.cap2 = c->win_cap2; xp.J = J; xp.G = c->world; xp.rank = c->rank;
+    AB_CUDA(c, timed(c, K_EXCHANGE, [&] { return launch_peer_exchange(xp, c->num_sms, c->stream); }));
+    return AB_OK;
+  }
   if (c->comm && c->world > 1) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }

@@ -107,6 +107,19 @@ cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_sco
 cudaError_t launch_finalize(int J, int G, long long stride, const unsigned long long* keys,
                             const unsigned long long* cur_keys, int32_t* best_idx, float* best_score,
                             float* cur_score, cudaStream_t s);
+// K3+K5 over NVLink peer memory (exchange.cu): windows are [kPeerFlagWords flags | 2][G][cap2] u64
+constexpr int kPeerFlagWords = 64;
+constexpr int kMaxPeers = 8;
+struct PeerExchangeParams {
+  unsigned long long* win[kMaxPeers];   // every rank's window (IPC-mapped; win[rank] is the own one)
+  const unsigned long long* keys;       // [2J] this rank's keys (K2)
+  unsigned int* counter;                // per-rank block counter (zero between calls)
+  int32_t* best_idx; float* best_score; float* cur_score;
+  unsigned long long epoch;             // >= 1, grows by one per call
+  long long cap2;                       // slot stride (u64), >= 2J
+  int J, G, rank;
+};
+cudaError_t launch_peer_exchange(const PeerExchangeParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica

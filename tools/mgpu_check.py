@@ -34,7 +34,8 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
     allp = [torch.empty_like(packed) for _ in range(world)]
     dist.all_gather(allp, packed)
     same_all_ranks = all(torch.equal(allp[0], x) for x in allp)
-    res = {"config": name, "world": world, "cta_group": cg, "same_on_all_ranks": same_all_ranks}
+    res = {"config": name, "world": world, "cta_group": cg, "same_on_all_ranks": same_all_ranks,
+           "peer_exchange": net.peer_exchange()}
     # host entry point: each rank copies only its encoder shard of the statistics -> same results
     hb, hs, hc = net.argmax_host(jobs, grid, cur.cpu().numpy(), b, e)
     res["host_same_as_device"] = bool(np.array_equal(hb, bi.cpu().numpy())
@@ -104,13 +105,21 @@ def main():
               synth.log_grid(64, 64), 2),
              ("C4-subset-ragged-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(33)),
               synth.log_grid(45, 23), 2)]
-    for name, desc, jobs, grid, cg in cases:
+    # both key exchanges: the fused peer-memory kernel (default) and the NCCL all-gather + K5
+    runs = [(mode,) + case for mode in ("peer", "nccl") for case in cases]
+    for mode, name, desc, jobs, grid, cg in runs:  # noqa: B007
+        if mode == "nccl":
+            os.environ["AUTOBYTE_EXCHANGE"] = "nccl"
+        else:
+            os.environ.pop("AUTOBYTE_EXCHANGE", None)
         r = run(name, desc, jobs, grid, cg, dev, rank, world)
+        r["exchange"] = mode
         if rank == 0:
             print(json.dumps(r), flush=True)
             ok &= (r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
                    and r["topk_same_on_all_ranks"] and r["topk_g_invariant"] and r["host_same_as_device"]
-                   and r["adapt_host_same_as_device"] and (world == 1 or r["host_staged_fraction"] < 0.75))
+                   and r["adapt_host_same_as_device"] and (world == 1 or r["host_staged_fraction"] < 0.75)
+                   and r["peer_exchange"] == (world > 1 and mode == "peer"))
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
