@@ -327,8 +327,28 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
     sX[jj][i] = v;
   }
   __syncthreads();
-  for (int e = tid; e < nj * kXDim; e += kEncThreads)
-    p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
+  if (p.xG <= 1) {
+    for (int e = tid; e < nj * kXDim; e += kEncThreads)
+      p.x_out[(size_t)(j0 + e / kXDim) * kXDim + e % kXDim] = sX[e / kXDim][e % kXDim];
+  } else {
+    // x all-gather fused into the epilogue: the rows go straight into every rank's window over
+    // NVLink (own window included); the last CTA of this rank raises its flag in every window
+    for (int e = tid; e < nj * kXDim; e += kEncThreads) {
+      const float v = sX[e / kXDim][e % kXDim];
+      const size_t o = (size_t)(j0 + e / kXDim) * kXDim + e % kXDim;
+#pragma unroll 1
+      for (int r = 0; r < p.xG; ++r) p.xg[r][o] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(p.xcounter, 1u) == gridDim.x - 1) {
+      *p.xcounter = 0u;
+      __threadfence_system();
+#pragma unroll 1
+      for (int r = 0; r < p.xG; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.xflag[r] + p.xrank), "l"(p.xepoch) : "memory");
+    }
+  }
   ENC_ACC(4, t_epi);
 }
 
@@ -439,7 +459,8 @@ cudaError_t launch_lstm_hj(const EncodeParams& p, cudaStream_t s) {
     attr_done |= 1ull << (dev & 63);
   }
   const int n = p.j_end - p.j_begin;
-  encode_kernel<HJ><<<(n + C::NJ - 1) / C::NJ, kEncThreads, C::BYTES, s>>>(p);
+  const int blocks = n > 0 ? (n + C::NJ - 1) / C::NJ : 1;
+  encode_kernel<HJ><<<blocks, kEncThreads, C::BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -450,7 +471,8 @@ int encode_jobs_per_half(int n, int num_sms) {
 
 // K1a over jobs [p.j_begin, p.j_end): writes rows of p.x_out (global job index).
 cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s) {
-  if (p.j_end <= p.j_begin) return cudaSuccess;
+  // (an empty range still launches one CTA when its flag must be raised for the x all-gather)
+  if (p.j_end <= p.j_begin && p.xG <= 1) return cudaSuccess;
   switch (encode_jobs_per_half(p.j_end - p.j_begin, num_sms)) {
     case 1: return launch_lstm_hj<1>(p, s);
     case 2: return launch_lstm_hj<2>(p, s);

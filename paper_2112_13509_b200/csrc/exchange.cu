@@ -88,6 +88,26 @@ __global__ void __launch_bounds__(256) peer_exchange_kernel(const __grid_constan
   }
 }
 
+// Consumers of the x all-gather (K1b, K4) run after this on the stream: the fused K1a epilogue
+// (encode.cu) stores every rank's rows into this rank's window before raising its flag.
+__global__ void peer_wait_kernel(const unsigned long long* flags, int G, unsigned long long epoch, int rank) {
+  if (threadIdx.x >= G) return;
+  const long long t0 = clock64();
+  while (ld_acquire_sys(flags + threadIdx.x) < epoch) {
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("autobyte: x all-gather watchdog (rank %d waiting for rank %d, epoch %llu)\n", rank, threadIdx.x, epoch);
+      __trap();
+    }
+  }
+  __threadfence();
+}
+
+cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch, int rank,
+                             cudaStream_t s) {
+  peer_wait_kernel<<<1, 32, 0, s>>>(flags, G, epoch, rank);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_peer_exchange(const PeerExchangeParams& p, int num_sms, cudaStream_t s) {
   const long long n2 = 2LL * p.J;
   long long nb = (n2 + 255) / 256;

@@ -48,6 +48,13 @@ struct EncodeParams {
   unsigned long long* keys;      // [J] reset to 0, or null
   unsigned long long* cur_keys;  // [J] reset to 0, or null
   float* stash;        // [J][l_max][kEncStash] forward states for encoder fine-tuning, or null
+  // G > 1 with the peer-memory window: K1a also stores its x rows into every rank's window
+  // (xg[r], row j at xg[r] + j*82; xg[rank] == x_out) and its last CTA raises xflag[r][rank] = epoch
+  int xG, xrank;
+  float* xg[8];
+  unsigned long long* xflag[8];
+  unsigned int* xcounter;
+  unsigned long long xepoch;
 };
 
 struct alignas(64) ScoreParams {
@@ -108,7 +115,8 @@ cudaError_t launch_finalize(int J, int G, long long stride, const unsigned long 
                             const unsigned long long* cur_keys, int32_t* best_idx, float* best_score,
                             float* cur_score, cudaStream_t s);
 // K3+K5 over NVLink peer memory (exchange.cu): windows are [kPeerFlagWords flags | 2][G][cap2] u64
-constexpr int kPeerFlagWords = 64;
+constexpr int kPeerFlagWords = 64;   // [0, 32): key-exchange flags, [32, 64): x all-gather flags
+constexpr int kPeerXFlags = 32;
 constexpr int kMaxPeers = 8;
 struct PeerExchangeParams {
   unsigned long long* win[kMaxPeers];   // every rank's window (IPC-mapped; win[rank] is the own one)
@@ -120,6 +128,9 @@ struct PeerExchangeParams {
   int J, G, rank;
 };
 cudaError_t launch_peer_exchange(const PeerExchangeParams& p, int num_sms, cudaStream_t s);
+// one warp waits until flags[r] >= epoch for r < G (stream order then holds the consumers back)
+cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch, int rank,
+                             cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica

@@ -104,14 +104,19 @@ def main():
              ("C4-subset-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(300)),
               synth.log_grid(64, 64), 2),
              ("C4-subset-ragged-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(33)),
-              synth.log_grid(45, 23), 2)]
-    # both key exchanges: the fused peer-memory kernel (default) and the NCCL all-gather + K5
-    runs = [(mode,) + case for mode in ("peer", "nccl") for case in cases]
+              synth.log_grid(45, 23), 2),
+             # fewer jobs than ranks at G = 4: a rank with an empty encoder shard still takes part
+             ("C3-three-jobs", c3.desc, c3.jobs.subset(np.arange(3)), synth.log_grid(5, 3), 1)]
+    # every exchange: the fused peer-memory key kernel (default), the same plus the x all-gather
+    # fused into K1a's epilogue (opt-in AUTOBYTE_PEER_X=1), and NCCL all-gathers + K5
+    runs = [(mode,) + case for mode in ("peer", "peer_x", "nccl") for case in cases]
     for mode, name, desc, jobs, grid, cg in runs:  # noqa: B007
+        os.environ.pop("AUTOBYTE_EXCHANGE", None)
+        os.environ.pop("AUTOBYTE_PEER_X", None)
         if mode == "nccl":
             os.environ["AUTOBYTE_EXCHANGE"] = "nccl"
-        else:
-            os.environ.pop("AUTOBYTE_EXCHANGE", None)
+        elif mode == "peer_x":
+            os.environ["AUTOBYTE_PEER_X"] = "1"
         r = run(name, desc, jobs, grid, cg, dev, rank, world)
         r["exchange"] = mode
         if rank == 0:
@@ -119,7 +124,7 @@ def main():
             ok &= (r["same_on_all_ranks"] and r["g_invariant"] and r["adapt_same_on_all_ranks"] and r["adapt_g_invariant"]
                    and r["topk_same_on_all_ranks"] and r["topk_g_invariant"] and r["host_same_as_device"]
                    and r["adapt_host_same_as_device"] and (world == 1 or r["host_staged_fraction"] < 0.75)
-                   and r["peer_exchange"] == (world > 1 and mode == "peer"))
+                   and r["peer_exchange"] == (world > 1 and mode != "nccl"))
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
