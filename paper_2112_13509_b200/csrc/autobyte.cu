@@ -247,7 +247,7 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
     ep.xG = G; ep.xrank = c->rank; ep.xcounter = c->win_xcounter.ptr; ep.xepoch = e;
     ep.x_out = ep.xg[c->rank];
     AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
-    AB_CUDA(c, timed(c, K_EXCHANGE, [&] { return launch_peer_wait(c->win.ptr + kPeerXFlags, G, e, c->rank, c->stream); }));
+    AB_CUDA(c, timed(c, K_OTHER, [&] { return launch_peer_wait(c->win.ptr + kPeerXFlags, G, e, c->rank, c->stream); }));
     ep.xG = 0;   // K1b and later launches with these params are not part of the gather
     *out = ep;
     return AB_OK;
@@ -653,7 +653,9 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
     xp.keys = c->keys.ptr; xp.counter = c->win_counter.ptr;
     xp.best_idx = best_idx; xp.best_score = best_score; xp.cur_score = cur_score;
     xp.epoch = ++c->epoch; xp.cap2 = c->win_cap2; xp.J = J; xp.G = c->world; xp.rank = c->rank;
-    AB_CUDA(c, timed(c, K_EXCHANGE, [&] { return launch_peer_exchange(xp, c->num_sms, c->stream); }));
+    // (profiled as K5, whose work it includes: finalize_ms then also holds the wait for the
+    // slowest rank, exchange_ms only the NCCL x all-gathers)
+    AB_CUDA(c, timed(c, K_FINALIZE, [&] { return launch_peer_exchange(xp, c->num_sms, c->stream); }));
     return AB_OK;
   }
   if (c->comm && c->world > 1) {
