@@ -260,7 +260,10 @@ autobyte_status autobyte_trigger(autobyte_ctx* ctx, int32_t J, const int32_t* be
  * (world > 1) every rank still passes the full job arrays, but only the statistics of the
  * jobs its own encoder shard reads (T, B_down, B_up, n_layers, model_type, arch_type of
  * ceil(J/world) jobs) are copied; n_workers is copied for all jobs. AUTOBYTE_CHECK=1 copies
- * everything (the range checks read every job). */
+ * everything (the range checks read every job). When T is in page-locked (pinned / registered)
+ * host memory it is not staged: the encoder kernel reads its shard of T over PCIe itself, so the
+ * transfer overlaps the LSTM steps (AUTOBYTE_ZERO_COPY=0 disables this); the caller must not
+ * modify T until the call returns, which it does only after the results are on the host. */
 
 /* Host-to-device bytes the staging above moves for the job statistics of J jobs with
  * l_max layers on this rank (the e2e accounting of bench.py). Returns 0 for a NULL ctx. */

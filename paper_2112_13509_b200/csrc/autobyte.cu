@@ -105,6 +105,7 @@ struct autobyte_ctx {
   size_t win_xoff = 0;               // u64 word offset of the x region in a window
   unsigned long long xepoch = 0;
   bool peer_x = false;               // AUTOBYTE_PEER_X=1: x all-gather through the windows (opt-in)
+  bool zero_copy = true;             // *_host: K1a reads page-locked T over PCIe (AUTOBYTE_ZERO_COPY=0 off)
   // staging for the *_host entry points
   DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
   DevBuf<int32_t> sN, sL, sM, sArc, sCur, rIdx;
@@ -328,7 +329,11 @@ bool setup_peer_window(autobyte_ctx* c) {
 // reads T, B_d, B_u, l, m and arc (every rank encodes 1/G of the jobs and all-gathers x), so only
 // that slice crosses PCIe, copied to its global offset; n is read for every job (K1b's worker
 // mean, K4's mask). With AUTOBYTE_CHECK=1 everything is copied (the range checks read all jobs).
-cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs) {
+// T (three quarters of the bytes) is not staged when it lives in page-locked host memory: K1a then
+// streams its shard of T over PCIe itself (its cp.async chunk prefetch reads the mapped host
+// buffer), so the transfer overlaps the LSTM steps instead of preceding them. *T_dev is the
+// pointer K1a reads. AUTOBYTE_ZERO_COPY=0 always stages.
+cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs, const float** T_dev) {
   const int J = jobs->J;
   int jb = 0, je = J;
   encode_range(c, J, &jb, &je);
@@ -338,7 +343,15 @@ cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs) {
     return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream) : cudaSuccess;
   };
   cudaError_t e;
-  if ((e = h2d(c->sT.ptr + jb * lt, jobs->T + jb * lt, nj * lt * 4)) != cudaSuccess) return e;
+  *T_dev = c->sT.ptr;
+  cudaPointerAttributes pa{};
+  if (c->zero_copy && !c->check && cudaPointerGetAttributes(&pa, jobs->T) == cudaSuccess &&
+      pa.type == cudaMemoryTypeHost && pa.devicePointer) {
+    *T_dev = static_cast<const float*>(pa.devicePointer);
+  } else {
+    cudaGetLastError();   // (pageable memory: clear the query's error, stage as usual)
+    if ((e = h2d(c->sT.ptr + jb * lt, jobs->T + jb * lt, nj * lt * 4)) != cudaSuccess) return e;
+  }
   if ((e = h2d(c->sBd.ptr + (size_t)jb * kNMax, jobs->B_down + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
   if ((e = h2d(c->sBu.ptr + (size_t)jb * kNMax, jobs->B_up + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
   if ((e = h2d(c->sN.ptr, jobs->n_workers, (size_t)J * 4)) != cudaSuccess) return e;
@@ -495,6 +508,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   const char* ex = std::getenv("AUTOBYTE_EXCHANGE");
   c->exchange_allreduce = ex && std::strcmp(ex, "allreduce") == 0;
   c->exchange_nccl = ex && (std::strcmp(ex, "nccl") == 0 || c->exchange_allreduce);
+  const char* zc = std::getenv("AUTOBYTE_ZERO_COPY");
+  c->zero_copy = !(zc && zc[0] == '0');
   const char* px = std::getenv("AUTOBYTE_PEER_X");
   c->peer_x = px && px[0] == '1';
   const char* chk = std::getenv("AUTOBYTE_CHECK");
@@ -891,12 +906,13 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
   AB_CUDA(c, c->rIdx.ensure(J)); AB_CUDA(c, c->rScore.ensure(J)); AB_CUDA(c, c->rCur.ensure(J));
   if (cur_idx) AB_CUDA(c, c->sCur.ensure(J));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  AB_CUDA(c, stage_jobs_host(c, jobs));
+  const float* T_dev = nullptr;
+  AB_CUDA(c, stage_jobs_host(c, jobs, &T_dev));
   AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
   if (cur_idx) AB_CUDA(c, h2d(c->sCur.ptr, cur_idx, (size_t)J * 4));
   autobyte_job_stats dj = *jobs;
-  dj.T = c->sT.ptr; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
+  dj.T = T_dev; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
   dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
   autobyte_grid dg = *grid;
   dg.partition_bytes = reinterpret_cast<const int64_t*>(c->sSp.ptr); dg.credit_mult = c->sSc.ptr;
@@ -926,12 +942,13 @@ autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* s
   AB_CUDA(c, c->sSp.ensure(B)); AB_CUDA(c, c->sSc.ensure(B)); AB_CUDA(c, c->sV.ensure((size_t)B * kNMax));
   AB_CUDA(c, c->loss_tmp.ensure(1));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  AB_CUDA(c, stage_jobs_host(c, samples));
+  const float* T_dev = nullptr;
+  AB_CUDA(c, stage_jobs_host(c, samples, &T_dev));
   AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
   AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));
   autobyte_job_stats dj = *samples;
-  dj.T = c->sT.ptr; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
+  dj.T = T_dev; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
   dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
   s = autobyte_adapt(c, &dj, reinterpret_cast<const int64_t*>(c->sSp.ptr), c->sSc.ptr, c->sV.ptr, lr, steps,
                      loss_before ? c->loss_tmp.ptr : nullptr);

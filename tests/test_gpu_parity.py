@@ -538,6 +538,33 @@ def test_host_entry_point_matches_device():
     check_argmax(bi_h[sample], s_ora, RTOL)
 
 
+def test_host_entry_points_read_pinned_T_in_place():
+    """Page-locked T is read by K1a over PCIe (no staging copy): same bits as the device path,
+    for argmax_host and adapt_host."""
+    import copy
+    c = synth.config("C3")
+    W = synth.make_weights(c.desc)
+    pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory().numpy()
+    jobs = copy.copy(c.jobs)
+    jobs.T = pin(c.jobs.T)
+    cur = synth.current_configs(c.jobs.J, c.grid.C, 4)
+    net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    bi_h, bs_h, cs_h = net.argmax_host(jobs, c.grid, cur)
+    bi_d, bs_d, cs_d = gpu_argmax(net, c.jobs, c.grid, cur)
+    assert np.array_equal(bi_h, bi_d) and np.array_equal(bs_h, bs_d) and np.array_equal(cs_h, cs_d)
+    batch = synth.make_adapt_batch(c.jobs, c.grid, 5)
+    pb = copy.copy(batch)
+    pb.jobs = copy.copy(batch.jobs)
+    pb.jobs.T = pin(batch.jobs.T)
+    l_pinned = net.adapt_host(pb.jobs, pb.S_p, pb.S_c, pb.V_bar, 1e-3, 1)
+    w_pinned = net.get_weights_blob()
+    net2 = make(c.desc.hidden_layers, c.desc.hidden_width, W)
+    l_paged = net2.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, 1e-3, 1)
+    assert l_pinned == l_paged and w_pinned == net2.get_weights_blob()
+    net.close()
+    net2.close()
+
+
 def test_host_staging_bytes_and_alignment_check():
     """G = 1: the host entry points stage every job's statistics (T, B_d, B_u, l, m, arc, n); a T
     pointer that is not 16-byte aligned (K1a's cp.async rows) is refused on the host, no launch."""
