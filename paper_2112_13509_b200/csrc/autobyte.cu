@@ -329,35 +329,41 @@ bool setup_peer_window(autobyte_ctx* c) {
 // reads T, B_d, B_u, l, m and arc (every rank encodes 1/G of the jobs and all-gathers x), so only
 // that slice crosses PCIe, copied to its global offset; n is read for every job (K1b's worker
 // mean, K4's mask). With AUTOBYTE_CHECK=1 everything is copied (the range checks read all jobs).
-// T (three quarters of the bytes) is not staged when it lives in page-locked host memory: K1a then
-// streams its shard of T over PCIe itself (its cp.async chunk prefetch reads the mapped host
-// buffer), so the transfer overlaps the LSTM steps instead of preceding them. *T_dev is the
-// pointer K1a reads. AUTOBYTE_ZERO_COPY=0 always stages.
-cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs, const float** T_dev) {
+// Arrays read by K1a alone (T -- three quarters of the bytes --, B_down, B_up, n_layers, model_type,
+// arch_type) are not staged when they live in page-locked host memory: K1a reads its shard of them
+// over PCIe itself (its cp.async chunk prefetch streams T from the mapped host buffer), so the
+// transfer overlaps the LSTM steps and no copy is issued. n_workers (also read by K1b and K4) is
+// always copied. *dj receives the pointers the kernels read. AUTOBYTE_ZERO_COPY=0 always stages.
+cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs, autobyte_job_stats* dj) {
   const int J = jobs->J;
   int jb = 0, je = J;
   encode_range(c, J, &jb, &je);
   if (c->check) { jb = 0; je = J; }
   const size_t nj = (size_t)(je - jb), lt = (size_t)jobs->l_max * kNMax;
-  auto h2d = [&](void* d, const void* h, size_t bytes) {
-    return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream) : cudaSuccess;
-  };
-  cudaError_t e;
-  *T_dev = c->sT.ptr;
-  cudaPointerAttributes pa{};
-  if (c->zero_copy && !c->check && cudaPointerGetAttributes(&pa, jobs->T) == cudaSuccess &&
-      pa.type == cudaMemoryTypeHost && pa.devicePointer) {
-    *T_dev = static_cast<const float*>(pa.devicePointer);
-  } else {
+  cudaError_t e = cudaSuccess;
+  // in place if page-locked, else copy the rank's slice [jb, je) (row width w elements of size es)
+  auto place = [&](const void* h, void* staging, size_t w, size_t es) -> const void* {
+    cudaPointerAttributes pa{};
+    if (c->zero_copy && !c->check && cudaPointerGetAttributes(&pa, h) == cudaSuccess &&
+        pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      return pa.devicePointer;
     cudaGetLastError();   // (pageable memory: clear the query's error, stage as usual)
-    if ((e = h2d(c->sT.ptr + jb * lt, jobs->T + jb * lt, nj * lt * 4)) != cudaSuccess) return e;
-  }
-  if ((e = h2d(c->sBd.ptr + (size_t)jb * kNMax, jobs->B_down + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
-  if ((e = h2d(c->sBu.ptr + (size_t)jb * kNMax, jobs->B_up + (size_t)jb * kNMax, nj * kNMax * 4)) != cudaSuccess) return e;
-  if ((e = h2d(c->sN.ptr, jobs->n_workers, (size_t)J * 4)) != cudaSuccess) return e;
-  if ((e = h2d(c->sL.ptr + jb, jobs->n_layers + jb, nj * 4)) != cudaSuccess) return e;
-  if ((e = h2d(c->sM.ptr + jb, jobs->model_type + jb, nj * 4)) != cudaSuccess) return e;
-  return h2d(c->sArc.ptr + jb, jobs->arch_type + jb, nj * 4);
+    const size_t off = (size_t)jb * w * es, bytes = nj * w * es;
+    if (bytes && e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(staging) + off, static_cast<const uint8_t*>(h) + off, bytes,
+                          cudaMemcpyHostToDevice, c->stream);
+    return staging;
+  };
+  *dj = *jobs;
+  dj->T = static_cast<const float*>(place(jobs->T, c->sT.ptr, lt, 4));
+  dj->B_down = static_cast<const float*>(place(jobs->B_down, c->sBd.ptr, kNMax, 4));
+  dj->B_up = static_cast<const float*>(place(jobs->B_up, c->sBu.ptr, kNMax, 4));
+  dj->n_layers = static_cast<const int32_t*>(place(jobs->n_layers, c->sL.ptr, 1, 4));
+  dj->model_type = static_cast<const int32_t*>(place(jobs->model_type, c->sM.ptr, 1, 4));
+  dj->arch_type = static_cast<const int32_t*>(place(jobs->arch_type, c->sArc.ptr, 1, 4));
+  if (e != cudaSuccess) return e;
+  dj->n_workers = c->sN.ptr;
+  return cudaMemcpyAsync(c->sN.ptr, jobs->n_workers, (size_t)J * 4, cudaMemcpyHostToDevice, c->stream);
 }
 
 // Bytes the *_host staging above moves for J jobs on this rank (for the e2e accounting).
@@ -906,14 +912,11 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
   AB_CUDA(c, c->rIdx.ensure(J)); AB_CUDA(c, c->rScore.ensure(J)); AB_CUDA(c, c->rCur.ensure(J));
   if (cur_idx) AB_CUDA(c, c->sCur.ensure(J));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  const float* T_dev = nullptr;
-  AB_CUDA(c, stage_jobs_host(c, jobs, &T_dev));
+  autobyte_job_stats dj{};
+  AB_CUDA(c, stage_jobs_host(c, jobs, &dj));
   AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
   if (cur_idx) AB_CUDA(c, h2d(c->sCur.ptr, cur_idx, (size_t)J * 4));
-  autobyte_job_stats dj = *jobs;
-  dj.T = T_dev; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
-  dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
   autobyte_grid dg = *grid;
   dg.partition_bytes = reinterpret_cast<const int64_t*>(c->sSp.ptr); dg.credit_mult = c->sSc.ptr;
   s = autobyte_argmax(c, &dj, &dg, cur_idx ? c->sCur.ptr : nullptr, c->rIdx.ptr, c->rScore.ptr,
@@ -942,14 +945,11 @@ autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* s
   AB_CUDA(c, c->sSp.ensure(B)); AB_CUDA(c, c->sSc.ensure(B)); AB_CUDA(c, c->sV.ensure((size_t)B * kNMax));
   AB_CUDA(c, c->loss_tmp.ensure(1));
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
-  const float* T_dev = nullptr;
-  AB_CUDA(c, stage_jobs_host(c, samples, &T_dev));
+  autobyte_job_stats dj{};
+  AB_CUDA(c, stage_jobs_host(c, samples, &dj));
   AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
   AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
   AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));
-  autobyte_job_stats dj = *samples;
-  dj.T = T_dev; dj.B_down = c->sBd.ptr; dj.B_up = c->sBu.ptr;
-  dj.n_workers = c->sN.ptr; dj.n_layers = c->sL.ptr; dj.model_type = c->sM.ptr; dj.arch_type = c->sArc.ptr;
   s = autobyte_adapt(c, &dj, reinterpret_cast<const int64_t*>(c->sSp.ptr), c->sSc.ptr, c->sV.ptr, lr, steps,
                      loss_before ? c->loss_tmp.ptr : nullptr);
   if (s != AB_OK) return s;

@@ -539,14 +539,15 @@ def test_host_entry_point_matches_device():
 
 
 def test_host_entry_points_read_pinned_T_in_place():
-    """Page-locked T is read by K1a over PCIe (no staging copy): same bits as the device path,
-    for argmax_host and adapt_host."""
+    """Page-locked encoder inputs (T, B_d, B_u, l, m, arc) are read by K1a over PCIe (no staging
+    copy): same bits as the device path, for argmax_host and adapt_host."""
     import copy
     c = synth.config("C3")
     W = synth.make_weights(c.desc)
     pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory().numpy()
     jobs = copy.copy(c.jobs)
-    jobs.T = pin(c.jobs.T)
+    for f in ("T", "B_d", "B_u", "l", "m", "arc"):   # (n stays pageable: it is always copied)
+        setattr(jobs, f, pin(getattr(c.jobs, f)))
     cur = synth.current_configs(c.jobs.J, c.grid.C, 4)
     net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
     bi_h, bs_h, cs_h = net.argmax_host(jobs, c.grid, cur)
@@ -555,7 +556,8 @@ def test_host_entry_points_read_pinned_T_in_place():
     batch = synth.make_adapt_batch(c.jobs, c.grid, 5)
     pb = copy.copy(batch)
     pb.jobs = copy.copy(batch.jobs)
-    pb.jobs.T = pin(batch.jobs.T)
+    for f in ("T", "B_d", "B_u", "n", "l", "m", "arc"):
+        setattr(pb.jobs, f, pin(getattr(batch.jobs, f)))
     l_pinned = net.adapt_host(pb.jobs, pb.S_p, pb.S_c, pb.V_bar, 1e-3, 1)
     w_pinned = net.get_weights_blob()
     net2 = make(c.desc.hidden_layers, c.desc.hidden_width, W)
