@@ -334,6 +334,16 @@ bool setup_peer_window(autobyte_ctx* c) {
 // over PCIe itself (its cp.async chunk prefetch streams T from the mapped host buffer), so the
 // transfer overlaps the LSTM steps and no copy is issued. n_workers (also read by K1b and K4) is
 // always copied. *dj receives the pointers the kernels read. AUTOBYTE_ZERO_COPY=0 always stages.
+// Device address of a page-locked host buffer (zero-copy), or nullptr (pageable: must be copied).
+const void* host_in_place(const autobyte_ctx* c, const void* h) {
+  cudaPointerAttributes pa{};
+  if (c->zero_copy && !c->check && cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+      pa.devicePointer)
+    return pa.devicePointer;
+  cudaGetLastError();   // (pageable memory: clear the query's error)
+  return nullptr;
+}
+
 cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs, autobyte_job_stats* dj) {
   const int J = jobs->J;
   int jb = 0, je = J;
@@ -343,11 +353,7 @@ cudaError_t stage_jobs_host(autobyte_ctx* c, const autobyte_job_stats* jobs, aut
   cudaError_t e = cudaSuccess;
   // in place if page-locked, else copy the rank's slice [jb, je) (row width w elements of size es)
   auto place = [&](const void* h, void* staging, size_t w, size_t es) -> const void* {
-    cudaPointerAttributes pa{};
-    if (c->zero_copy && !c->check && cudaPointerGetAttributes(&pa, h) == cudaSuccess &&
-        pa.type == cudaMemoryTypeHost && pa.devicePointer)
-      return pa.devicePointer;
-    cudaGetLastError();   // (pageable memory: clear the query's error, stage as usual)
+    if (const void* d = host_in_place(c, h)) return d;
     const size_t off = (size_t)jb * w * es, bytes = nj * w * es;
     if (bytes && e == cudaSuccess)
       e = cudaMemcpyAsync(static_cast<uint8_t*>(staging) + off, static_cast<const uint8_t*>(h) + off, bytes,
@@ -914,11 +920,15 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
   autobyte_job_stats dj{};
   AB_CUDA(c, stage_jobs_host(c, jobs, &dj));
-  AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
-  AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
+  // the grid is read once (K0): in place when page-locked; current configs (read per tile by K2) are copied
+  const void* sp_h = host_in_place(c, grid->partition_bytes);
+  const void* sc_h = host_in_place(c, grid->credit_mult);
+  if (!sp_h) AB_CUDA(c, h2d(c->sSp.ptr, grid->partition_bytes, (size_t)grid->P * 8));
+  if (!sc_h) AB_CUDA(c, h2d(c->sSc.ptr, grid->credit_mult, (size_t)grid->Q * 4));
   if (cur_idx) AB_CUDA(c, h2d(c->sCur.ptr, cur_idx, (size_t)J * 4));
   autobyte_grid dg = *grid;
-  dg.partition_bytes = reinterpret_cast<const int64_t*>(c->sSp.ptr); dg.credit_mult = c->sSc.ptr;
+  dg.partition_bytes = sp_h ? static_cast<const int64_t*>(sp_h) : reinterpret_cast<const int64_t*>(c->sSp.ptr);
+  dg.credit_mult = sc_h ? static_cast<const float*>(sc_h) : c->sSc.ptr;
   s = autobyte_argmax(c, &dj, &dg, cur_idx ? c->sCur.ptr : nullptr, c->rIdx.ptr, c->rScore.ptr,
                       cur_score ? c->rCur.ptr : nullptr);
   if (s != AB_OK) return s;
@@ -947,10 +957,16 @@ autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* s
   auto h2d = [&](void* d, const void* h, size_t bytes) { return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream); };
   autobyte_job_stats dj{};
   AB_CUDA(c, stage_jobs_host(c, samples, &dj));
-  AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
-  AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
-  AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));
-  s = autobyte_adapt(c, &dj, reinterpret_cast<const int64_t*>(c->sSp.ptr), c->sSc.ptr, c->sV.ptr, lr, steps,
+  // observed configurations and speeds are read by K4 once per step: in place when page-locked
+  const void* sp_h = host_in_place(c, sp_bytes);
+  const void* sc_h = host_in_place(c, sc_mult);
+  const void* v_h = host_in_place(c, v_obs);
+  if (!sp_h) AB_CUDA(c, h2d(c->sSp.ptr, sp_bytes, (size_t)B * 8));
+  if (!sc_h) AB_CUDA(c, h2d(c->sSc.ptr, sc_mult, (size_t)B * 4));
+  if (!v_h) AB_CUDA(c, h2d(c->sV.ptr, v_obs, (size_t)B * kNMax * 4));
+  s = autobyte_adapt(c, &dj, sp_h ? static_cast<const int64_t*>(sp_h) : reinterpret_cast<const int64_t*>(c->sSp.ptr),
+                     sc_h ? static_cast<const float*>(sc_h) : c->sSc.ptr,
+                     v_h ? static_cast<const float*>(v_h) : c->sV.ptr, lr, steps,
                      loss_before ? c->loss_tmp.ptr : nullptr);
   if (s != AB_OK) return s;
   if (loss_before)

@@ -549,8 +549,10 @@ def test_host_entry_points_read_pinned_T_in_place():
     for f in ("T", "B_d", "B_u", "l", "m", "arc"):   # (n stays pageable: it is always copied)
         setattr(jobs, f, pin(getattr(c.jobs, f)))
     cur = synth.current_configs(c.jobs.J, c.grid.C, 4)
+    grid = copy.copy(c.grid)
+    grid.S_p, grid.S_c = pin(c.grid.S_p), pin(c.grid.S_c)
     net = make(c.desc.hidden_layers, c.desc.hidden_width, W)
-    bi_h, bs_h, cs_h = net.argmax_host(jobs, c.grid, cur)
+    bi_h, bs_h, cs_h = net.argmax_host(jobs, grid, cur)
     bi_d, bs_d, cs_d = gpu_argmax(net, c.jobs, c.grid, cur)
     assert np.array_equal(bi_h, bi_d) and np.array_equal(bs_h, bs_d) and np.array_equal(cs_h, cs_d)
     batch = synth.make_adapt_batch(c.jobs, c.grid, 5)
@@ -558,6 +560,7 @@ def test_host_entry_points_read_pinned_T_in_place():
     pb.jobs = copy.copy(batch.jobs)
     for f in ("T", "B_d", "B_u", "n", "l", "m", "arc"):
         setattr(pb.jobs, f, pin(getattr(batch.jobs, f)))
+    pb.S_p, pb.S_c, pb.V_bar = pin(batch.S_p), pin(batch.S_c), pin(batch.V_bar)
     l_pinned = net.adapt_host(pb.jobs, pb.S_p, pb.S_c, pb.V_bar, 1e-3, 1)
     w_pinned = net.get_weights_blob()
     net2 = make(c.desc.hidden_layers, c.desc.hidden_width, W)

@@ -27,6 +27,8 @@ def main():
         setattr(jobs, f, pin(getattr(c.jobs, f)))
         setattr(ajobs, f, pin(getattr(ad.jobs, f)))
     cur = pin(synth.current_configs(c.jobs.J, c.grid.C, synth.BASE_SEED + 400))
+    grid = copy.copy(c.grid)
+    grid.S_p, grid.S_c = pin(c.grid.S_p), pin(c.grid.S_c)
     sp, sc, vb = pin(ad.S_p), pin(ad.S_c), pin(ad.V_bar)
     nets = {}
     for zc in ("1", "0"):
@@ -35,14 +37,14 @@ def main():
     res = {"1": [], "0": []}
     for _ in range(3):
         for net in nets.values():
-            net.argmax_host(jobs, c.grid, cur)
+            net.argmax_host(jobs, grid, cur)
             net.adapt_host(ajobs, sp, sc, vb, 1e-4, 1)
     for r in range(reps):
         for zc, net in nets.items():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(5):
-                net.argmax_host(jobs, c.grid, cur)
+                net.argmax_host(jobs, grid, cur)
                 net.adapt_host(ajobs, sp, sc, vb, 1e-4, 1)
             res[zc].append((time.perf_counter() - t0) / 5 * 1e3)
     for zc in ("1", "0"):
