@@ -260,10 +260,13 @@ autobyte_status autobyte_trigger(autobyte_ctx* ctx, int32_t J, const int32_t* be
  * (world > 1) every rank still passes the full job arrays, but only the statistics of the
  * jobs its own encoder shard reads (T, B_down, B_up, n_layers, model_type, arch_type of
  * ceil(J/world) jobs) are copied; n_workers is copied for all jobs. AUTOBYTE_CHECK=1 copies
- * everything (the range checks read every job). When T is in page-locked (pinned / registered)
- * host memory it is not staged: the encoder kernel reads its shard of T over PCIe itself, so the
- * transfer overlaps the LSTM steps (AUTOBYTE_ZERO_COPY=0 disables this); the caller must not
- * modify T until the call returns, which it does only after the results are on the host. */
+ * everything (the range checks read every job). Arrays in page-locked (pinned /
+ * registered) host memory that one kernel reads once are not staged but read in place over PCIe:
+ * T, B_down, B_up, n_layers, model_type, arch_type (by the encoder kernel, so the transfer of T
+ * overlaps the LSTM steps), the grid's partition_bytes / credit_mult (by the grid encoder) and
+ * adapt's sp_bytes / sc_mult / v_obs (by the adaptation kernel). n_workers and cur_idx are always
+ * copied. AUTOBYTE_ZERO_COPY=0 stages everything. The caller must not modify the inputs until the
+ * call returns, which it does only after the results are on the host. */
 
 /* Host-to-device bytes the staging above moves for the job statistics of J jobs with
  * l_max layers on this rank (the e2e accounting of bench.py). Returns 0 for a NULL ctx. */
