@@ -570,6 +570,13 @@ def test_host_entry_points_read_pinned_T_in_place():
     net2.close()
 
 
+def test_single_gpu_has_no_peer_exchange():
+    """Without a communicator the key exchange is skipped (K5 alone), so the peer window is off."""
+    net = make(2, 64, synth.make_weights(synth.NetDesc(2, 64)))
+    assert net.peer_exchange() is False
+    net.close()
+
+
 def test_host_staging_bytes_and_alignment_check():
     """G = 1: the host entry points stage every job's statistics (T, B_d, B_u, l, m, arc, n); a T
     pointer that is not 16-byte aligned (K1a's cp.async rows) is refused on the host, no launch."""
