@@ -815,6 +815,9 @@ extern "C" int ab_debug_stats(unsigned long long* out, int reset) {
 namespace ab {
 // Tensor map over the packed weights: a 2-D array of 128-byte rows (64 bf16), SWIZZLE_NONE (the
 // data is pre-swizzled), box = 64 bf16 x NCH/2 rows = one CTA's half of a weight stage.
+#ifndef AB_TMAP_L2_PROMOTION
+#define AB_TMAP_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -833,7 +836,7 @@ bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L
   cuuint32_t box[2] = {64, static_cast<cuuint32_t>(NCH / 2)};
   cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(wpack), dims, strides, box,
-                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, AB_TMAP_L2_PROMOTION,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace ab
