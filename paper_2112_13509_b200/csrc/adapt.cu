@@ -53,20 +53,21 @@ struct Gemm {
 };
 
 // Shared memory (dynamic, 1 KB aligned):
-//   planes  2 buffers x {A big, A small [128][32] tf32, B big, B small [128][32] tf32}, UMMA SW128
-//           K-major (row r of an 8-row 1 KB atom at 128 r bytes, 16-byte chunk j at chunk j ^ (r % 8))
+//   planes  kBufs buffers x {A big, A small [128][32] tf32, B big, B small [TN][32] tf32}, UMMA
+//           SW128 K-major (row r of an 8-row 1 KB atom at 128 r bytes, 16-byte chunk j at j ^ (r % 8))
 //   raw     kStages x {A, B} fp32 slices as copied from global in their own orientation:
 //           K-contiguous [rows][kTK + 4] or MN-contiguous [kTK][rows + 8]
-// Two tile widths: N = 64 with a 3-deep raw ring for small batches (online adaptation: more tiles
-// per phase, B = 1024 4x512 0.265 ms vs 0.30 ms with N = 128), N = 128 with a 2-deep ring for large
-// batches (offline training: half the MMAs per FLOP, 8.2 vs 7.2 M samples/s at B = 32768).
+// Two tile widths: N = 64 with 3 plane buffers and a 2-deep raw ring for small batches (online
+// adaptation: more tiles per phase), N = 128 with 2 buffers and a 2-deep ring for large batches
+// (offline training: half the MMAs per FLOP, 8.2 vs 7.2 M samples/s at B = 32768).
 template <int TN>
 struct TileCfg {
 #ifndef AB_ADAPT_STAGES64
 #define AB_ADAPT_STAGES64 2
 #endif
-  // cp.async depth of the raw slices: a slice costs ~2k cycles, mostly L2 latency over the
-  // prefetch distance (kStages - 1 slices), so N = 64 tiles take the deepest ring that fits
+  // cp.async depth of the raw slices. Depth 3 vs 4 measured the same (a slice's data lands long
+  // before it is split, K-slice trace), so N = 64 tiles spend the shared memory on a third plane
+  // buffer instead and keep a 2-deep ring (prefetch distance one slice, ~1.5k cycles)
   static constexpr int kStages = TN == 64 ? AB_ADAPT_STAGES64 : 2;
   static constexpr int kRawA = (kTM * (kTK + 4) > kTK * (kTM + 8)) ? kTM * (kTK + 4) : kTK * (kTM + 8);   // floats
   static constexpr int kRawB = (TN * (kTK + 4) > kTK * (TN + 8)) ? TN * (kTK + 4) : kTK * (TN + 8);
