@@ -12,9 +12,10 @@
 // Every output element is produced by exactly one thread with a fixed summation order, so the
 // update is deterministic and replicas on different GPUs stay bit-identical without traffic.
 // The work is ~3x a B-row forward (5 GFLOP at B=1024, 4x512): latency-bound, << 1% of a C5 step.
-// Every GEMM runs on the legacy mma.sync tensor path with 3xTF32 split operands (big*big +
-// big*small + small*big, ~fp32 accuracy), which keeps the gradient well inside the parity
-// tolerance (K4) at a fraction of the SIMT instruction count.
+// Every GEMM runs on tcgen05 (kind::tf32, accumulators in TMEM) with 3xTF32 split operands
+// (big*big + big*small + small*big, ~2^-20 relative), which keeps the gradient well inside the
+// parity tolerance (K4): a dedicated issuer warp, 8 worker warps that stage, split
+// and run the epilogue (gemm_tile).
 #include <climits>
 #include <cstdlib>
 
