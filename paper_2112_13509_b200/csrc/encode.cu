@@ -6,7 +6,9 @@
 //     thread (g, half) owns gate row g of both layers, weights in registers, for HJ jobs
 //   x_j = [h | log2 B_d | log2 B_u | n/16 | l/64 | E_m[m] | E_arc[arc]]   (Table 2)
 //   K1a takes a job range, so at G > 1 each rank encodes 1/G of the jobs and the x rows are
-//   all-gathered before K1b (autobyte.cu run_encode).
+//   all-gathered before K1b (autobyte.cu run_lstm: NCCL, or stored by K1a's epilogue into every
+//   rank's peer window with AUTOBYTE_PEER_X=1). T chunks are prefetched with cp.async (from
+//   device memory, or in place from page-locked host memory on the *_host path).
 // K1b, 32 jobs per CTA, all jobs:
 //   a_j = W1[:, :82] x_j + b1     (layer-1 projection of the job half of the concatenation)
 //   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3)

@@ -10,10 +10,11 @@
 //                                                folded into w_j / beta_j by K1, R#3)
 //   key = ord32(s) << 32 | ~c  -> atomicMax per job   (P:342 arg-max, ties to smallest c, R#11)
 //
-// Structure: persistent CTAs (one per SM), 10 warps.
+// Structure: persistent CTAs (one per SM; CTA pairs by default for H >= 256), 18 warps.
 //   warp 0      TMA producer: streams 64-wide K blocks of the packed bf16 weights into an
-//               NS-stage shared-memory ring with cp.async.bulk (L2 evict_last: every CTA
-//               re-reads the same 1.5 MB at 4x512, so they stay L2-resident).
+//               NS-stage shared-memory ring (cp.async.bulk, or 2-D tensor-map copies with
+//               .cta_group::2 for CTA pairs; L2 evict_last: every CTA re-reads the same 1.5 MB
+//               at 4x512, so they stay L2-resident).
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.
 //   warps 2..17 epilogue: 4 warps per TMEM lane quadrant, each owning a quarter of the columns.
 // Activations ping-pong between buffer X (shared memory, UMMA SW128 K-major layout, used as
