@@ -694,3 +694,40 @@ def test_device_checks_reject_out_of_range_inputs():
         with pytest.raises(AutoByteError) as ei:
             gpu_argmax(net, jobs, g)
         assert ei.value.status == AB_E_INVALID
+
+
+# ------------------------------------------------------------------------------------- degenerate shapes
+def test_degenerate_shapes_single_job_single_candidate_and_shard_errors():
+    """The method's degenerate cases (SURVEY §8(b), include/autobyte.h grid contract): one job;
+    a 1x1 grid (the arg-max is candidate 0 and its score is the oracle's single score); shards of
+    one candidate anywhere in the grid (the arg-max is that candidate, its global index, exactly);
+    a shard that is empty, reversed or out of range is AB_E_SHAPE before any launch."""
+    from paper_2112_13509_b200.autobyte import AB_E_SHAPE, AutoByteError
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H))
+    net = make(L, H, W)
+    jobs1 = synth.small_fleet(1, 11)
+    # 1x1 grid
+    g11 = synth.log_grid(1, 1)
+    s_ora = oracle.score_matrix(W, jobs1, g11)
+    check_scores(gpu_scores(net, jobs1, g11), s_ora, RTOL)
+    bi, bs, _ = gpu_argmax(net, jobs1, g11)
+    assert bi.tolist() == [0]
+    assert abs(bs[0] - s_ora[0, 0]) <= RTOL * max(abs(s_ora[0, 0]), 1e-30)
+    # one job over a ragged grid (C = 7 * 13 = 91: less than one tile)
+    g = synth.log_grid(7, 13)
+    s_ora = oracle.score_matrix(W, jobs1, g)
+    check_scores(gpu_scores(net, jobs1, g), s_ora, RTOL)
+    check_argmax(gpu_argmax(net, jobs1, g)[0], s_ora, RTOL)
+    # single-candidate shards: first, interior, last
+    jobs = synth.small_fleet(5, 12)
+    C = 7 * 13
+    for c in (0, 45, C - 1):
+        bi, bs, _ = gpu_argmax(net, jobs, g, begin=c, end=c + 1)
+        assert bi.tolist() == [c] * 5
+        s_gpu = gpu_scores(net, jobs, g, begin=c, end=c + 1)
+        np.testing.assert_array_equal(bs, s_gpu[:, 0])
+    for b, e in ((3, 3), (5, 4), (0, C + 1), (-1, 2)):
+        with pytest.raises(AutoByteError) as ei:
+            gpu_argmax(net, jobs, g, begin=b, end=e)
+        assert ei.value.status == AB_E_SHAPE
