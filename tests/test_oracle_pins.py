@@ -474,3 +474,19 @@ def test_train_scope_all_moves_the_encoder_and_descends():
     assert any(not np.array_equal(Wa[k], W[k].astype(np.float64)) for k in oracle.ENCODER_PARAMS)
     _, _, l2 = oracle.train(Wa, batch, 1, "sgd", lr=0.0, scope="all")
     assert l2[0] < la[0]
+
+
+def test_sharded_argmax_combines_to_numpy_argmax():
+    """The cross-shard reduction (SURVEY §8(b) "reduced with an NCCL allgather"): every shard's
+    (index with its global offset, score), reduced by max score then smaller index, equals
+    numpy's first-max arg-max of the whole row; a one-candidate shard returns its own index."""
+    rng = np.random.default_rng(7)
+    s = np.round(rng.normal(size=(6, 23)), 1)   # rounding makes ties likely
+    full = np.argmax(s, axis=1)
+    for bounds in ([0, 23], [0, 5, 6, 17, 23], [0, 1, 2, 3, 23]):
+        parts = [oracle.argmax_rows(s[:, b:e], c_offset=b) for b, e in zip(bounds[:-1], bounds[1:])]
+        for r in range(s.shape[0]):
+            cands = sorted(((-p[1][r], p[0][r]) for p in parts))
+            assert cands[0][1] == full[r]
+    idx, val = oracle.argmax_rows(s[:, 9:10], c_offset=9)
+    assert idx.tolist() == [9] * 6 and np.array_equal(val, s[:, 9])
