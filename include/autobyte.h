@@ -32,6 +32,11 @@
  *    the weights; adapt mutates them in stream order.
  *  - No CPU fallback: without a usable sm_100a device, autobyte_create fails with
  *    AB_E_CUDA / AB_E_UNSUPPORTED.
+ *  - Watchdogs: no kernel traps. An internal wait that exceeds its limit records a code in a
+ *    device-wide status word and the kernel runs to its end with invalid results; the next call on
+ *    any ctx of that device (or autobyte_synchronize / a *_host call, after its own kernels) returns
+ *    AB_E_CUDA (pipeline watchdog) or AB_E_NCCL (peer timeout) once, with the reason in
+ *    autobyte_last_error, and the CUDA context stays usable.
  */
 #ifndef AUTOBYTE_H_
 #define AUTOBYTE_H_
@@ -150,7 +155,13 @@ autobyte_status autobyte_synchronize(autobyte_ctx* ctx);
 /* ---- multi-GPU (candidate-axis sharding) ----------------------------- */
 /* Fill 128 bytes with a fresh NCCL unique id (rank 0 calls it and broadcasts the bytes). */
 autobyte_status autobyte_get_unique_id(void* out_128_bytes);
-/* Join a world of `world` ranks (one per GPU; collective: every rank calls it). After this,
+/* Join a world of `world` ranks (one per GPU; collective: every rank calls it). Shards of a
+ * multi-rank partition may be empty (C < world): such a rank scores nothing but joins the
+ * exchange. A peer wait that exceeds AUTOBYTE_PEER_TIMEOUT_S seconds (default 120, 0 = forever)
+ * makes that call's results invalid and the next call (or autobyte_synchronize) return AB_E_NCCL;
+ * nothing traps, the ctx stays usable. Calls may be captured into CUDA graphs (the exchange epoch
+ * is a device counter; the opt-in AUTOBYTE_PEER_X gather falls back to NCCL while capturing).
+ * After this,
  * autobyte_argmax exchanges the per-job best keys so every rank returns the global result;
  * shards must partition [0, C) across ranks. world == 1 detaches.
  * Exchange (§8(a) a-7): by default every rank maps the other ranks' key windows through CUDA
@@ -183,6 +194,25 @@ autobyte_status autobyte_score(autobyte_ctx* ctx, const autobyte_job_stats* jobs
 autobyte_status autobyte_argmax(autobyte_ctx* ctx, const autobyte_job_stats* jobs,
                                 const autobyte_grid* grid, const int32_t* cur_idx,
                                 int32_t* best_idx, float* best_score, float* cur_score);
+
+/* The per-shard half of autobyte_argmax, for callers that reduce across ranks themselves (the
+ * north star's "per-shard (score, index) bests ... reduced with an NCCL allgather"): runs the same
+ * encoder and K2 as autobyte_argmax on this rank's shard and writes the 2J arg-max keys, DEVICE
+ * keys_out[2J] u64, without any cross-rank exchange: keys_out[j] = max over this shard of
+ * ord32(s[j][c]) << 32 | (2^32 - 1 - c) (0 when no score is a number), keys_out[J + j] = the same key
+ * of the current configuration cur_idx[j] when this shard holds it, else 0 (cur_idx may be NULL).
+ * ord32 is the order-preserving map of fp32 onto u32 (NaN -> 0), so the max of the keys is the
+ * best score with ties to the smaller global c (R#11). With a communicator attached the encoder
+ * is still sharded over the ranks (collective). Errors as autobyte_argmax. */
+autobyte_status autobyte_argmax_keys(autobyte_ctx* ctx, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                                     const int32_t* cur_idx, uint64_t* keys_out);
+/* Decode G blocks of such keys (DEVICE keys[G][2J], e.g. the result of an all-gather of every
+ * rank's autobyte_argmax_keys) into best_idx / best_score / cur_score [J] (DEVICE; cur_score
+ * nullable) exactly as autobyte_argmax does after its own exchange: the per-job max over the G
+ * blocks, -1 / NaN for a job with no valid score. J, G >= 1 (else AB_E_SHAPE, no launch). The max
+ * is order-free, so any partition of the grid gives the single-rank result bit for bit. */
+autobyte_status autobyte_reduce_keys(autobyte_ctx* ctx, int32_t J, int32_t G, const uint64_t* keys,
+                                     int32_t* best_idx, float* best_score, float* cur_score);
 
 /* Per-job top-k candidates (R#19): idx[j][i] / score[j][i] (i < k, [J][k]
  * each, DEVICE) are the i-th best global candidate of job j over the grid — descending score,

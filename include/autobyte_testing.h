@@ -1,0 +1,30 @@
+/*
+ * autobyte_testing.h — test hooks of libautobyte.so (not part of the product API; the tests call
+ * them to exercise multi-rank protocols on a single GPU).
+ */
+#ifndef AUTOBYTE_TESTING_H_
+#define AUTOBYTE_TESTING_H_
+
+#include "autobyte.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* The NVLink peer-memory key exchange (exchange.cu) among G virtual ranks on the
+ * ctx's ONE device: G windows laid out like the IPC-shared ones, virtual rank r runs the same
+ * kernel (push its keys into every window, raise its epoch flag everywhere, wait for all G flags,
+ * reduce) on its own stream with one block, `calls` times in a row (epochs 1..calls, both window
+ * parities). keys: DEVICE [G][2J] u64 (rank r's autobyte_argmax_keys output); outputs DEVICE [G][J]
+ * each: what virtual rank r returns from the last call. absent_rank (0..G-1, or -1 for none) is
+ * never launched, so the others wait for it until timeout_ms and the call returns AB_E_NCCL (the
+ * status-word path of a dead peer). 1 <= G <= 8, J >= 1, calls >= 1, timeout_ms >= 1 (else
+ * AB_E_SHAPE). Synchronous. */
+autobyte_status autobyte_debug_peer_loopback(autobyte_ctx* ctx, int32_t G, int32_t J, int32_t calls,
+                                             int32_t absent_rank, int32_t timeout_ms, const uint64_t* keys,
+                                             int32_t* best_idx, float* best_score, float* cur_score);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOBYTE_TESTING_H_ */

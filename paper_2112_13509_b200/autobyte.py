@@ -74,7 +74,8 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_synchronize", "autobyte_get_unique_id", "autobyte_attach_comm", "autobyte_encode",
            "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
            "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
-           "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile"]
+           "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile",
+           "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback"]
 
 _lib = None
 
@@ -119,6 +120,9 @@ def load_library(path: Optional[str] = None):
         "autobyte_set_profiling": (I32, [P, ctypes.c_int]),
         "autobyte_get_profile": (I32, [P, P]),
         "autobyte_reset_profile": (I32, [P]),
+        "autobyte_argmax_keys": (I32, [P, P, P, P, P]),
+        "autobyte_reduce_keys": (I32, [P, I32, I32, P, P, P, P]),
+        "autobyte_debug_peer_loopback": (I32, [P, I32, I32, I32, I32, I32, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -313,6 +317,40 @@ class AutoByte:
         self._check(self.lib.autobyte_argmax(self.ctx, ctypes.byref(js), ctypes.byref(g), cur, out[0].data_ptr(),
                                              out[1].data_ptr(), out[2].data_ptr()), "argmax")
         return out
+
+    def argmax_keys(self, jobs: DeviceJobs, grid: DeviceGrid, cur_idx=None, begin: int = 0,
+                    end: Optional[int] = None):
+        """This shard's 2J arg-max keys (u64 as int64 tensor) without any cross-rank exchange."""
+        import torch
+        keys = torch.empty(2 * jobs.J, dtype=torch.int64, device=self.torch_device)
+        g, js = grid.struct(begin, end), jobs.struct()
+        cur = cur_idx.data_ptr() if cur_idx is not None else None
+        self._check(self.lib.autobyte_argmax_keys(self.ctx, ctypes.byref(js), ctypes.byref(g), cur, keys.data_ptr()),
+                    "argmax_keys")
+        return keys
+
+    def reduce_keys(self, keys, J: int):
+        """Decode [G][2J] keys (autobyte_reduce_keys) -> (best_idx, best_score, cur_score)."""
+        import torch
+        G = int(keys.numel()) // (2 * J)
+        out = (torch.empty(J, dtype=torch.int32, device=self.torch_device),
+               torch.empty(J, dtype=torch.float32, device=self.torch_device),
+               torch.empty(J, dtype=torch.float32, device=self.torch_device))
+        self._check(self.lib.autobyte_reduce_keys(self.ctx, J, G, keys.data_ptr(), out[0].data_ptr(),
+                                                  out[1].data_ptr(), out[2].data_ptr()), "reduce_keys")
+        return out
+
+    def debug_peer_loopback(self, keys, J: int, calls: int = 3, absent_rank: int = -1, timeout_ms: int = 20000):
+        """Test hook: the NVLink key-exchange kernel among G virtual ranks on this one GPU."""
+        import torch
+        G = int(keys.numel()) // (2 * J)
+        bi = torch.empty((G, J), dtype=torch.int32, device=self.torch_device)
+        bs = torch.empty((G, J), dtype=torch.float32, device=self.torch_device)
+        cs = torch.empty((G, J), dtype=torch.float32, device=self.torch_device)
+        self._check(self.lib.autobyte_debug_peer_loopback(self.ctx, G, J, int(calls), int(absent_rank),
+                                                          int(timeout_ms), keys.data_ptr(), bi.data_ptr(),
+                                                          bs.data_ptr(), cs.data_ptr()), "debug_peer_loopback")
+        return bi, bs, cs
 
     def adapt(self, samples: DeviceJobs, S_p, S_c, V_bar, lr: float, steps: int, want_loss: bool = True):
         import torch

@@ -1,10 +1,13 @@
 """Build libautobyte.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with the repo)."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -26,7 +29,7 @@ def sources():
 
 def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + \
-        [os.path.join(ROOT, "include", "autobyte.h")]
+        sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def up_to_date() -> bool:
@@ -49,16 +52,29 @@ def build(force: bool = False, verbose: bool = False, stats: bool = False, exp: 
     if not force and not stats and not exp and not name and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *(["-DAB_STATS"] if stats else []), *([f"-DAB_EXP={exp}"] if exp else []),
-           *[f"-D{d}" for d in defines], *sources(), "-o", lib_path + ".tmp",
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
+    flags = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+             "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+             "-I", os.path.join(ROOT, "include"), "-I", inc,
+             *(["-DAB_STATS"] if stats else []), *([f"-DAB_EXP={exp}"] if exp else []),
+             *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        flags.insert(1, "-Xptxas=-v")
+    # one object per translation unit, compiled in parallel, then one shared-library link
+    objdir = tempfile.mkdtemp(prefix="ab_build_")
+    objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in sources()]
+    cmds = [[*flags, "-c", src, "-o", obj] for src, obj in zip(sources(), objs)]
+    if verbose:
+        for c in cmds:
+            print(" ".join(c), file=sys.stderr)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+            if verbose or r.returncode:
+                sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", lib_path + ".tmp",
+                    "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"], check=True)
+    shutil.rmtree(objdir, ignore_errors=True)
     os.replace(lib_path + ".tmp", lib_path)
     return lib_path
 

@@ -380,9 +380,16 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
       atomicAdd(&bar[1], 1u);
     } else {
       unsigned int cur;
-      do {
+      const long long t0 = clock64();
+#pragma unroll 1
+      for (uint32_t i = 1;; ++i) {
         asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-      } while (cur == g);
+        if (cur != g) break;
+        if ((i & 1023u) == 0) {   // watchdog (ptx.cuh): record, then run to the end instead of trapping
+          if (ab_aborted()) break;
+          if (clock64() - t0 > (1ll << 36)) { ab_raise(kStatusPipeline, blockIdx.x); break; }
+        }
+      }
     }
     gen = g + 1;
     __threadfence();
@@ -712,6 +719,8 @@ cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int*
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(adapt_kernel), dim3(grid), dim3(kAdaptThreads), args,
                                      kAdaptSmemBytes, s);
 }
+
+AB_STATUS_SETTER(set_status_adapt)   // device status word pointer of this unit (ptx.cuh)
 
 }  // namespace ab
 

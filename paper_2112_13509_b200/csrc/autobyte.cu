@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/autobyte_testing.h"
 #include "internal.h"
 
 using namespace ab;
@@ -96,9 +97,10 @@ struct autobyte_ctx {
   bool peer = false;
   DevBuf<unsigned long long> win;
   DevBuf<unsigned int> win_counter;
+  DevBuf<unsigned long long> win_epoch;   // device counter of completed key exchanges (exchange.cu advances it)
   unsigned long long* peer_win[kMaxPeers] = {};
   long long win_cap2 = 0;            // slot stride in u64 (2 x job capacity)
-  unsigned long long epoch = 0;
+  unsigned long long peer_timeout_ns = 0;   // AUTOBYTE_PEER_TIMEOUT_S (default 120 s; 0 = wait forever)
   // x all-gather through the same windows (K1a epilogue stores, encode.cu): [2 parities][xcap][82] fp32
   DevBuf<unsigned int> win_xcounter;
   long long win_xcap = 0;
@@ -106,6 +108,7 @@ struct autobyte_ctx {
   unsigned long long xepoch = 0;
   bool peer_x = false;               // AUTOBYTE_PEER_X=1: x all-gather through the windows (opt-in)
   bool zero_copy = true;             // *_host: K1a reads page-locked T over PCIe (AUTOBYTE_ZERO_COPY=0 off)
+  volatile int* status = nullptr;    // device status word of this device (ptx.cuh), mapped host memory
   // staging for the *_host entry points
   DevBuf<float> sT, sBd, sBu, sSc, sV, rScore, rCur;
   DevBuf<int32_t> sN, sL, sM, sArc, sCur, rIdx;
@@ -129,6 +132,48 @@ autobyte_status fail(autobyte_ctx* c, autobyte_status s, const std::string& msg)
 }
 autobyte_status cuda_fail(autobyte_ctx* c, cudaError_t e, const char* what) {
   return fail(c, AB_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// One status word per device (ptx.cuh "device status word"): [0] = code, [1] = detail (block or peer
+// rank). Page-locked and mapped, so the host reads it without synchronising; every translation unit
+// gets the device address once per device.
+std::mutex g_status_mu;
+int* g_status_host[64] = {};
+
+cudaError_t device_status_word(int device, volatile int** out) {
+  std::lock_guard<std::mutex> lock(g_status_mu);
+  if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+  if (!g_status_host[device]) {
+    int* h = nullptr;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h), 64, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    h[0] = h[1] = 0;
+    int* d = nullptr;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0)) != cudaSuccess) return e;
+    for (auto set : {set_status_adapt, set_status_encode, set_status_encoder_bwd, set_status_exchange,
+                     set_status_score, set_status_topk})
+      if ((e = set(d)) != cudaSuccess) return e;
+    g_status_host[device] = h;
+  }
+  *out = g_status_host[device];
+  return cudaSuccess;
+}
+
+// A watchdog fired in an earlier kernel of this device: report it once (and clear it). Results of
+// the call whose kernel recorded it are invalid; the context and the CUDA context stay usable.
+autobyte_status take_status(autobyte_ctx* c) {
+  if (!c->status) return AB_OK;
+  const int code = c->status[0];
+  if (code == 0) return AB_OK;
+  const int detail = c->status[1];
+  c->status[1] = 0;
+  c->status[0] = 0;
+  if (code == kStatusPeerKeys || code == kStatusPeerX)
+    return fail(c, AB_E_NCCL, std::string(code == kStatusPeerKeys ? "peer key exchange" : "peer x all-gather") +
+                                  " timed out waiting for rank " + std::to_string(detail) +
+                                  " (AUTOBYTE_PEER_TIMEOUT_S); the results of that call are invalid");
+  return fail(c, AB_E_CUDA, "kernel pipeline watchdog fired in block " + std::to_string(detail) +
+                                " (an internal wait exceeded ~2^36 cycles); the results of that call are invalid");
 }
 
 #define AB_CUDA(ctx, expr)                                            \
@@ -171,8 +216,13 @@ autobyte_status check_grid_host(autobyte_ctx* c, const autobyte_grid* g) {
   if (g->P < 1 || g->Q < 1) return fail(c, AB_E_SHAPE, "grid P and Q must be >= 1");
   const long long C = (long long)g->P * g->Q;
   if (C > 0x7FFFFFFFLL) return fail(c, AB_E_SHAPE, "grid has more than 2^31-1 candidates");
-  if (g->shard_begin < 0 || g->shard_end > C || g->shard_begin >= g->shard_end)
-    return fail(c, AB_E_SHAPE, "shard must satisfy 0 <= begin < end <= P*Q");
+  // with a communicator attached an empty shard is a valid part of a partition of [0, C) (C < world
+  // gives some ranks nothing to score): that rank skips K0/K2 but still joins the collectives
+  const bool multi = c && c->comm && c->world > 1;
+  if (g->shard_begin < 0 || g->shard_end > C || g->shard_begin > g->shard_end ||
+      (g->shard_begin == g->shard_end && !multi))
+    return fail(c, AB_E_SHAPE, multi ? "shard must satisfy 0 <= begin <= end <= P*Q"
+                                     : "shard must satisfy 0 <= begin < end <= P*Q");
   if (!g->partition_bytes || !g->credit_mult) return fail(c, AB_E_INVALID, "grid array pointer is NULL");
   return AB_OK;
 }
@@ -234,13 +284,17 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
   ep.x_out = c->x.ptr;
   ep.j_begin = jb;
   ep.j_end = je;
-  if (shard && c->peer && c->peer_x && J <= c->win_xcap) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->stream, &cap) != cudaSuccess) { cudaGetLastError(); cap = cudaStreamCaptureStatusNone; }
+  // the fused x gather takes its epoch from the host, so a captured call would replay a stale one:
+  // while the stream is being captured the NCCL all-gather (graph-capturable) is used instead
+  if (shard && c->peer && c->peer_x && J <= c->win_xcap && cap == cudaStreamCaptureStatusNone) {
     // x all-gather fused into K1a (opt-in, AUTOBYTE_PEER_X=1): its epilogue stores the rank's rows
     // into every window and raises an epoch flag; one warp then waits for all ranks' flags before
     // K1b / K4 read the own window. Measured at G = 4 it is ~1 % slower per step than the NCCL
     // all-gather (4.89 vs 4.84 ms: the system-scope fence after the remote stores sits at the end
     // of every K1a CTA, plus one more launch), so the NCCL path stays the default.
-    const unsigned long long e = ++c->xepoch;
+    const unsigned long long e = c->xepoch + 1;   // committed only once both launches succeeded
     for (int r = 0; r < G; ++r) {
       ep.xg[r] = reinterpret_cast<float*>(c->peer_win[r] + c->win_xoff) + (size_t)(e & 1ull) * c->win_xcap * kXDim;
       ep.xflag[r] = c->peer_win[r] + kPeerXFlags;
@@ -248,7 +302,10 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
     ep.xG = G; ep.xrank = c->rank; ep.xcounter = c->win_xcounter.ptr; ep.xepoch = e;
     ep.x_out = ep.xg[c->rank];
     AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
-    AB_CUDA(c, timed(c, K_OTHER, [&] { return launch_peer_wait(c->win.ptr + kPeerXFlags, G, e, c->rank, c->stream); }));
+    AB_CUDA(c, timed(c, K_OTHER, [&] {
+              return launch_peer_wait(c->win.ptr + kPeerXFlags, G, e, c->peer_timeout_ns, c->stream);
+            }));
+    c->xepoch = e;
     ep.xG = 0;   // K1b and later launches with these params are not part of the gather
     *out = ep;
     return AB_OK;
@@ -278,6 +335,7 @@ void close_peer_window(autobyte_ctx* c) {
   }
   c->win.release();
   c->win_counter.release();
+  c->win_epoch.release();
   c->win_xcounter.release();
   c->peer = false;
   c->win_cap2 = 0;
@@ -293,10 +351,14 @@ bool setup_peer_window(autobyte_ctx* c) {
   c->win_xcap = c->win_cap2 / 2;
   c->win_xoff = kPeerFlagWords + 2 * (size_t)G * c->win_cap2;
   const size_t words = c->win_xoff + (size_t)c->win_xcap * kXDim;   // 2 parities x 82 fp32 = 82 words per job
+  // every rank starts from zeroed flags, counters and epochs (a re-attached ctx included), so the
+  // ranks' epoch sequences agree from the first exchange on
+  c->xepoch = 0;
   int ok = c->win.ensure(words) == cudaSuccess && c->win_counter.ensure(1) == cudaSuccess &&
-           c->win_xcounter.ensure(1) == cudaSuccess &&
+           c->win_xcounter.ensure(1) == cudaSuccess && c->win_epoch.ensure(1) == cudaSuccess &&
            cudaMemsetAsync(c->win.ptr, 0, words * 8, c->stream) == cudaSuccess &&
            cudaMemsetAsync(c->win_counter.ptr, 0, sizeof(unsigned int), c->stream) == cudaSuccess &&
+           cudaMemsetAsync(c->win_epoch.ptr, 0, sizeof(unsigned long long), c->stream) == cudaSuccess &&
            cudaMemsetAsync(c->win_xcounter.ptr, 0, sizeof(unsigned int), c->stream) == cudaSuccess;
   cudaIpcMemHandle_t mine{};
   if (ok) ok = cudaIpcGetMemHandle(&mine, c->win.ptr) == cudaSuccess;
@@ -393,15 +455,16 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   ep.a_out = c->jobvec.ptr; ep.what_out = c->jobvec.ptr + H; ep.beta_out = c->jobvec.ptr + 2 * H;
   ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
   AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_project(ep, c->stream); }));
+  const long long cs = grid->shard_end - grid->shard_begin;
+  if (cs == 0) return AB_OK;   // empty shard of a multi-rank partition: the keys stay 0 (K1b reset them)
   // K0: candidate encodings u_c of this shard (§8(a) a-1), 8 bytes per candidate
-  AB_CUDA(c, c->u.ensure((size_t)(grid->shard_end - grid->shard_begin)));
+  AB_CUDA(c, c->u.ensure((size_t)cs));
   AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_grid(*grid, c->u.ptr, c->stream); }));
 
   ScoreParams sp{};
   sp.J = J; sp.H = c->desc.hidden_width; sp.G = c->desc.hidden_layers - 1;
   sp.P = grid->P; sp.Q = grid->Q;
   sp.c_begin = grid->shard_begin; sp.c_end = grid->shard_end;
-  const long long cs = grid->shard_end - grid->shard_begin;
   sp.tiles_per_job = static_cast<int>((cs + kTileM - 1) / kTileM);
   sp.n_tiles = (long long)sp.tiles_per_job * J;
   sp.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); sp.S_c = grid->credit_mult;
@@ -526,12 +589,16 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   c->peer_x = px && px[0] == '1';
   const char* chk = std::getenv("AUTOBYTE_CHECK");
   c->check = chk && chk[0] == '1';
+  const char* pt = std::getenv("AUTOBYTE_PEER_TIMEOUT_S");
+  const double pts = pt ? std::atof(pt) : 120.0;
+  c->peer_timeout_ns = pts > 0 ? static_cast<unsigned long long>(pts * 1e9) : 0ull;
   auto bail = [&](cudaError_t e, const char* what) {
     std::fprintf(stderr, "autobyte_create: %s: %s\n", what, cudaGetErrorString(e));
     autobyte_destroy(c);
     return AB_E_CUDA;
   };
   cudaError_t e;
+  if ((e = device_status_word(device, &c->status)) != cudaSuccess) return bail(e, "device status word");
   if ((e = c->params.ensure(c->off.total)) != cudaSuccess) return bail(e, "alloc params");
   if ((e = c->grads.ensure(c->off.total * kAdaptSplitK)) != cudaSuccess) return bail(e, "alloc grads");
   if ((e = cudaMemsetAsync(c->grads.ptr, 0, c->off.total * kAdaptSplitK * sizeof(float), c->stream)) != cudaSuccess)
@@ -593,7 +660,7 @@ autobyte_status autobyte_synchronize(autobyte_ctx* c) {
   if (!c) return AB_E_INVALID;
   DeviceGuard guard(c->device);
   AB_CUDA(c, cudaStreamSynchronize(c->stream));
-  return AB_OK;
+  return take_status(c);
 }
 
 autobyte_status autobyte_get_unique_id(void* out) {
@@ -634,6 +701,7 @@ int32_t autobyte_peer_exchange(const autobyte_ctx* c) { return c && c->peer ? 1 
 
 autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs, float* x_out) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
   if (s != AB_OK) return s;
   if (!x_out) return fail(c, AB_E_INVALID, "x_out is NULL");
@@ -649,10 +717,11 @@ autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs,
 autobyte_status autobyte_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                float* scores) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
   if (s != AB_OK) return s;
   if ((s = check_grid_host(c, grid)) != AB_OK) return s;
-  if (!scores) return fail(c, AB_E_INVALID, "scores is NULL");
+  if (!scores && grid->shard_end > grid->shard_begin) return fail(c, AB_E_INVALID, "scores is NULL");
   DeviceGuard guard(c->device);
   if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
   return run_encode_and_score(c, jobs, grid, nullptr, scores);
@@ -661,6 +730,7 @@ autobyte_status autobyte_score(autobyte_ctx* c, const autobyte_job_stats* jobs, 
 autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                 const int32_t* cur_idx, int32_t* best_idx, float* best_score, float* cur_score) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
   if (s != AB_OK) return s;
   if ((s = check_grid_host(c, grid)) != AB_OK) return s;
@@ -679,7 +749,8 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
     for (int r = 0; r < c->world; ++r) xp.win[r] = c->peer_win[r];
     xp.keys = c->keys.ptr; xp.counter = c->win_counter.ptr;
     xp.best_idx = best_idx; xp.best_score = best_score; xp.cur_score = cur_score;
-    xp.epoch = ++c->epoch; xp.cap2 = c->win_cap2; xp.J = J; xp.G = c->world; xp.rank = c->rank;
+    xp.epoch = c->win_epoch.ptr; xp.timeout_ns = c->peer_timeout_ns;
+    xp.cap2 = c->win_cap2; xp.J = J; xp.G = c->world; xp.rank = c->rank;
     // (profiled as K5, whose work it includes: finalize_ms then also holds the wait for the
     // slowest rank, exchange_ms only the NCCL x all-gathers)
     AB_CUDA(c, timed(c, K_FINALIZE, [&] { return launch_peer_exchange(xp, c->num_sms, c->stream); }));
@@ -705,6 +776,81 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
             return launch_finalize(J, G, 2LL * J, kin, kin + J, best_idx, best_score, cur_score, c->stream);
           }));
   return AB_OK;
+}
+
+autobyte_status autobyte_argmax_keys(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
+                                     const int32_t* cur_idx, uint64_t* keys_out) {
+  if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (!keys_out) return fail(c, AB_E_INVALID, "keys_out is NULL");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
+  if ((s = run_encode_and_score(c, jobs, grid, cur_idx, nullptr)) != AB_OK) return s;
+  AB_CUDA(c, cudaMemcpyAsync(keys_out, c->keys.ptr, (size_t)2 * jobs->J * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  return AB_OK;
+}
+
+autobyte_status autobyte_reduce_keys(autobyte_ctx* c, int32_t J, int32_t G, const uint64_t* keys, int32_t* best_idx,
+                                     float* best_score, float* cur_score) {
+  if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
+  if (J < 1 || G < 1) return fail(c, AB_E_SHAPE, "J and G must be >= 1");
+  if (!keys || !best_idx || !best_score) return fail(c, AB_E_INVALID, "keys / best_idx / best_score is NULL");
+  DeviceGuard guard(c->device);
+  const unsigned long long* k = reinterpret_cast<const unsigned long long*>(keys);
+  AB_CUDA(c, timed(c, K_FINALIZE, [&] {
+            return launch_finalize(J, G, 2LL * J, k, k + J, best_idx, best_score, cur_score, c->stream);
+          }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_debug_peer_loopback(autobyte_ctx* c, int32_t G, int32_t J, int32_t calls, int32_t absent_rank,
+                                             int32_t timeout_ms, const uint64_t* keys, int32_t* best_idx,
+                                             float* best_score, float* cur_score) {
+  if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
+  if (G < 1 || G > kMaxPeers || J < 1 || calls < 1 || timeout_ms < 1)
+    return fail(c, AB_E_SHAPE, "need 1 <= G <= 8, J >= 1, calls >= 1, timeout_ms >= 1");
+  if (!keys || !best_idx || !best_score || !cur_score) return fail(c, AB_E_INVALID, "NULL pointer");
+  DeviceGuard guard(c->device);
+  AB_CUDA(c, cudaStreamSynchronize(c->stream));
+  // G windows on this device, laid out exactly as setup_peer_window lays out the IPC-shared ones
+  const long long cap2 = 2LL * J;
+  const size_t words = kPeerFlagWords + 2 * (size_t)G * cap2;
+  DevBuf<unsigned long long> win, epochs;
+  DevBuf<unsigned int> counters;
+  AB_CUDA(c, win.ensure(words * G));
+  AB_CUDA(c, epochs.ensure(G));
+  AB_CUDA(c, counters.ensure(G));
+  AB_CUDA(c, cudaMemset(win.ptr, 0, words * G * 8));
+  AB_CUDA(c, cudaMemset(epochs.ptr, 0, G * 8));
+  AB_CUDA(c, cudaMemset(counters.ptr, 0, G * 4));
+  std::vector<cudaStream_t> st(G, nullptr);
+  for (auto& x : st) AB_CUDA(c, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  cudaError_t e = cudaSuccess;
+  for (int call = 0; call < calls && e == cudaSuccess; ++call) {
+    for (int r = 0; r < G && e == cudaSuccess; ++r) {   // virtual rank r on its own stream
+      if (r == absent_rank) continue;
+      PeerExchangeParams xp{};
+      for (int q = 0; q < G; ++q) xp.win[q] = win.ptr + (size_t)q * words;
+      xp.keys = reinterpret_cast<const unsigned long long*>(keys) + (size_t)r * cap2;
+      xp.counter = counters.ptr + r;
+      xp.best_idx = best_idx + (size_t)r * J; xp.best_score = best_score + (size_t)r * J;
+      xp.cur_score = cur_score + (size_t)r * J;
+      xp.epoch = epochs.ptr + r; xp.timeout_ns = 1000000ull * static_cast<unsigned long long>(timeout_ms);
+      xp.cap2 = cap2; xp.J = J; xp.G = G; xp.rank = r;
+      e = launch_peer_exchange(xp, c->num_sms, st[r], false);
+    }
+    for (auto& x : st)
+      if (e == cudaSuccess) e = cudaStreamSynchronize(x);
+  }
+  for (auto& x : st) cudaStreamDestroy(x);
+  if (e != cudaSuccess) return cuda_fail(c, e, "peer loopback");
+  return take_status(c);
 }
 
 }  // extern "C"
@@ -752,6 +898,7 @@ extern "C" {
 autobyte_status autobyte_topk(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid, int32_t k,
                               int32_t* idx, float* score) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
   if (s != AB_OK) return s;
   if ((s = check_grid_host(c, grid)) != AB_OK) return s;
@@ -762,13 +909,16 @@ autobyte_status autobyte_topk(autobyte_ctx* c, const autobyte_job_stats* jobs, c
   const int J = jobs->J;
   const long long cs = grid->shard_end - grid->shard_begin;
   const int G = (c->comm && c->world > 1) ? c->world : 1;
-  AB_CUDA(c, c->topk_scores.ensure((size_t)J * cs));
+  AB_CUDA(c, c->topk_scores.ensure(cs > 0 ? (size_t)J * cs : 1));
   AB_CUDA(c, c->topk_keys.ensure((size_t)G * J * k));
   if ((s = run_encode_and_score(c, jobs, grid, nullptr, c->topk_scores.ptr)) != AB_OK) return s;
   unsigned long long* mine = c->topk_keys.ptr + (G > 1 ? (size_t)c->rank * J * k : 0);
-  AB_CUDA(c, timed(c, K_FINALIZE, [&] {
-            return launch_topk(J, cs, c->topk_scores.ptr, grid->shard_begin, k, mine, c->stream);
-          }));
+  if (cs == 0)   // empty shard of a multi-rank partition: an all-empty list (key 0 = no candidate)
+    AB_CUDA(c, cudaMemsetAsync(mine, 0, (size_t)J * k * sizeof(unsigned long long), c->stream));
+  else
+    AB_CUDA(c, timed(c, K_FINALIZE, [&] {
+              return launch_topk(J, cs, c->topk_scores.ptr, grid->shard_begin, k, mine, c->stream);
+            }));
   if (G > 1) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
@@ -787,6 +937,7 @@ autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* sample
                                const float* sc_mult, const float* v_obs, float lr, int32_t steps,
                                float* loss_before) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
   if (s != AB_OK) return s;
   if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "adapt input pointer is NULL");
@@ -803,6 +954,7 @@ autobyte_status autobyte_train(autobyte_ctx* c, const autobyte_job_stats* sample
                                const float* sc_mult, const float* v_obs, const autobyte_optimizer* opt,
                                int32_t steps, float* losses) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
   if (s != AB_OK) return s;
   if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "train input pointer is NULL");
@@ -885,6 +1037,7 @@ autobyte_status autobyte_trigger(autobyte_ctx* c, int32_t J, const int32_t* best
                                  const int32_t* cur_idx, const float* cur_score, const float* v_observed,
                                  float gain, float drift, int32_t* action) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   if (J < 1) return fail(c, AB_E_SHAPE, "J must be >= 1");
   if (!best_idx || !best_score || !cur_idx || !cur_score || !action)
     return fail(c, AB_E_INVALID, "trigger array pointer is NULL");
@@ -905,6 +1058,7 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
                                      const int32_t* cur_idx, int32_t* best_idx, float* best_score,
                                      float* cur_score) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
   if (s != AB_OK) return s;
   if ((s = check_grid_host(c, grid)) != AB_OK) return s;
@@ -937,13 +1091,14 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
   AB_CUDA(c, d2h(best_score, c->rScore.ptr, (size_t)J * 4));
   if (cur_score) AB_CUDA(c, d2h(cur_score, c->rCur.ptr, (size_t)J * 4));
   AB_CUDA(c, cudaStreamSynchronize(c->stream));
-  return AB_OK;
+  return take_status(c);
 }
 
 autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                     const float* sc_mult, const float* v_obs, float lr, int32_t steps,
                                     float* loss_before) {
   if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
   if (s != AB_OK) return s;
   if (!sp_bytes || !sc_mult || !v_obs) return fail(c, AB_E_INVALID, "adapt input pointer is NULL");
@@ -972,7 +1127,7 @@ autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* s
   if (loss_before)
     AB_CUDA(c, cudaMemcpyAsync(loss_before, c->loss_tmp.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
   AB_CUDA(c, cudaStreamSynchronize(c->stream));
-  return AB_OK;
+  return take_status(c);
 }
 
 autobyte_status autobyte_get_weights(autobyte_ctx* c, void* host_blob, size_t bytes) {
@@ -992,7 +1147,7 @@ autobyte_status autobyte_get_weights(autobyte_ctx* c, void* host_blob, size_t by
   AB_CUDA(c, cudaMemcpyAsync(b + kBlobHeader, c->params.ptr, c->off.total * sizeof(float), cudaMemcpyDeviceToHost,
                              c->stream));
   AB_CUDA(c, cudaStreamSynchronize(c->stream));
-  return AB_OK;
+  return take_status(c);
 }
 
 autobyte_status autobyte_set_profiling(autobyte_ctx* c, int enable) {

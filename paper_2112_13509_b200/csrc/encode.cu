@@ -564,6 +564,8 @@ cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s)
   return cudaGetLastError();
 }
 
+AB_STATUS_SETTER(set_status_encode)   // device status word pointer of this unit (ptx.cuh)
+
 }  // namespace ab
 
 #ifdef AB_STATS

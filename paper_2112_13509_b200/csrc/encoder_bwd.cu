@@ -351,4 +351,6 @@ cudaError_t launch_encoder_update(const EncodeParams& p, const float* dX, int ld
   return cudaGetLastError();
 }
 
+AB_STATUS_SETTER(set_status_encoder_bwd)   // device status word pointer of this unit (ptx.cuh)
+
 }  // namespace ab

@@ -32,6 +32,13 @@ struct ParamOffsets {
 };
 ParamOffsets make_offsets(const autobyte_net_desc& d);
 
+// Device status word codes (ptx.cuh): what a watchdog records instead of trapping.
+enum : int {
+  kStatusPipeline = 1,   // an mbarrier / grid-barrier wait inside one kernel exceeded ~2^36 cycles
+  kStatusPeerKeys = 2,   // the NVLink key exchange waited longer than AUTOBYTE_PEER_TIMEOUT_S for a peer
+  kStatusPeerX = 3,      // the NVLink x all-gather waited longer than AUTOBYTE_PEER_TIMEOUT_S for a peer
+};
+
 // ---------------------------------------------------------------- kernel parameter blocks
 struct EncodeParams {
   int J, l_max, H;
@@ -123,14 +130,15 @@ struct PeerExchangeParams {
   const unsigned long long* keys;       // [2J] this rank's keys (K2)
   unsigned int* counter;                // per-rank block counter (zero between calls)
   int32_t* best_idx; float* best_score; float* cur_score;
-  unsigned long long epoch;             // >= 1, grows by one per call
+  unsigned long long* epoch;            // device counter: last completed epoch (the kernel advances it)
+  unsigned long long timeout_ns;        // peer wait limit (0 = wait forever)
   long long cap2;                       // slot stride (u64), >= 2J
   int J, G, rank;
 };
-cudaError_t launch_peer_exchange(const PeerExchangeParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_peer_exchange(const PeerExchangeParams& p, int num_sms, cudaStream_t s, bool cooperative = true);
 // one warp waits until flags[r] >= epoch for r < G (stream order then holds the consumers back)
-cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch, int rank,
-                             cudaStream_t s);
+cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch,
+                             unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica
@@ -155,5 +163,12 @@ cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
 bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L);
+// device status word (ptx.cuh): each translation unit's copy of the pointer, set per device
+cudaError_t set_status_adapt(int* p);
+cudaError_t set_status_encode(int* p);
+cudaError_t set_status_encoder_bwd(int* p);
+cudaError_t set_status_exchange(int* p);
+cudaError_t set_status_score(int* p);
+cudaError_t set_status_topk(int* p);
 
 }  // namespace ab

@@ -11,6 +11,32 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---------------------------------------------------------------- device status word (no traps)
+// Watchdogs never __trap(): a wait that exceeds its limit records a code in the device-wide status
+// word and returns as if the wait had completed, and every other wait returns at once while the word
+// is set, so the kernel runs to its end (its results invalid) and the CUDA context stays usable. The
+// word lives in mapped page-locked host memory (one per device, owned by autobyte.cu); each
+// translation unit holds its own copy of the pointer, set at autobyte_create through the
+// AB_STATUS_SETTER function that unit defines. The host maps the code to AB_E_CUDA / AB_E_NCCL
+// (autobyte_last_error says which wait) and clears it.
+static __device__ int* g_ab_status = nullptr;
+// (codes: kStatus* in internal.h, which every unit includes first)
+__device__ __forceinline__ bool ab_aborted() {
+  const int* s = g_ab_status;
+  return s != nullptr && *reinterpret_cast<const volatile int*>(s) != 0;
+}
+static __device__ __noinline__ void ab_raise(int code, int detail) {
+  int* s = g_ab_status;
+  if (s == nullptr) return;
+  if (*reinterpret_cast<volatile int*>(s) == 0) {
+    reinterpret_cast<volatile int*>(s)[1] = detail;
+    reinterpret_cast<volatile int*>(s)[0] = code;
+  }
+  __threadfence_system();
+}
+#define AB_STATUS_SETTER(fn) \
+  cudaError_t fn(int* p) { return cudaMemcpyToSymbol(g_ab_status, &p, sizeof(p)); }
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -38,11 +64,15 @@ __device__ __forceinline__ uint32_t mbar_try(uint32_t addr, uint32_t parity) {
 }
 static __device__ __noinline__ void mbar_wait_slow(uint32_t addr, uint32_t parity) {
   const long long t0 = clock64();
-  while (!mbar_try(addr, parity)) {
+#pragma unroll 1
+  for (uint32_t i = 1; !mbar_try(addr, parity); ++i) {
+    if ((i & 1023u) != 0) continue;
+    if (ab_aborted()) return;
     if (clock64() - t0 > (1ll << 36)) {
       printf("autobyte: mbarrier watchdog (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x, addr,
              parity);
-      __trap();
+      ab_raise(kStatusPipeline, blockIdx.x);
+      return;
     }
   }
 }
@@ -206,10 +236,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_cluster(addr, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_cluster(addr, parity)) {
+#pragma unroll 1
+  for (uint32_t i = 1; !mbar_try_cluster(addr, parity); ++i) {
+    if ((i & 1023u) != 0) continue;
+    if (ab_aborted()) return;
     if (clock64() - t0 > (1ll << 36)) {
       printf("autobyte: cluster mbarrier watchdog (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-      __trap();
+      ab_raise(kStatusPipeline, blockIdx.x);
+      return;
     }
   }
 }

@@ -645,11 +645,14 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 template <int H, int CG, int P3>
 static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
   using C = ScoreCfg<H, CG, P3>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<H, CG, P3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  static unsigned long long attr_done = 0;   // per device: the > 48 KB opt-in is a per-device attribute
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!(attr_done >> (dev & 63) & 1ull)) {
+    e = cudaFuncSetAttribute(score_kernel<H, CG, P3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    attr_done |= 1ull << (dev & 63);
   }
   const long long units = CG == 2 ? (p.n_tiles + 1) / 2 : p.n_tiles;
   const long long max_units = num_sms / CG;
@@ -790,6 +793,8 @@ cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int
   pack_kernel<<<blocks, 256, 0, s>>>(params, off, H, L, planes, wpack);
   return cudaGetLastError();
 }
+
+AB_STATUS_SETTER(set_status_score)   // device status word pointer of this unit (ptx.cuh)
 
 }  // namespace ab
 

@@ -176,4 +176,6 @@ cudaError_t launch_topk_merge(int J, int G, int k, const unsigned long long* lis
   return cudaGetLastError();
 }
 
+AB_STATUS_SETTER(set_status_topk)   // device status word pointer of this unit (ptx.cuh)
+
 }  // namespace ab

@@ -73,3 +73,19 @@ def check_argmax(best_gpu, s_ora, rtol, c_offset=0):
             assert b == int(np.argmax(row)), f"job {j}: best {b} != oracle {int(np.argmax(row))}"
         assert row[b] >= top1 - rtol * scale, f"job {j}: regret {(top1 - row[b]) / scale:.3e}"
     return non_tied
+
+
+def lstm_golden_weights(L: int = 1, H: int = 8):
+    """Weights of tests/golden/lstm_closed_form.json (every value exact in fp32): the embedding
+    passes t'[worker 0] to unit 0's g gate of LSTM layer 1 (x 1/4, recurrent x 2), layer 2 takes
+    h1[0] into its unit-0 g gate; forget / output gate biases +1 / -1; everything else zero."""
+    desc = synth.NetDesc(L, H)
+    W = {k: np.zeros(s, np.float32) for k, s in synth.param_shapes(desc).items()}
+    W["W_e"][0, 0] = 1.0
+    for name in ("lstm1_b", "lstm2_b"):
+        W[name][32:64] = 1.0
+        W[name][96:128] = -1.0
+    W["lstm1_Wx"][64, 0] = 0.25
+    W["lstm1_Wh"][64, 0] = 2.0
+    W["lstm2_Wx"][64, 0] = 1.0
+    return W

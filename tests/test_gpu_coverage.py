@@ -1,0 +1,319 @@
+"""GPU parity on the configurations and corners the repo quotes (round-2 coverage): the encoder's
+padding contract, single-layer and 200-layer jobs and the closed-form LSTM golden; adaptation at the
+bench's own configuration (B = 1024, 4x512) and training on the large-batch tile path (B >= 4096);
+C3 element by element; the C5 arg-max against the oracle's maximum over all 1,048,576 candidates;
+and the cross-shard key reduction (K5 over G key blocks, and the NVLink exchange kernel among
+virtual ranks) on ONE GPU, bit for bit against the single-shard result. Tolerances as
+DESIGN.md §6."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.helpers import check_argmax, check_scores, load_golden, lstm_golden_weights
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_13509_b200 import autobyte
+    autobyte.load_library()
+
+
+def make(L, H, W):
+    from paper_2112_13509_b200.autobyte import AutoByte
+    return AutoByte(L, H, W, device=0)
+
+
+def dev(jobs, grid=None):
+    from paper_2112_13509_b200.autobyte import DeviceGrid, DeviceJobs
+    dj = DeviceJobs.from_host(jobs)
+    return (dj, DeviceGrid.from_host(grid)) if grid is not None else dj
+
+
+def gpu_scores(net, jobs, grid, begin=0, end=None):
+    dj, dg = dev(jobs, grid)
+    s = net.score(dj, dg, begin, end)
+    torch.cuda.synchronize()
+    return s.cpu().numpy()
+
+
+def gpu_argmax(net, jobs, grid, cur=None, begin=0, end=None):
+    dj, dg = dev(jobs, grid)
+    cur_t = torch.as_tensor(cur, dtype=torch.int32, device="cuda") if cur is not None else None
+    bi, bs, cs = net.argmax(dj, dg, cur_t, begin, end)
+    torch.cuda.synchronize()
+    return bi.cpu().numpy(), bs.cpu().numpy(), cs.cpu().numpy()
+
+
+def dev_batch(batch):
+    to = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda")
+    return (dev(batch.jobs), to(batch.S_p, torch.int64), to(batch.S_c, torch.float32),
+            to(batch.V_bar, torch.float32))
+
+
+def check_update(W0, W_ora, W_gpu, tol):
+    for k in oracle.HEAD_PARAMS(W_ora):
+        d_ora = W_ora[k] - W0[k].astype(np.float64)
+        d_gpu = W_gpu[k].astype(np.float64) - W0[k].astype(np.float64)
+        rel = np.linalg.norm(d_gpu - d_ora) / max(np.linalg.norm(d_ora), 1e-30)
+        assert rel <= tol, (k, rel)
+
+
+# ------------------------------------------------------------------------------------- K1 encoder
+@pytest.mark.parametrize("l", [1, 2])
+def test_encoder_lstm_closed_form_golden(l):
+    """tests/golden/lstm_closed_form.json on the GPU: T reaches x through t' = log2(1 + T/1 ms),
+    the embedding and both LSTM layers (fp32 device math vs the float64 closed form)."""
+    g = load_golden("lstm_closed_form.json")
+    W = lstm_golden_weights(1, 64)
+    T = np.zeros((1, 2, 16), np.float32)
+    T[0, :, 0] = g["job"]["T_ms"]
+    T[0, :, 1:] = np.nan                 # padded workers: ignored (include/autobyte.h)
+    one = lambda v: np.array([v], np.int32)
+    Bd = np.ones((1, 16), np.float32)
+    jobs = synth.Jobs(T, Bd, Bd.copy(), one(1), one(l), one(0), one(0))
+    x = make(1, 64, W).encode(dev(jobs)).cpu().numpy()
+    assert abs(x[0, 0] - g["expected_x0"][f"l{l}"]) <= 1e-6
+    assert np.all(x[0, 1:32] == 0.0)
+
+
+def test_encoder_ignores_garbage_and_nan_in_padding():
+    """include/autobyte.h: entries of layers >= n_layers[j] or workers >= n_workers[j] (T, B_d, B_u)
+    are ignored. NaN / huge / negative padding gives bit-identical x, scores and arg-max."""
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H), seed=21)
+    jobs = synth.small_fleet(40, 23)
+    dirty = jobs.subset(np.arange(40))
+    rng = np.random.default_rng(3)
+    for j in range(40):
+        n, l = dirty.n[j], dirty.l[j]
+        fill = [np.nan, 1e30, -5.0, np.inf][j % 4]
+        dirty.T[j, :, n:] = fill
+        dirty.T[j, l:, :] = rng.choice([np.nan, -1.0, 7e20])
+        dirty.B_d[j, n:] = fill
+        dirty.B_u[j, n:] = -3.0 if j % 2 else np.nan
+    net = make(L, H, W)
+    x0 = net.encode(dev(jobs)).cpu().numpy()
+    x1 = net.encode(dev(dirty)).cpu().numpy()
+    assert np.array_equal(x0, x1)
+    grid = synth.log_grid(16, 16)
+    assert np.array_equal(gpu_scores(net, jobs, grid), gpu_scores(net, dirty, grid))
+    a, b = gpu_argmax(net, jobs, grid), gpu_argmax(net, dirty, grid)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    np.testing.assert_allclose(x0, oracle.encode_jobs(W, jobs), rtol=1e-4, atol=2e-5)
+
+
+def test_encoder_single_layer_jobs():
+    """l_j = 1 for every job (one LSTM step from h0 = c0 = 0): x and scores vs the oracle."""
+    L, H = 2, 128
+    W = synth.make_weights(synth.NetDesc(L, H), seed=31)
+    jobs = synth.small_fleet(33, 31, l_max=4)
+    jobs.l[:] = 1
+    jobs.T[:, 1:, :] = 0.0
+    net = make(L, H, W)
+    x = net.encode(dev(jobs)).cpu().numpy()
+    np.testing.assert_allclose(x, oracle.encode_jobs(W, jobs), rtol=1e-4, atol=2e-5)
+    grid = synth.log_grid(8, 9)
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    check_scores(gpu_scores(net, jobs, grid), s_ora, RTOL)
+    check_argmax(gpu_argmax(net, jobs, grid)[0], s_ora, RTOL)
+
+
+@pytest.mark.parametrize("J", [3, 300])
+def test_encoder_long_sequences_l_max_200(J):
+    """l_max = 200 with job lengths 1..200 (K1a stages T 8-16 layers at a time through a two-chunk
+    ring, so 200 layers cross many chunk boundaries): x vs the oracle and bit-invariance of a job's
+    x under regrouping (J = 3 vs the same jobs inside J = 300)."""
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H), seed=41)
+    rng = np.random.default_rng(J)
+    base = synth.small_fleet(J, 41 + J)
+    T = np.zeros((J, 200, 16), np.float32)
+    l = rng.integers(1, 201, size=J).astype(np.int32)
+    l[: min(J, 3)] = [200, 1, 137][: min(J, 3)]
+    for j in range(J):
+        n = base.n[j]
+        T[j, : l[j], :n] = rng.uniform(0.05, 40.0, size=(l[j], n)).astype(np.float32)
+    jobs = synth.Jobs(T, base.B_d, base.B_u, base.n, l, base.m, base.arc)
+    net = make(L, H, W)
+    x = net.encode(dev(jobs)).cpu().numpy()
+    idx = np.unique(np.concatenate([[0, 1, 2][: min(J, 3)], rng.integers(0, J, size=min(J, 12))]))
+    np.testing.assert_allclose(x[idx], oracle.encode_jobs(W, jobs, idx), rtol=1e-4, atol=2e-5)
+    if J > 3:
+        x3 = net.encode(dev(jobs.subset(np.arange(3)))).cpu().numpy()
+        assert np.array_equal(x3, x[:3])
+
+
+# ------------------------------------------------------------------------------------- K4 at the bench config
+def test_adapt_at_bench_configuration_b1024_4x512():
+    """One SGD step on C4's adaptation minibatch (B = 1024 samples, 4x512) — the K4 launch bench.py
+    times — against the oracle: loss_before within 1e-4, per-tensor update within 1e-3."""
+    c = synth.config("C4")
+    W = synth.make_weights(c.desc)
+    batch = c.adapt
+    lr = 1e-3
+    W_ora, loss_ora = oracle.adapt(W, batch, lr=lr, steps=1)
+    net = make(4, 512, W)
+    loss = net.adapt_host(batch.jobs, batch.S_p, batch.S_c, batch.V_bar, lr=lr, steps=1)
+    assert abs(loss - loss_ora) <= 1e-4 * loss_ora, (loss, loss_ora)
+    check_update(W, W_ora, net.get_weights(), 1e-3)
+
+
+@pytest.mark.parametrize("L,H,B", [(4, 512, 4096), (3, 256, 8192)])
+def test_train_large_batch_tile_path(L, H, B):
+    """autobyte_train at B >= 4096, where K4 switches to 128x128 tiles (adapt.cu), Adam over two
+    calls (moments carried) vs oracle.train: per-step losses and per-tensor updates."""
+    W = synth.make_weights(synth.NetDesc(L, H), seed=7 * L + B)
+    # short-sequence models keep the oracle's per-job LSTM loop fast at these batch sizes
+    jobs = synth.make_jobs(B, 90 + L, ["alexnet", "vgg16", "transformer"], [0, 1], list(range(1, 17)), l_max=16)
+    batch = synth.make_adapt_batch(jobs, synth.log_grid(64, 64), 17)
+    kw = dict(lr=3e-4, beta1=0.9, beta2=0.99, eps=1e-6)
+    W1, st, l1 = oracle.train(W, batch, 1, "adam", **kw)
+    W2, _, l2 = oracle.train(W1, batch, 1, "adam", state=st, **kw)
+    net = make(L, H, W)
+    db = dev_batch(batch)
+    g1 = net.train(*db, 1, "adam", **kw).cpu().numpy()
+    g2 = net.train(*db, 1, "adam", **kw).cpu().numpy()
+    got, want = np.concatenate([g1, g2]), np.array(l1 + l2)
+    assert abs(got[0] - want[0]) <= 1e-4 * want[0]
+    np.testing.assert_allclose(got, want, rtol=1e-3)
+    check_update(W, W2, net.get_weights(), 2e-3)
+    # SGD on the same tile path: one step == oracle.adapt
+    W_s, _ = oracle.adapt(W, batch, lr=1e-2, steps=1)
+    net2 = make(L, H, W)
+    net2.adapt(*db, 1e-2, 1)
+    torch.cuda.synchronize()
+    check_update(W, W_s, net2.get_weights(), 1e-3)
+
+
+# ------------------------------------------------------------------------------------- C3 in full
+def test_c3_full_score_matrix_and_every_job_argmax():
+    """C3 (256 jobs x 4096 candidates, 3x256) element by element against the oracle (per-job 2e-2)
+    and the arg-max rules on all 256 jobs, plus best_score == the job's max GPU score."""
+    c = synth.config("C3")
+    W = synth.make_weights(c.desc)
+    net = make(3, 256, W)
+    s = gpu_scores(net, c.jobs, c.grid)
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid)
+    err = check_scores(s, s_ora, RTOL)
+    bi, bs, _ = gpu_argmax(net, c.jobs, c.grid)
+    nt = check_argmax(bi, s_ora, RTOL)
+    assert np.array_equal(bs, s.max(axis=1))
+    assert np.array_equal(bs, s[np.arange(256), bi])
+    print(f"C3 full: max err {err.max():.2e}, non-tied {nt}/256")
+
+
+# ------------------------------------------------------------------------------------- C5 regret
+@pytest.mark.slow
+def test_c5_argmax_regret_over_the_full_grid():
+    """C5 (1024 jobs x 1,048,576 candidates, 4x512): for 2 jobs the oracle scores ALL 1M candidates;
+    the GPU's arg-max must satisfy the arg-max rules against the global maximum, and its
+    best_score must be within tolerance of the oracle's score of the returned candidate."""
+    c = synth.config("C5")
+    W = synth.make_weights(c.desc)
+    net = make(4, 512, W)
+    bi, bs, _ = gpu_argmax(net, c.jobs, c.grid)
+    u = oracle.encode_grid(c.grid.S_p, c.grid.S_c)
+    for j in (0, 613):
+        x = oracle.encode_jobs(W, c.jobs, [j])[0]
+        s = np.concatenate([oracle.score_pairs(W, x, c.jobs.n[j], u[a:a + 65536])
+                            for a in range(0, u.shape[0], 65536)])
+        check_argmax(bi[j:j + 1], s[None], RTOL)
+        assert abs(bs[j] - s[bi[j]]) <= RTOL * np.max(np.abs(s))
+
+
+# ------------------------------------------------------------------------------------- G > 1 reduction on 1 GPU
+def _shard_keys(net, jobs, grid, G, cur):
+    """Each of G contiguous shards' keys (autobyte_argmax_keys), stacked [G][2J]; an empty shard
+    (C < G) contributes zero keys, as an empty rank does."""
+    from paper_2112_13509_b200.autobyte import DeviceGrid, shard_bounds
+    dj, dg = dev(jobs), DeviceGrid.from_host(grid)
+    cur_t = torch.as_tensor(cur, dtype=torch.int32, device="cuda")
+    blocks = []
+    for r in range(G):
+        b, e = shard_bounds(grid.C, r, G)
+        if e > b:
+            blocks.append(net.argmax_keys(dj, dg, cur_t, b, e))
+        else:
+            blocks.append(torch.zeros(2 * jobs.J, dtype=torch.int64, device="cuda"))
+    return torch.cat(blocks)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_sharded_keys_reduce_to_the_single_gpu_result(G):
+    """a-7 on one GPU: K2 on G candidate shards into G key blocks, reduced by K5 (the NCCL
+    all-gather path's reduction) == the G = 1 arg-max bit for bit, for best index, best score and
+    current score; the arg-max rules hold against the oracle."""
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H), seed=G)
+    jobs = synth.small_fleet(37, 50 + G)
+    grid = synth.log_grid(16, 13)
+    net = make(L, H, W)
+    cur = synth.current_configs(jobs.J, grid.C, G)
+    ref = gpu_argmax(net, jobs, grid, cur)
+    keys = _shard_keys(net, jobs, grid, G, cur)
+    bi, bs, cs = (t.cpu().numpy() for t in net.reduce_keys(keys, jobs.J))
+    assert np.array_equal(bi, ref[0]) and np.array_equal(bs, ref[1]) and np.array_equal(cs, ref[2])
+    check_argmax(bi, oracle.score_matrix(W, jobs, grid), RTOL)
+
+
+def test_sharded_keys_with_empty_and_single_candidate_shards():
+    """C = 3 candidates over G = 8 shards: five shards are empty, three hold one candidate each."""
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H), seed=9)
+    jobs = synth.small_fleet(5, 9)
+    grid = synth.log_grid(1, 3)
+    net = make(L, H, W)
+    cur = synth.current_configs(jobs.J, grid.C, 1)
+    ref = gpu_argmax(net, jobs, grid, cur)
+    keys = _shard_keys(net, jobs, grid, 8, cur)
+    out = [t.cpu().numpy() for t in net.reduce_keys(keys, jobs.J)]
+    for a, b in zip(out, ref):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_peer_exchange_kernel_loopback(G):
+    """The NVLink key-exchange kernel itself (exchange.cu: push into every window, epoch flags,
+    wait, per-job max) among G virtual ranks on one GPU, over 3 consecutive calls (both window
+    parities): every virtual rank returns the single-GPU result bit for bit."""
+    L, H = 2, 128
+    W = synth.make_weights(synth.NetDesc(L, H), seed=100 + G)
+    jobs = synth.small_fleet(300, 60 + G)
+    grid = synth.log_grid(32, 32)
+    net = make(L, H, W)
+    cur = synth.current_configs(jobs.J, grid.C, 5)
+    ref = gpu_argmax(net, jobs, grid, cur)
+    keys = _shard_keys(net, jobs, grid, G, cur)
+    bi, bs, cs = (t.cpu().numpy() for t in net.debug_peer_loopback(keys, jobs.J, calls=3))
+    for r in range(G):
+        assert np.array_equal(bi[r], ref[0]) and np.array_equal(bs[r], ref[1]) and np.array_equal(cs[r], ref[2])
+
+
+def test_peer_exchange_timeout_is_an_error_not_a_trap():
+    """A virtual rank that never arrives: the others give up after the timeout, the call returns
+    AB_E_NCCL (device status word, no __trap), and the same context keeps working afterwards."""
+    from paper_2112_13509_b200.autobyte import AB_E_NCCL, AutoByteError
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H), seed=5)
+    jobs = synth.small_fleet(20, 5)
+    grid = synth.log_grid(8, 8)
+    net = make(L, H, W)
+    cur = synth.current_configs(jobs.J, grid.C, 5)
+    keys = _shard_keys(net, jobs, grid, 2, cur)
+    with pytest.raises(AutoByteError) as ei:
+        net.debug_peer_loopback(keys, jobs.J, calls=1, absent_rank=1, timeout_ms=200)
+    assert ei.value.status == AB_E_NCCL
+    assert b"timed out" in net.lib.autobyte_last_error(net.ctx)
+    # the context (and the CUDA context) is still usable
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    check_scores(gpu_scores(net, jobs, grid), s_ora, RTOL)
+    bi, _, _ = net.debug_peer_loopback(keys, jobs.J, calls=2)
+    assert np.array_equal(bi.cpu().numpy()[0], gpu_argmax(net, jobs, grid)[0])

@@ -490,3 +490,84 @@ def test_sharded_argmax_combines_to_numpy_argmax():
             assert cands[0][1] == full[r]
     idx, val = oracle.argmax_rows(s[:, 9:10], c_offset=9)
     assert idx.tolist() == [9] * 6 and np.array_equal(val, s[:, 9])
+
+
+# ---------------------------------------------------------------- closed-form LSTM encoder (l = 1, 2)
+@pytest.mark.parametrize("l", [1, 2])
+def test_lstm_closed_form_golden(l):
+    """tests/golden/lstm_closed_form.json: x[0] of a one-worker job written out by hand through
+    t' = log2(1 + T/1 ms), the embedding and both LSTM layers (the l = 1 single-step closed form
+    and one recurrent step). Pins the feature transform, the gate order and the recurrence."""
+    import math
+    from tests.helpers import load_golden
+    g = load_golden("lstm_closed_form.json")
+    t = math.tanh
+    sf, so = 1.0 / (1.0 + math.exp(-1.0)), 1.0 / (1.0 + math.exp(1.0))
+    # the closed form of the file's derivation, evaluated independently of the oracle
+    c1 = 0.5 * t(0.5); h1 = so * t(c1); c2 = 0.5 * t(h1); h2 = so * t(c2)
+    if l == 2:
+        c1 = sf * c1 + 0.5 * t(0.25 + 2 * h1); h1 = so * t(c1)
+        c2 = sf * c2 + 0.5 * t(h1); h2 = so * t(c2)
+    assert h2 == pytest.approx(g["expected_x0"][f"l{l}"], rel=1e-15)
+    from tests.helpers import lstm_golden_weights
+    W = lstm_golden_weights()
+    T = np.zeros((2, 16), np.float32)
+    T[:, 0] = g["job"]["T_ms"]
+    T[:, 1:] = 1e9                      # padded workers carry garbage
+    Bd = np.ones(16, np.float32)
+    x = oracle.encode_job(W, T, Bd, Bd, 1, l, 0, 0)
+    assert x[0] == pytest.approx(h2, rel=1e-13, abs=1e-16)
+    assert np.all(x[1:32] == 0.0)
+
+
+def test_lstm_single_step_ignores_recurrent_weights_and_forget_gate():
+    """l = 1 with h0 = c0 = 0 (R#5): c = i*g and h = o*tanh(c), so the recurrent weights W_h and
+    the forget gate cannot influence the output."""
+    desc = synth.NetDesc(2, 64)
+    W = synth.make_weights(desc, seed=77)
+    jobs = synth.small_fleet(3, 5)
+    W2 = {k: v.copy() for k, v in W.items()}
+    rng = np.random.default_rng(1)
+    for name in ("lstm1_Wh", "lstm2_Wh"):
+        W2[name] = rng.normal(0, 5, W[name].shape).astype(np.float32)
+    for name in ("lstm1_Wx", "lstm2_Wx"):
+        W2[name][32:64] = rng.normal(0, 5, (32, W[name].shape[1])).astype(np.float32)
+    for name in ("lstm1_b", "lstm2_b"):
+        W2[name][32:64] = rng.normal(0, 5, 32).astype(np.float32)
+    for j in range(3):
+        args = (jobs.T[j], jobs.B_d[j], jobs.B_u[j], jobs.n[j], 1, jobs.m[j], jobs.arc[j])
+        assert np.array_equal(oracle.encode_job(W, *args), oracle.encode_job(W2, *args))
+        # ... while at l = 2 they do
+        args2 = args[:4] + (2,) + args[5:]
+        assert not np.array_equal(oracle.encode_job(W, *args2), oracle.encode_job(W2, *args2))
+
+
+# ---------------------------------------------------------------- worker-permutation equivariance
+@pytest.mark.parametrize("seed", range(3))
+def test_worker_permutation_equivariance_at_n_max(seed):
+    """permuting the workers of T's columns and of B_d / B_u consistently permutes
+    V_hat identically when n = n_max. With general weights this holds once the weights that see a
+    worker index are permuted with it (W_e's columns, W1's two bandwidth blocks, W_o's rows and
+    b_o), so a worker index crossed anywhere in the encoder or the head breaks it; the score (the
+    mean over all 16 workers) is invariant."""
+    desc = synth.NetDesc(2, 32)
+    W = synth.make_weights(desc, seed=300 + seed)
+    jobs = synth.make_jobs(2, 40 + seed, ["vgg16", "alexnet"], [0, 1], [16])
+    rng = np.random.default_rng(seed)
+    pi = rng.permutation(16)
+    Wp = {k: v.copy() for k, v in W.items()}
+    Wp["W_e"] = W["W_e"][:, pi]
+    Wp["W1"][:, 32:48] = W["W1"][:, 32 + pi]
+    Wp["W1"][:, 48:64] = W["W1"][:, 48 + pi]
+    Wp["W_o"] = W["W_o"][pi]
+    Wp["b_o"] = W["b_o"][pi]
+    u = oracle.encode_grid(np.array([1 << 20, 1 << 26], np.int64), np.array([1.0, 7.0], np.float32))
+    for j in range(2):
+        x = oracle.encode_job(W, jobs.T[j], jobs.B_d[j], jobs.B_u[j], 16, jobs.l[j], jobs.m[j], jobs.arc[j])
+        xp = oracle.encode_job(Wp, jobs.T[j][:, pi], jobs.B_d[j][pi], jobs.B_u[j][pi], 16, jobs.l[j], jobs.m[j],
+                               jobs.arc[j])
+        Z = np.concatenate([np.broadcast_to(x, (4, 82)), u], axis=1)
+        Zp = np.concatenate([np.broadcast_to(xp, (4, 82)), u], axis=1)
+        V, Vp = oracle.head_forward(W, Z), oracle.head_forward(Wp, Zp)
+        np.testing.assert_allclose(Vp, V[:, pi], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(oracle.speed(Vp, 16), oracle.speed(V, 16), rtol=1e-12)
