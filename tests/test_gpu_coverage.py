@@ -114,7 +114,7 @@ def test_encoder_single_layer_jobs():
     """l_j = 1 for every job (one LSTM step from h0 = c0 = 0): x and scores vs the oracle."""
     L, H = 2, 128
     W = synth.make_weights(synth.NetDesc(L, H), seed=31)
-    jobs = synth.small_fleet(33, 31, l_max=4)
+    jobs = synth.make_jobs(33, 31, ["alexnet"], [0, 1], list(range(1, 17)), l_max=8)
     jobs.l[:] = 1
     jobs.T[:, 1:, :] = 0.0
     net = make(L, H, W)
