@@ -160,7 +160,9 @@ autobyte_status autobyte_get_unique_id(void* out_128_bytes);
  * exchange. A peer wait that exceeds AUTOBYTE_PEER_TIMEOUT_S seconds (default 120, 0 = forever)
  * makes that call's results invalid and the next call (or autobyte_synchronize) return AB_E_NCCL;
  * nothing traps, the ctx stays usable. Calls may be captured into CUDA graphs (the exchange epoch
- * is a device counter; the opt-in AUTOBYTE_PEER_X gather falls back to NCCL while capturing).
+ * is a device counter; the opt-in AUTOBYTE_PEER_X gather falls back to NCCL while capturing);
+ * capture only after one eager call of the same shapes (workspaces are allocated on first use),
+ * and destroy such graphs before autobyte_destroy (captured NCCL work holds the communicator).
  * After this,
  * autobyte_argmax exchanges the per-job best keys so every rank returns the global result;
  * shards must partition [0, C) across ranks. world == 1 detaches.

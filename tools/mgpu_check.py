@@ -91,6 +91,43 @@ def run(name, desc, jobs, grid, cg, dev, rank, world):
     return res
 
 
+def graph_replay(dev, rank, world):
+    """CUDA-graph capture of the sharded argmax (the exchange epoch is a device counter, so every
+    replay is a fresh exchange): replays with changed inputs (current configs rewritten in place)
+    must equal eager calls on every rank."""
+    c3 = synth.config("C3")
+    jobs, grid = c3.jobs.subset(np.arange(64)), synth.log_grid(32, 32)
+    W = synth.make_weights(c3.desc)
+    s = torch.cuda.Stream(dev)
+    net = AutoByte(c3.desc.hidden_layers, c3.desc.hidden_width, W, device=dev.index, stream=s)
+    abd.attach(net)
+    dj, dg = DeviceJobs.from_host(jobs, dev), DeviceGrid.from_host(grid, dev)
+    b, e = abd.my_shard(grid.C)
+    cur = torch.zeros(jobs.J, dtype=torch.int32, device=dev)
+    out = tuple(torch.empty(jobs.J, dtype=dt, device=dev) for dt in (torch.int32, torch.float32, torch.float32))
+    with torch.cuda.stream(s):
+        net.argmax(dj, dg, cur, b, e, out=out)   # warm-up: workspaces allocated outside the capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        net.argmax(dj, dg, cur, b, e, out=out)
+    ok = True
+    for rep in range(4):
+        cur.copy_(torch.as_tensor(synth.current_configs(jobs.J, grid.C, 100 + rep), device=dev))
+        g.replay()
+        s.synchronize()
+        got = [t.clone() for t in out]
+        with torch.cuda.stream(s):
+            ref = net.argmax(dj, dg, cur, b, e)
+        s.synchronize()
+        ok &= torch.equal(got[0], ref[0]) and torch.equal(got[1].view(torch.int32), ref[1].view(torch.int32)) and \
+            torch.equal(torch.nan_to_num(got[2]), torch.nan_to_num(ref[2]))
+    del g   # a graph holding captured NCCL work must go before the ctx's communicator is destroyed
+    torch.cuda.synchronize(dev)
+    net.close()
+    return {"graph_replay_same_as_eager": bool(ok), "world": world}
+
+
 def main():
     dist.init_process_group("nccl")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -106,7 +143,10 @@ def main():
              ("C4-subset-ragged-cg2", synth.NetDesc(4, 512), synth.config("C4").jobs.subset(np.arange(33)),
               synth.log_grid(45, 23), 2),
              # fewer jobs than ranks at G = 4: a rank with an empty encoder shard still takes part
-             ("C3-three-jobs", c3.desc, c3.jobs.subset(np.arange(3)), synth.log_grid(5, 3), 1)]
+             ("C3-three-jobs", c3.desc, c3.jobs.subset(np.arange(3)), synth.log_grid(5, 3), 1),
+             # fewer candidates than ranks (C = 1 and 3): some ranks hold an empty shard and still join
+             ("one-candidate", synth.NetDesc(2, 64), c3.jobs.subset(np.arange(9)), synth.log_grid(1, 1), 1),
+             ("three-candidates", synth.NetDesc(2, 64), c3.jobs.subset(np.arange(9)), synth.log_grid(1, 3), 1)]
     # every exchange: the fused peer-memory key kernel (default), the same plus the x all-gather
     # fused into K1a's epilogue (opt-in AUTOBYTE_PEER_X=1), and NCCL all-gathers + K5
     runs = [(mode,) + case for mode in ("peer", "peer_x", "nccl") for case in cases]
@@ -125,6 +165,13 @@ def main():
                    and r["topk_same_on_all_ranks"] and r["topk_g_invariant"] and r["host_same_as_device"]
                    and r["adapt_host_same_as_device"] and (world == 1 or r["host_staged_fraction"] < 0.75)
                    and r["peer_exchange"] == (world > 1 and mode != "nccl"))
+    gr = graph_replay(dev, rank, world)
+    okt = torch.tensor([int(gr["graph_replay_same_as_eager"])], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        gr["all_ranks"] = bool(okt.item())
+        print(json.dumps(gr), flush=True)
+        ok &= gr["all_ranks"]
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
