@@ -137,11 +137,21 @@ def oracle_sample(c, W, seconds, max_jobs=64):
     return done * c.grid.C / dt, done, threads
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_obj(c, W, seconds):
     rate, jobs, threads = oracle_sample(c, W, seconds)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{jobs} of {c.jobs.J} jobs x all {c.grid.C} candidates (encode + score + arg-max, float64 numpy)",
-            "nproc": os.cpu_count()}
+            "nproc": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 def run_reference(args):
@@ -172,7 +182,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {**describe(c), "parallelism": "single-process CPU oracle"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": f"per step 1 of {c.jobs.J} jobs x all {c.grid.C} candidates + 16-sample adapt"},
+                             "sample": f"per step 1 of {c.jobs.J} jobs x all {c.grid.C} candidates + 16-sample adapt",
+                             "nproc": os.cpu_count(), "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     return 0
@@ -329,7 +340,7 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MB write)",
                        "weights": "random He-uniform init of the 4x512 head (no trained weights exist)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "score_kernel<512> (K2)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": f"score_kernel<{H}> (K2, {L}x{H})",
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS 8192^3)",
                          "frac_of_sustained": achieved / peak_sus, "frac_of_datasheet_2250": achieved / 2250.0,
                          "k2_ms_per_launch": k2_ms, "k2_share_of_step": step_share,

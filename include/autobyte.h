@@ -69,7 +69,7 @@ typedef enum {
 
 typedef enum {
   AB_PREC_BF16 = 0,   /* bf16 tensor-core operands, fp32 accumulate (parity 2e-2, R#16) */
-  AB_PREC_FP32 = 1    /* split-operand bf16x3 emulation of fp32 products (parity 1e-4); H <= 256 */
+  AB_PREC_FP32 = 1    /* split-operand bf16x3 emulation of fp32 products (parity 1e-4); every H */
 } autobyte_precision;
 
 /* Shape of the meta-network (R#1-R#6). Supported: hidden_layers (L) in 1..8,

@@ -79,6 +79,7 @@ struct autobyte_ctx {
   DevBuf<float> params;          // fp32 masters (blob payload order)
   DevBuf<float> grads;           // same layout, head part used by adapt
   DevBuf<__nv_bfloat16> wpack;   // packed bf16 W_2..W_L for K2
+  DevBuf<uint32_t> spill;        // K2 activation scratch of the fp32 path at H = 512
   DevBuf<unsigned int> barrier;  // grid barrier of K4 (2 words)
   DevBuf<int> flag;              // AUTOBYTE_CHECK device flag
   // per-call workspace
@@ -473,7 +474,8 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.u = c->u.ptr;
   sp.wpack = c->wpack.ptr;
   sp.wmap = c->wmap;
-  sp.cta_group = c->planes == 2 ? 1 : c->cta_group;
+  sp.cta_group = c->planes == 2 ? (c->desc.hidden_width == 512 ? 2 : 1) : c->cta_group;
+  sp.spill = c->spill.ptr;
   sp.precision3 = c->planes == 2 ? 1 : 0;
   sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
   sp.cur_idx = cur_idx; sp.scores = scores;
@@ -559,7 +561,6 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   s = autobyte_validate_blob(desc, blob, blob_bytes);
   if (s != AB_OK) return s;
   if (precision != AB_PREC_BF16 && precision != AB_PREC_FP32) return AB_E_INVALID;
-  if (precision == AB_PREC_FP32 && desc->hidden_width > 256) return AB_E_UNSUPPORTED;   // hi+lo activations exceed smem
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -616,7 +617,13 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   const char* cg = std::getenv("AUTOBYTE_CTA_GROUP");
   c->cta_group = desc->hidden_width >= 256 ? 2 : 1;
   if (cg && (cg[0] == '1' || cg[0] == '2')) c->cta_group = cg[0] - '0';
-  if (!make_weight_tmap(&c->wmap, c->wpack.ptr, desc->hidden_width, desc->hidden_layers)) {
+  if (precision == AB_PREC_FP32 && desc->hidden_width == 512 && desc->hidden_layers > 1) {
+    // K2's activation scratch of the fp32 path at H = 512 (score.cu SPILL): per CTA 128 rows x the
+    // hi and lo bf16 of one layer (256 KB), one CTA per SM; it stays L2-resident
+    if ((e = c->spill.ensure((size_t)c->num_sms * kTileM * desc->hidden_width)) != cudaSuccess)
+      return bail(e, "alloc fp32 scratch");
+  }
+  if (!make_weight_tmap(&c->wmap, c->wpack.ptr, desc->hidden_width, desc->hidden_layers, c->planes)) {
     autobyte_destroy(c);
     return AB_E_CUDA;
   }
@@ -642,7 +649,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   }
   close_peer_window(c);
   if (c->comm) ncclCommDestroy(c->comm);
-  c->params.release(); c->grads.release(); c->wpack.release(); c->barrier.release(); c->flag.release();
+  c->params.release(); c->grads.release(); c->wpack.release(); c->spill.release(); c->barrier.release(); c->flag.release();
   c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
   c->opt_m.release(); c->opt_v.release(); c->topk_scores.release(); c->topk_keys.release();
   c->enc_stash.release(); c->enc_dz.release(); c->enc_part.release();

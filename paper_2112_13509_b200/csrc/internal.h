@@ -84,6 +84,7 @@ struct alignas(64) ScoreParams {
   unsigned long long* cur_keys; // [J]
   const int32_t* cur_idx;       // [J] or null
   float* scores;                // [J][c_end - c_begin] or null
+  uint32_t* spill;              // fp32 path at H = 512: [grid][128][spill_u32] activation scratch
 };
 
 struct AdaptParams {
@@ -142,6 +143,7 @@ cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned lo
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica
+__host__ __device__ int packed_weight_nch(int H, int planes);              // rows per packed tile
 #ifndef AB_WREP
 #define AB_WREP 1   // L2 replicas of the packed bf16 weights (CTA pair i streams replica i % AB_WREP)
 #endif
@@ -162,7 +164,7 @@ constexpr int kAdaptSplitK = 4;   // must match adapt.cu kSplitK (gradient parti
 cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model, int n_arch,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
-bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L);
+bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L, int planes);
 // device status word (ptx.cuh): each translation unit's copy of the pointer, set per device
 cudaError_t set_status_adapt(int* p);
 cudaError_t set_status_encode(int* p);

@@ -62,25 +62,33 @@ __device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3
 // P3 = 1 is the fp32-accuracy path (AB_PREC_FP32): every operand x is split into bf16 hi = rn(x) and
 // lo = rn(x - hi), and each product is hi*hi + hi*lo + lo*hi (the lo*lo term, ~2^-16 relative, is
 // dropped), so activations and weights take twice the storage and three MMAs per K step.
+// At H <= 256 both planes of both activation buffers fit on chip (X hi+lo in shared memory, Y hi+lo
+// in TMEM). At H = 512 (SPILL) they do not: a layer's input lives as hi plane in X (128 KB of shared
+// memory) + lo plane in TMEM (256 columns), next to two 128-column accumulators, and there is no
+// second buffer. Each epilogue thread therefore parks its share of the layer's output (hi and lo
+// bf16 of its row and column group, 128 B per chunk) in a per-CTA global scratch that stays in L2,
+// and once the layer's last chunk shows all of its MMAs done, reads its own share back into X / TMEM
+// piece by piece (afull per piece), so the next layer starts on piece 0 while later pieces load.
 template <int H, int CG, int P3 = 0>
 struct ScoreCfg {
-  static constexpr int NCH = P3 ? 64 : (H >= 128 ? 128 : H);  // N of one MMA / one TMEM accumulator chunk
+  static constexpr bool SPILL = P3 && H == 512;
+  static constexpr int NCH = P3 ? (SPILL ? 128 : 64) : (H >= 128 ? 128 : H);  // N of one MMA / accumulator chunk
   static constexpr int NP = P3 ? 2 : 1;           // operand planes (hi, lo)
   static constexpr int NQ = H / NCH;              // chunks per layer
   static constexpr int NKB = H / 64;              // 64-element K blocks per layer
   static constexpr int KB_PER_Q = NCH / 64;       // K blocks of the next layer produced by one chunk
   static constexpr int TILE_BYTES = NCH * 128;    // one (chunk, K block) weight tile of one plane
   static constexpr int STAGE_BYTES = TILE_BYTES * NP;   // ... of all planes
-  static constexpr int KBS = (CG == 2 && NKB >= 2) ? AB_KBS : 1;  // K blocks per pipeline stage
+  static constexpr int KBS = (CG == 2 && NKB >= 2 && !P3) ? AB_KBS : 1;  // K blocks per pipeline stage
   static constexpr int ATOM_BYTES = STAGE_BYTES / CG;        // this CTA's part of one K block (N-half for CG=2)
   static constexpr int CTA_STAGE_BYTES = ATOM_BYTES * KBS;   // this CTA's bytes per stage
   static constexpr int STAGE_TX = STAGE_BYTES * KBS;         // bytes per stage over the pair
   static constexpr int A_PLANE = kTileM * H * 2;  // bf16 activation tile (one plane), buffer X
-  static constexpr int A_BYTES = A_PLANE * NP;
+  static constexpr int A_BYTES = A_PLANE * (SPILL ? 1 : NP);   // SPILL: only the hi plane in smem
   static constexpr int NSPLIT = 4;                // epilogue warps per TMEM lane quadrant
   static constexpr int QC = NCH / NSPLIT;         // columns per epilogue warp per chunk
   static constexpr int G_CAP = H == 512 ? 3 : 7;  // hidden-layer biases kept in shared memory
-  static constexpr uint32_t Y_LO = H / 2;         // TMEM column offset of the lo plane of buffer Y
+  static constexpr uint32_t Y_LO = SPILL ? 0 : H / 2;   // TMEM column offset of the lo plane of buffer Y
   static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
   static constexpr int WV = H + 4;                // w_j | beta_j, 0, 0, 0 (one tile slot)
   static constexpr int WHAT_BYTES = 2 * WV * 4;   // two tile slots
@@ -100,6 +108,7 @@ struct ScoreCfg {
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t Y_COL = 256;          // TMEM column of activation buffer Y
   static constexpr int EPI_ARRIVALS = CG == 2 ? 32 : 16;   // 16 epilogue warps per CTA of the pair
+  static constexpr int SPILL_U32 = SPILL ? NQ * NSPLIT * (QC / 2) * NP : 0;   // scratch u32 per row (per CTA)
   static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(CTA_STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
@@ -148,6 +157,10 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
           if (CG == 2) {
             if (TS) umma_ts2(d_t, at, bd + 2 * kk, C::IDESC, acc);
             else umma_ss2(d_t, ad, bd + 2 * kk, C::IDESC, acc);
+            if (C::NP == 2) {   // SPILL: + A_hi (X) * W_lo + A_lo (TMEM, a_tmem0) * W_hi
+              umma_ss2(d_t, ad, bd + 2 * kk + ((C::TILE_BYTES / CG) >> 4), C::IDESC, 1u);
+              umma_ts2(d_t, at, bd + 2 * kk, C::IDESC, 1u);
+            }
           } else {
             if (TS) umma_ts(d_t, at, bd + 2 * kk, C::IDESC, acc);
             else umma_ss(d_t, ad, bd + 2 * kk, C::IDESC, acc);
@@ -268,9 +281,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
                   if (leader) mbar_arrive_expect_tx(&full[s], C::STAGE_TX);   // both halves of KBS blocks
 #pragma unroll
                   for (int a = 0; a < C::KBS; ++a)
-                    tma_load_2d_pair(sStage + s * C::CTA_STAGE_BYTES + a * C::ATOM_BYTES, &p.wmap, 0,
-                                     rep * rep_rows + (ti + a) * C::NCH + static_cast<int>(rank) * (C::NCH / 2),
-                                     &full[s], pol);
+#pragma unroll
+                    for (int pl = 0; pl < C::NP; ++pl)   // this CTA's half of the hi (then lo) tile
+                      tma_load_2d_pair(sStage + s * C::CTA_STAGE_BYTES + a * C::ATOM_BYTES + pl * (C::TILE_BYTES / 2),
+                                       &p.wmap, 0,
+                                       rep * rep_rows + ((ti + a) * C::NP + pl) * C::NCH +
+                                           static_cast<int>(rank) * (C::NCH / 2),
+                                       &full[s], pol);
                 } else {
                   mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
                   bulk_g2s(sStage + s * C::STAGE_BYTES, p.wpack + (size_t)rep * rep_rows * 64 + (size_t)ti * (C::NCH * 64 * C::NP),
@@ -306,9 +323,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #if defined(AB_EXP) && (AB_EXP & 8)
             if (false)   // timing experiment: every layer reads A from TMEM
 #else
-            if (src == 0)
+            if (C::SPILL || src == 0)
 #endif
-              mma_chunk<C, CG, false>(d_t, a_desc0, 0u, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
+              // (SPILL: every layer reads A hi from X and A lo from TMEM column Y_COL)
+              mma_chunk<C, CG, false>(d_t, a_desc0, C::SPILL ? tmem + C::Y_COL : 0u, b_desc0, full, empty, aw, aph, s,
+                                      ph, st, u == first + 2 * stride, g, q, trace_n);
             else
               mma_chunk<C, CG, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
             if (elect_one()) {
@@ -413,6 +432,55 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       __syncwarp();
       signal(&afull[q], CG == 2 ? mapa_shared(smem_u32(&afull[q]), 0) : 0u);
     };
+    // SPILL: a layer input's piece q is complete in X (hi) and TMEM (lo) for this warp
+    auto publish_both = [&](int q) {
+      fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      signal(&afull[q], CG == 2 ? mapa_shared(smem_u32(&afull[q]), 0) : 0u);
+    };
+    // SPILL: QC values -> hi plane into X, lo plane into TMEM (Y_COL), both at column c0
+    auto store_split = [&](int c0, const float (&v)[C::QC]) {
+      uint32_t hi[C::QC / 2], lo[C::QC / 2];
+#pragma unroll
+      for (int i = 0; i < C::QC / 2; ++i) {
+        hi[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        lo[i] = pack_bf16x2(v[2 * i] - __uint_as_float(hi[i] << 16), v[2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
+      }
+      store_plane(0, c0, hi, 0);
+      store_plane(1, c0, lo, 1);
+    };
+    // SPILL scratch: this thread's (row, column group) share of chunk q, hi then lo, 128 B; only this
+    // thread writes and reads it back (program order), so no fence is needed between the two
+    uint32_t* const spill_row = C::SPILL ? p.spill + ((size_t)blockIdx.x * kTileM + row) * C::SPILL_U32 : nullptr;
+    auto spill_store = [&](int q, const float (&v)[C::QC]) {
+      uint4* d = reinterpret_cast<uint4*>(spill_row + (q * C::NSPLIT + grp) * C::QC);
+      uint32_t hi[C::QC / 2], lo[C::QC / 2];
+#pragma unroll
+      for (int i = 0; i < C::QC / 2; ++i) {
+        hi[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        lo[i] = pack_bf16x2(v[2 * i] - __uint_as_float(hi[i] << 16), v[2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
+      }
+#pragma unroll
+      for (int i = 0; i < C::QC / 8; ++i) {
+        d[i] = make_uint4(hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
+        d[C::QC / 8 + i] = make_uint4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+      }
+    };
+    auto spill_reload = [&](int q) {   // chunk q's share back into X / TMEM
+      const uint4* d = reinterpret_cast<const uint4*>(spill_row + (q * C::NSPLIT + grp) * C::QC);
+      uint32_t hi[C::QC / 2], lo[C::QC / 2];
+#pragma unroll
+      for (int i = 0; i < C::QC / 8; ++i) {
+        const uint4 a = d[i], b = d[C::QC / 8 + i];
+        hi[4 * i] = a.x; hi[4 * i + 1] = a.y; hi[4 * i + 2] = a.z; hi[4 * i + 3] = a.w;
+        lo[4 * i] = b.x; lo[4 * i + 1] = b.y; lo[4 * i + 2] = b.z; lo[4 * i + 3] = b.w;
+      }
+      const int c0 = q * C::NCH + grp * C::QC;
+      store_plane(0, c0, hi, 0);
+      store_plane(1, c0, lo, 1);
+    };
     // layer-1 activations h1 = ReLU(a_j + W1c u_c) for the 128-column piece q (this warp's columns)
     auto build_piece = [&](int q, float up, float uc, int dst) {
       const int c0 = q * C::NCH + grp * C::QC;
@@ -442,7 +510,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           v[4 * i + 2] = relu(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)));
           v[4 * i + 3] = relu(fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
         }
-        store_vals(dst, c0, v);
+        if constexpr (C::SPILL) {
+          store_split(c0, v);
+          publish_both(q);
+          return;
+        } else {
+          store_vals(dst, c0, v);
+        }
       }
       publish(dst, q);
     };
@@ -537,7 +611,24 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           if (false)   // timing experiment: no epilogue math or activation stores
 #endif
           {
-            if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
+            if (!last && C::SPILL) {   // bias + ReLU in fp32 -> scratch; the last chunk refills X / TMEM
+              float v[C::QC];
+#pragma unroll
+              for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
+              if (q < C::NQ - 1) {
+                spill_store(q, v);
+              } else {
+                // this chunk's accumulator is ready, so every MMA of the layer (all readers of X and
+                // of the TMEM lo plane) has completed: reload pieces in order, publishing each
+#pragma unroll 1
+                for (int pq = 0; pq < C::NQ - 1; ++pq) {
+                  spill_reload(pq);
+                  publish_both(pq);
+                }
+                store_split(n0, v);
+                publish_both(q);
+              }
+            } else if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
               float v[C::QC];
 #pragma unroll
               for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
@@ -565,10 +656,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
               dot += (d4[0] + d4[1]) + (d4[2] + d4[3]);
             }
           }
-          if (!last) publish(dst, q);
+          if (!last && !C::SPILL) publish(dst, q);
           AB_ACC(st, 2, tc);
           AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
-          if (last && has_next && q == 0) {
+          // (SPILL: only once the last chunk shows the layer's MMAs done, X and TMEM are free)
+          if (last && has_next && q == (C::SPILL ? C::NQ - 1 : 0)) {
             // the next tile's h1, all pieces at once: once this warp has seen chunk 0 of the last
             // layer, the issuer has consumed every afull phase of this tile, so publishing the
             // next tile's phase cannot alias; building early takes h1 off the tile boundary
@@ -678,7 +770,7 @@ static cudaError_t launch_score_h(const ScoreParams& p, int num_sms, cudaStream_
   if constexpr (H <= 256) {
     if (p.precision3) return launch_score_hc<H, 1, 1>(p, num_sms, s);
   } else {
-    if (p.precision3) return cudaErrorNotSupported;
+    if (p.precision3) return launch_score_hc<H, 2, 1>(p, num_sms, s);   // SPILL variant (CTA pairs)
   }
   if (p.cta_group == 2) return launch_score_hc<H, 2, 0>(p, num_sms, s);
   return launch_score_hc<H, 1, 0>(p, num_sms, s);
@@ -760,10 +852,14 @@ cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_sco
 __host__ __device__ size_t packed_weight_elems(int H, int L, int planes) {
   return (size_t)(L > 1 ? L - 1 : 0) * H * H * planes;
 }
+// rows per packed tile = N of K2's accumulator chunks (ScoreCfg::NCH)
+__host__ __device__ int packed_weight_nch(int H, int planes) {
+  return planes == 2 ? (H == 512 ? 128 : 64) : (H >= 128 ? 128 : H);
+}
 
 __global__ void pack_kernel(const float* __restrict__ params, ParamOffsets off, int H, int L, int planes,
                             __nv_bfloat16* __restrict__ wpack) {
-  const int NCH = planes == 2 ? 64 : (H >= 128 ? 128 : H), NQ = H / NCH, NKB = H / 64;
+  const int NCH = packed_weight_nch(H, planes), NQ = H / NCH, NKB = H / 64;
   const size_t total = packed_weight_elems(H, L, planes);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const size_t tile_elems = (size_t)NCH * 64;
@@ -824,7 +920,7 @@ namespace ab {
 #ifndef AB_TMAP_L2_PROMOTION
 #define AB_TMAP_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
-bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L) {
+bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L, int planes) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -834,8 +930,8 @@ bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L
       return false;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const int NCH = H >= 128 ? 128 : H;
-  const size_t rows = packed_weight_elems(H, L, 1) / 64 * kWeightReplicas;
+  const int NCH = packed_weight_nch(H, planes);
+  const size_t rows = packed_weight_elems(H, L, planes) / 64 * kWeightReplicas;
   if (rows == 0) { std::memset(map, 0, sizeof(*map)); return true; }
   cuuint64_t dims[2] = {64, rows};
   cuuint64_t strides[1] = {128};

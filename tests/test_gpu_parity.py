@@ -641,11 +641,42 @@ def test_fp32_path_c3_sampled_and_exact_dyadic():
     assert np.array_equal(s_d[0], oracle.score_matrix(Wd, jobs, grid)[0])
 
 
-def test_fp32_path_rejects_h512():
-    from paper_2112_13509_b200.autobyte import AutoByteError
-    W = synth.make_weights(synth.NetDesc(2, 512))
-    with pytest.raises(AutoByteError):
-        make_fp32(2, 512, W)
+@pytest.mark.parametrize("L,P,Q", [(2, 7, 9), (3, 31, 9), (4, 16, 16)])
+def test_fp32_path_h512(L, P, Q):
+    """The fp32 path at H = 512 (K2's SPILL variant: layer outputs parked in an L2 scratch and
+    reloaded into X / TMEM piece by piece, CTA pairs, three MMAs per K step): per-job 1e-4 and the
+    arg-max rules at 1e-4, on ragged grids that leave partial tiles and an odd tile per pair."""
+    W = synth.make_weights(synth.NetDesc(L, 512), seed=L * 7 + 512)
+    jobs = synth.small_fleet(6, L + 512)
+    grid = synth.log_grid(P, Q)
+    s_ora = oracle.score_matrix(W, jobs, grid)
+    net = make_fp32(L, 512, W)
+    s = gpu_scores(net, jobs, grid)
+    err = check_scores(s, s_ora, RTOL32)
+    bi, bs, _ = gpu_argmax(net, jobs, grid)
+    nt = check_argmax(bi, s_ora, RTOL32)
+    assert np.array_equal(bs, s[np.arange(6), bi])
+    print(f"fp32 L={L} H=512: max err {err.max():.2e}, non-tied jobs {nt}/6")
+
+
+def test_fp32_path_h512_exact_dyadic_and_c4_sampled():
+    """Exact-dyadic 4x512 net bit for bit through the SPILL path, and the full C4 launch (4096 x
+    4096) on sampled jobs at 1e-4 with the arg-max rules."""
+    Wd, jobs, grid, _ = dyadic_net(4, 512, seed=4 * 1000 + 512)
+    s_d = gpu_scores(make_fp32(4, 512, Wd), jobs, grid).astype(np.float64)
+    assert np.array_equal(s_d[0], oracle.score_matrix(Wd, jobs, grid)[0])
+    c = synth.config("C4")
+    W = synth.make_weights(c.desc)
+    net = make_fp32(4, 512, W)
+    bi, bs, _ = gpu_argmax(net, c.jobs, c.grid)
+    sample = [0, 1, 2047, 4095]
+    s_ora = oracle.score_matrix(W, c.jobs, c.grid, job_idx=sample)
+    nt = check_argmax(bi[sample], s_ora, RTOL32)
+    for r, j in enumerate(sample):
+        assert abs(bs[j] - s_ora[r, bi[j]]) <= RTOL32 * np.max(np.abs(s_ora[r]))
+    s = gpu_scores(net, c.jobs.subset(sample), c.grid)
+    check_scores(s, s_ora, RTOL32)
+    print(f"fp32 C4 sampled: non-tied {nt}/4")
 
 
 def test_fp32_path_after_adapt():
