@@ -87,7 +87,8 @@ struct ScoreCfg {
   static constexpr int A_BYTES = A_PLANE * (SPILL ? 1 : NP);   // SPILL: only the hi plane in smem
   static constexpr int NSPLIT = 4;                // epilogue warps per TMEM lane quadrant
   static constexpr int QC = NCH / NSPLIT;         // columns per epilogue warp per chunk
-  static constexpr int G_CAP = H == 512 ? 3 : 7;  // hidden-layer biases kept in shared memory
+  static constexpr int G_CAP = SPILL ? 0 : (H == 512 ? 3 : 7);  // hidden-layer biases kept in shared memory
+                                                  // (SPILL: none; the space deepens the weight ring)
   static constexpr uint32_t Y_LO = SPILL ? 0 : H / 2;   // TMEM column offset of the lo plane of buffer Y
   static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
   static constexpr int WV = H + 4;                // w_j | beta_j, 0, 0, 0 (one tile slot)
@@ -451,11 +452,16 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       store_plane(0, c0, hi, 0);
       store_plane(1, c0, lo, 1);
     };
-    // SPILL scratch: this thread's (row, column group) share of chunk q, hi then lo, 128 B; only this
-    // thread writes and reads it back (program order), so no fence is needed between the two
-    uint32_t* const spill_row = C::SPILL ? p.spill + ((size_t)blockIdx.x * kTileM + row) * C::SPILL_U32 : nullptr;
+    // SPILL scratch: this thread's (row, column group) share of chunk q, hi then lo, as 2*QC/8 16-byte
+    // words; word i of the warp's 32 rows is 512 contiguous bytes (one coalesced access per warp
+    // instruction). Only this thread writes and reads its words back (program order): no fence.
+    // Layout per CTA: [chunk q][group grp][quadrant][word i][lane] x 16 B.
+    uint4* const spill_warp = C::SPILL ? reinterpret_cast<uint4*>(p.spill + (size_t)blockIdx.x * kTileM * C::SPILL_U32) +
+                                             (size_t)quad * (C::QC / 4) * 32 + lane
+                                       : nullptr;
+    auto spill_at = [&](int q) { return spill_warp + (size_t)(q * C::NSPLIT + grp) * 4 * (C::QC / 4) * 32; };
     auto spill_store = [&](int q, const float (&v)[C::QC]) {
-      uint4* d = reinterpret_cast<uint4*>(spill_row + (q * C::NSPLIT + grp) * C::QC);
+      uint4* d = spill_at(q);
       uint32_t hi[C::QC / 2], lo[C::QC / 2];
 #pragma unroll
       for (int i = 0; i < C::QC / 2; ++i) {
@@ -464,16 +470,16 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       }
 #pragma unroll
       for (int i = 0; i < C::QC / 8; ++i) {
-        d[i] = make_uint4(hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
-        d[C::QC / 8 + i] = make_uint4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+        d[32 * i] = make_uint4(hi[4 * i], hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
+        d[32 * (C::QC / 8 + i)] = make_uint4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
       }
     };
     auto spill_reload = [&](int q) {   // chunk q's share back into X / TMEM
-      const uint4* d = reinterpret_cast<const uint4*>(spill_row + (q * C::NSPLIT + grp) * C::QC);
+      const uint4* d = spill_at(q);
       uint32_t hi[C::QC / 2], lo[C::QC / 2];
 #pragma unroll
       for (int i = 0; i < C::QC / 8; ++i) {
-        const uint4 a = d[i], b = d[C::QC / 8 + i];
+        const uint4 a = d[32 * i], b = d[32 * (C::QC / 8 + i)];
         hi[4 * i] = a.x; hi[4 * i + 1] = a.y; hi[4 * i + 2] = a.z; hi[4 * i + 3] = a.w;
         lo[4 * i] = b.x; lo[4 * i + 1] = b.y; lo[4 * i + 2] = b.z; lo[4 * i + 3] = b.w;
       }
@@ -619,14 +625,15 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
                 spill_store(q, v);
               } else {
                 // this chunk's accumulator is ready, so every MMA of the layer (all readers of X and
-                // of the TMEM lo plane) has completed: reload pieces in order, publishing each
+                // of the TMEM lo plane) has completed: this chunk's piece goes straight in (freeing
+                // its registers), then the parked pieces come back in the order the next layer reads them
+                store_split(n0, v);
+                publish_both(q);
 #pragma unroll 1
                 for (int pq = 0; pq < C::NQ - 1; ++pq) {
                   spill_reload(pq);
                   publish_both(pq);
                 }
-                store_split(n0, v);
-                publish_both(q);
               }
             } else if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
               float v[C::QC];

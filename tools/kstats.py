@@ -1,5 +1,5 @@
 """Cycle accounting of K2 by warp role (needs libautobyte_stats.so: build.py --stats).
-Usage: python tools/kstats.py [L] [H] [J]"""
+Usage: python tools/kstats.py [L] [H] [J] [bf16|fp32]"""
 import ctypes
 import os
 import sys
@@ -22,15 +22,16 @@ def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     H = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     J = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
+    prec = sys.argv[4] if len(sys.argv) > 4 else "bf16"
     lib = ab.load_library(os.environ.get("AUTOBYTE_LIB") or STATS_LIB)
     fn = lib.ab_debug_stats
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     buf = (ctypes.c_ulonglong * 16)()
     jobs = ab.DeviceJobs.from_host(synth.small_fleet(J, 1))
     grid = ab.DeviceGrid.from_host(synth.log_grid(64, 64))
-    for cg in (1, 2):
+    for cg in ((1, 2) if prec == "bf16" else ((2,) if H == 512 else (1,))):
         os.environ["AUTOBYTE_CTA_GROUP"] = str(cg)
-        net = ab.AutoByte(L, H, synth.make_weights(synth.NetDesc(L, H)), device=0)
+        net = ab.AutoByte(L, H, synth.make_weights(synth.NetDesc(L, H)), device=0, precision=prec)
         net.argmax(jobs, grid)
         torch.cuda.synchronize()
         fn(buf, 1)
@@ -39,7 +40,7 @@ def main():
         fn(buf, 1)
         ctas = 148 // cg            # leader CTAs (the stats slots 0-11 come from rank 0)
         epi_warps = 16 * ctas
-        print(f"--- L={L} H={H} J={J} cta_group={cg}  (per producer/MMA warp and per epilogue warp, Mcycles)")
+        print(f"--- L={L} H={H} J={J} {prec} cta_group={cg}  (per producer/MMA warp and per epilogue warp, Mcycles)")
         for i, n in enumerate(NAMES):
             div = epi_warps if n.startswith(("epi", "peer")) else ctas
             print(f"{n:20s} {buf[i] / div / 1e6:9.3f}")
