@@ -3,6 +3,7 @@
 // K4 (adapt), K5 (finalize), and profiling.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -183,9 +184,21 @@ autobyte_status take_status(autobyte_ctx* c) {
     if (_e != cudaSuccess) return cuda_fail((ctx), _e, #expr);        \
   } while (0)
 
+// NVTX ranges (header-only NVTX3; near free without a tool attached): one per entry point and one
+// per kernel launch, named by kernel role, so an nsys / ncu timeline reads as the method's steps.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+const char* const kKindName[K_N] = {"K1 encode", "K2 score", "K5 finalize", "K3 exchange", "K4 adapt", "pack",
+                                    "other"};
+
 // Bracket one launch with profiling events (when enabled) and count it.
 template <typename F>
 cudaError_t timed(autobyte_ctx* c, int kind, F&& launch) {
+  NvtxRange range(kKindName[kind]);
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->profiling) {
     cudaEventCreate(&a);
@@ -554,6 +567,7 @@ autobyte_status autobyte_validate_blob(const autobyte_net_desc* d, const void* b
 
 autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob, size_t blob_bytes, int device,
                                 void* cuda_stream, autobyte_precision precision, autobyte_ctx** out) {
+  NvtxRange nvtx_range("autobyte_create");
   if (!out) return AB_E_INVALID;
   *out = nullptr;
   autobyte_status s = autobyte_validate_desc(desc);
@@ -680,6 +694,7 @@ autobyte_status autobyte_get_unique_id(void* out) {
 }
 
 autobyte_status autobyte_attach_comm(autobyte_ctx* c, const void* uid, int rank, int world) {
+  NvtxRange nvtx_range("autobyte_attach_comm");
   if (!c) return AB_E_INVALID;
   if (world < 1 || rank < 0 || rank >= world) return fail(c, AB_E_INVALID, "bad rank/world");
   DeviceGuard guard(c->device);
@@ -707,6 +722,7 @@ autobyte_status autobyte_attach_comm(autobyte_ctx* c, const void* uid, int rank,
 int32_t autobyte_peer_exchange(const autobyte_ctx* c) { return c && c->peer ? 1 : 0; }
 
 autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs, float* x_out) {
+  NvtxRange nvtx_range("autobyte_encode");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -723,6 +739,7 @@ autobyte_status autobyte_encode(autobyte_ctx* c, const autobyte_job_stats* jobs,
 
 autobyte_status autobyte_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                float* scores) {
+  NvtxRange nvtx_range("autobyte_score");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -736,6 +753,7 @@ autobyte_status autobyte_score(autobyte_ctx* c, const autobyte_job_stats* jobs, 
 
 autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                 const int32_t* cur_idx, int32_t* best_idx, float* best_score, float* cur_score) {
+  NvtxRange nvtx_range("autobyte_argmax");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -787,6 +805,7 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
 
 autobyte_status autobyte_argmax_keys(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                      const int32_t* cur_idx, uint64_t* keys_out) {
+  NvtxRange nvtx_range("autobyte_argmax_keys");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -803,6 +822,7 @@ autobyte_status autobyte_argmax_keys(autobyte_ctx* c, const autobyte_job_stats* 
 
 autobyte_status autobyte_reduce_keys(autobyte_ctx* c, int32_t J, int32_t G, const uint64_t* keys, int32_t* best_idx,
                                      float* best_score, float* cur_score) {
+  NvtxRange nvtx_range("autobyte_reduce_keys");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   if (J < 1 || G < 1) return fail(c, AB_E_SHAPE, "J and G must be >= 1");
@@ -904,6 +924,7 @@ extern "C" {
 
 autobyte_status autobyte_topk(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid, int32_t k,
                               int32_t* idx, float* score) {
+  NvtxRange nvtx_range("autobyte_topk");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -943,6 +964,7 @@ autobyte_status autobyte_topk(autobyte_ctx* c, const autobyte_job_stats* jobs, c
 autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                const float* sc_mult, const float* v_obs, float lr, int32_t steps,
                                float* loss_before) {
+  NvtxRange nvtx_range("autobyte_adapt");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
@@ -960,6 +982,7 @@ autobyte_status autobyte_adapt(autobyte_ctx* c, const autobyte_job_stats* sample
 autobyte_status autobyte_train(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                const float* sc_mult, const float* v_obs, const autobyte_optimizer* opt,
                                int32_t steps, float* losses) {
+  NvtxRange nvtx_range("autobyte_train");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
@@ -1043,6 +1066,7 @@ int64_t autobyte_optimizer_step(const autobyte_ctx* c) { return c ? c->opt_t : -
 autobyte_status autobyte_trigger(autobyte_ctx* c, int32_t J, const int32_t* best_idx, const float* best_score,
                                  const int32_t* cur_idx, const float* cur_score, const float* v_observed,
                                  float gain, float drift, int32_t* action) {
+  NvtxRange nvtx_range("autobyte_trigger");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   if (J < 1) return fail(c, AB_E_SHAPE, "J must be >= 1");
@@ -1064,6 +1088,7 @@ size_t autobyte_staged_job_bytes(const autobyte_ctx* c, int32_t J, int32_t l_max
 autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
                                      const int32_t* cur_idx, int32_t* best_idx, float* best_score,
                                      float* cur_score) {
+  NvtxRange nvtx_range("autobyte_argmax_host");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, jobs);
@@ -1104,6 +1129,7 @@ autobyte_status autobyte_argmax_host(autobyte_ctx* c, const autobyte_job_stats* 
 autobyte_status autobyte_adapt_host(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                     const float* sc_mult, const float* v_obs, float lr, int32_t steps,
                                     float* loss_before) {
+  NvtxRange nvtx_range("autobyte_adapt_host");
   if (!c) return AB_E_INVALID;
   if (autobyte_status ws = take_status(c)) return ws;
   autobyte_status s = check_jobs_host(c, samples);
