@@ -24,6 +24,13 @@ autobyte_status autobyte_debug_peer_loopback(autobyte_ctx* ctx, int32_t G, int32
                                              int32_t absent_rank, int32_t timeout_ms, const uint64_t* keys,
                                              int32_t* best_idx, float* best_score, float* cur_score);
 
+/* Memory debugging (the pool has no compute-sanitizer). With AUTOBYTE_DEBUG_MEM=1 set when a ctx is
+ * created, every library allocation from then on is filled with 0xFF bytes (NaN as fp32) so reads of
+ * never-written workspace surface as NaN / garbage in parity checks, and carries a 256-byte 0xA5
+ * canary after its requested size. This call synchronises the ctx's device and returns how many
+ * live canaries of that device were overwritten (0 = none; -1 on a CUDA error or NULL ctx). */
+int32_t autobyte_debug_mem_check(autobyte_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,7 +75,8 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_score", "autobyte_argmax", "autobyte_adapt", "autobyte_trigger", "autobyte_argmax_host",
            "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile",
-           "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback"]
+           "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback",
+           "autobyte_debug_mem_check"]
 
 _lib = None
 
@@ -123,6 +124,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_argmax_keys": (I32, [P, P, P, P, P]),
         "autobyte_reduce_keys": (I32, [P, I32, I32, P, P, P, P]),
         "autobyte_debug_peer_loopback": (I32, [P, I32, I32, I32, I32, I32, P, P, P, P]),
+        "autobyte_debug_mem_check": (I32, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -351,6 +353,10 @@ class AutoByte:
                                                           int(timeout_ms), keys.data_ptr(), bi.data_ptr(),
                                                           bs.data_ptr(), cs.data_ptr()), "debug_peer_loopback")
         return bi, bs, cs
+
+    def debug_mem_check(self) -> int:
+        """Test hook: overwritten workspace canaries on this device (AUTOBYTE_DEBUG_MEM=1)."""
+        return int(self.lib.autobyte_debug_mem_check(self.ctx))
 
     def adapt(self, samples: DeviceJobs, S_p, S_c, V_bar, lr: float, steps: int, want_loss: bool = True):
         import torch

@@ -37,20 +37,45 @@ struct DeviceGuard {
   }
 };
 
+// Memory debugging (AUTOBYTE_DEBUG_MEM=1 at create; the pool's compute-sanitizer is unavailable):
+// every library allocation is poisoned with 0xFF bytes (NaN as fp32, ~0 as integers), so a kernel
+// that reads workspace it never wrote produces NaN / garbage that the parity tests catch, and the
+// 256-byte slack after the requested size holds a 0xA5 canary that autobyte_debug_mem_check reads
+// back, so a write past the end of any workspace is counted.
+bool g_debug_mem = false;
+std::mutex g_canary_mu;
+std::vector<std::pair<uint8_t*, size_t>> g_canaries;   // (tail address, owner device)
+constexpr size_t kCanaryBytes = 256;
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t n = 0;
   cudaError_t ensure(size_t want) {
     if (want <= n && ptr) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T) + 256);
-    if (e == cudaSuccess) n = want;
-    return e;
+    release();
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T) + kCanaryBytes);
+    if (e != cudaSuccess) { ptr = nullptr; return e; }
+    n = want;
+    if (g_debug_mem) {
+      uint8_t* tail = reinterpret_cast<uint8_t*>(ptr) + want * sizeof(T);
+      if ((e = cudaMemset(ptr, 0xFF, want * sizeof(T))) != cudaSuccess) return e;
+      if ((e = cudaMemset(tail, 0xA5, kCanaryBytes)) != cudaSuccess) return e;
+      if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;   // before any stream uses it
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> lock(g_canary_mu);
+      g_canaries.push_back({tail, static_cast<size_t>(dev)});
+    }
+    return cudaSuccess;
   }
   void release() {
+    if (ptr && g_debug_mem) {
+      uint8_t* tail = reinterpret_cast<uint8_t*>(ptr) + n * sizeof(T);
+      std::lock_guard<std::mutex> lock(g_canary_mu);
+      for (auto it = g_canaries.begin(); it != g_canaries.end(); ++it)
+        if (it->first == tail) { g_canaries.erase(it); break; }
+    }
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     n = 0;
@@ -604,6 +629,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   c->peer_x = px && px[0] == '1';
   const char* chk = std::getenv("AUTOBYTE_CHECK");
   c->check = chk && chk[0] == '1';
+  const char* dm = std::getenv("AUTOBYTE_DEBUG_MEM");
+  if (dm && dm[0] == '1') g_debug_mem = true;   // process-wide from the first such create on
   const char* pt = std::getenv("AUTOBYTE_PEER_TIMEOUT_S");
   const double pts = pt ? std::atof(pt) : 120.0;
   c->peer_timeout_ns = pts > 0 ? static_cast<unsigned long long>(pts * 1e9) : 0ull;
@@ -833,6 +860,22 @@ autobyte_status autobyte_reduce_keys(autobyte_ctx* c, int32_t J, int32_t G, cons
             return launch_finalize(J, G, 2LL * J, k, k + J, best_idx, best_score, cur_score, c->stream);
           }));
   return AB_OK;
+}
+
+int32_t autobyte_debug_mem_check(autobyte_ctx* c) {
+  if (!c) return -1;
+  DeviceGuard guard(c->device);
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  std::lock_guard<std::mutex> lock(g_canary_mu);
+  int32_t bad = 0;
+  std::vector<uint8_t> h(kCanaryBytes);
+  for (auto& t : g_canaries) {
+    if (static_cast<int>(t.second) != c->device) continue;
+    if (cudaMemcpy(h.data(), t.first, kCanaryBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (uint8_t b : h)
+      if (b != 0xA5) { ++bad; break; }
+  }
+  return bad;
 }
 
 autobyte_status autobyte_debug_peer_loopback(autobyte_ctx* c, int32_t G, int32_t J, int32_t calls, int32_t absent_rank,

@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from tools.mgpu_check import graph_replay  # noqa: E402
+from tests.mgpu_check import graph_replay  # noqa: E402
 
 
 def main():

@@ -1,4 +1,4 @@
-"""Multi-GPU parity through torchrun (needs >= 2 GPUs; tools/mgpu_check.py does the checks)."""
+"""Multi-GPU parity through torchrun (needs >= 2 GPUs; tests/mgpu_check.py does the checks)."""
 import os
 import subprocess
 import sys
@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_candidate_sharding_is_g_invariant():
     n = min(torch.cuda.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(ROOT, "tools", "mgpu_check.py")]
+           "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(ROOT, "tests", "mgpu_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(out.stdout[-4000:], out.stderr[-4000:])
     assert out.returncode == 0 and "MGPU_OK" in out.stdout
