@@ -266,6 +266,20 @@ typedef struct {
 autobyte_status autobyte_train(autobyte_ctx* ctx, const autobyte_job_stats* samples,
                                const int64_t* sp_bytes, const float* sc_mult, const float* v_obs,
                                const autobyte_optimizer* opt, int32_t steps, float* losses);
+/* Offline training over a dataset ("360000 iterations" of collected runtime samples;
+ * P:418-423 "offline training"; R#18; SURVEY §8(f) NEXT 2 at scale): `steps` optimiser steps, step s
+ * on the minibatch of the `batch` dataset rows order[s][0..batch). dataset (J = N samples),
+ * sp_bytes / sc_mult [N] and v_obs [N][n_max] are the whole dataset (DEVICE); order is DEVICE int32
+ * [steps][batch], every entry in [0, N) (caller's contract: the shuffle is an input, e.g. one
+ * randperm per epoch; out-of-range entries are undefined behaviour). The samples are encoded once
+ * (frozen encoder), then ONE kernel runs all steps: per step it gathers the minibatch rows, runs
+ * forward, backward and the optimiser exactly as autobyte_train does on that minibatch (same
+ * objective, head scope, Adam state carried in the context). losses (nullable, DEVICE [steps]) gets
+ * each step's mean Eq. 2 norm before its update. opt->scope must be AB_SCOPE_HEAD
+ * (AB_E_UNSUPPORTED otherwise); other errors as autobyte_train. Deterministic. */
+autobyte_status autobyte_train_epoch(autobyte_ctx* ctx, const autobyte_job_stats* dataset, const int64_t* sp_bytes,
+                                     const float* sc_mult, const float* v_obs, const int32_t* order,
+                                     int32_t batch, int32_t steps, const autobyte_optimizer* opt, float* losses);
 /* Zero the Adam moments and step count (asynchronous, stream-ordered). */
 autobyte_status autobyte_reset_optimizer(autobyte_ctx* ctx);
 /* Adam step count t so far (host value; no synchronisation). */

@@ -76,7 +76,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile",
            "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback",
-           "autobyte_debug_mem_check"]
+           "autobyte_debug_mem_check", "autobyte_train_epoch"]
 
 _lib = None
 
@@ -125,6 +125,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_reduce_keys": (I32, [P, I32, I32, P, P, P, P]),
         "autobyte_debug_peer_loopback": (I32, [P, I32, I32, I32, I32, I32, P, P, P, P]),
         "autobyte_debug_mem_check": (I32, [P]),
+        "autobyte_train_epoch": (I32, [P, P, P, P, P, P, I32, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -391,6 +392,23 @@ class AutoByte:
                                             V_bar.data_ptr(), ctypes.byref(opt), int(steps),
                                             losses.data_ptr() if losses is not None else None), "train")
         return losses[:int(steps)] if losses is not None else None
+
+    def train_epoch(self, dataset: DeviceJobs, S_p, S_c, V_bar, order, optimizer: str = "adam", lr: float = 1e-3,
+                    beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, want_losses: bool = True):
+        """Dataset-level offline training (autobyte_train_epoch): order is a [steps][batch] int32
+        device tensor of dataset rows (e.g. torch.randperm per epoch, reshaped); returns the per-step
+        mean Eq. 2 norms before each update (device tensor)."""
+        import torch
+        kind = {"sgd": OPT_SGD, "adam": OPT_ADAM}[optimizer]
+        opt = Optimizer(kind, lr, beta1, beta2, eps, 0)
+        order = order.to(torch.int32).contiguous()
+        steps, batch = int(order.shape[0]), int(order.shape[1])
+        losses = torch.empty(max(steps, 1), dtype=torch.float32, device=self.torch_device) if want_losses else None
+        js = dataset.struct()
+        self._check(self.lib.autobyte_train_epoch(self.ctx, ctypes.byref(js), S_p.data_ptr(), S_c.data_ptr(),
+                                                  V_bar.data_ptr(), order.data_ptr(), batch, steps, ctypes.byref(opt),
+                                                  losses.data_ptr() if losses is not None else None), "train_epoch")
+        return losses[:steps] if losses is not None else None
 
     def reset_optimizer(self):
         self._check(self.lib.autobyte_reset_optimizer(self.ctx), "reset_optimizer")

@@ -437,7 +437,7 @@ __device__ void colsum_split(const float* X, int B, int N, long long ld, float* 
 // W_o is staged in shared memory once per CTA; lane l accumulates k = l, l+32, ... in fp32 FMA and
 // the 16 sums are reduced with a fixed xor butterfly (deterministic).
 __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, const float* vbar, const int32_t* nvalid,
-                         float scale, int B, int H, float* R, float* sW) {
+                         const int32_t* idx, float scale, int B, int H, float* R, float* sW) {
   {   // W_o -> shared memory with 8 independent 16-byte loads in flight per thread (H % 4 == 0)
     const float4* src = reinterpret_cast<const float4*>(Wo);
     float4* dst = reinterpret_cast<float4*>(sW);
@@ -483,8 +483,9 @@ __device__ void out_rows(const float* Hl, const float* Wo, const float* bo, cons
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == w) mine = v;
     }
+    const long long s = idx ? idx[b] : b;   // dataset row of minibatch row b (autobyte_train_epoch)
     if (lane < kNMax)
-      R[b * kNMax + lane] = lane < nvalid[b] ? (mine + bo[lane] - vbar[b * kNMax + lane]) * scale : 0.f;
+      R[b * kNMax + lane] = lane < nvalid[s] ? (mine + bo[lane] - vbar[s * kNMax + lane]) * scale : 0.f;
   }
   __syncthreads();   // sW aliases the GEMM ring
 }
@@ -600,21 +601,31 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   float* D[2] = {R + (size_t)B * 16, R + (size_t)B * 16 + (size_t)B * H};
   auto Hk = [&](int k) { return Hs + (size_t)(k - 1) * B * H; };
 
-  // phase 0: Z = [x | u(S_p, S_c)] (R#8)
-  for (int e = gtid; e < B * kZDim; e += gthreads) {
-    const int b = e / kZDim, i = e % kZDim;
-    float v;
-    if (i < kXDim) v = p.x[(size_t)b * kXDim + i];
-    else if (i == kXDim) v = static_cast<float>((log2(static_cast<double>(p.S_p[b])) - 21.0) / 8.0);
-    else v = static_cast<float>((static_cast<double>(p.S_c[b]) - 8.5) / 8.0);
-    Z[e] = v;
-  }
+  // phase 0: Z = [x | u(S_p, S_c)] (R#8) of the minibatch; with p.idx (autobyte_train_epoch) row b
+  // of step `step` is dataset row idx[step][b], gathered here, and Z is rebuilt every step
+  auto build_Z = [&](int step) {
+    const int32_t* ix = p.idx ? p.idx + (size_t)step * B : nullptr;
+    for (int e = gtid; e < B * kZDim; e += gthreads) {
+      const int b = e / kZDim, i = e % kZDim;
+      const long long r = ix ? ix[b] : b;
+      float v;
+      if (i < kXDim) v = p.x[(size_t)r * kXDim + i];
+      else if (i == kXDim) v = static_cast<float>((log2(static_cast<double>(p.S_p[r])) - 21.0) / 8.0);
+      else v = static_cast<float>((static_cast<double>(p.S_c[r]) - 8.5) / 8.0);
+      Z[e] = v;
+    }
+  };
+  build_Z(0);
   grid_sync(p.barrier, gen);
 
   const int nsteps = p.steps > 0 ? p.steps : 0;
   for (int step = 0; step <= nsteps; ++step) {
     const bool fwd_only = (step == nsteps);   // trailing forward only when loss is still needed
     if (fwd_only && !(nsteps == 0 && p.loss_before)) break;
+    if (p.idx && step > 0) {   // the previous step's last update (W1, b1) ran before this barrier
+      build_Z(step);
+      grid_sync(p.barrier, gen);
+    }
     // ---------------- forward with stash
     for (int k = 1; k <= L; ++k) {
       const int Kin = k == 1 ? kZDim : H;
@@ -635,7 +646,8 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
 #endif
       grid_sync(p.barrier, gen);
     }
-    out_rows(Hk(L), P + p.off.W_o, P + p.off.b_o, p.v_obs, p.n, 1.0f / static_cast<float>(B), B, H, R, ring);
+    out_rows(Hk(L), P + p.off.W_o, P + p.off.b_o, p.v_obs, p.n, p.idx ? p.idx + (size_t)step * B : nullptr,
+             1.0f / static_cast<float>(B), B, H, R, ring);
     grid_sync(p.barrier, gen);
     if (((step == 0 && p.loss_before) || (p.losses && !fwd_only)) && blockIdx.x == 0) {
       // mean over b of the Eq. 2 norm ||mask (V_hat - V_bar)||_2; R holds residual / B

@@ -929,8 +929,11 @@ namespace {
 // K1a on the samples (sharded across ranks) + K4 + re-pack: the body of adapt and train.
 autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* samples, const int64_t* sp_bytes,
                                 const float* sc_mult, const float* v_obs, int opt, float lr, float beta1,
-                                float beta2, float eps, int32_t steps, float* loss_before, float* losses) {
-  const int B = samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
+                                float beta2, float eps, int32_t steps, float* loss_before, float* losses,
+                                const int32_t* idx = nullptr, int batch = 0) {
+  // idx != nullptr (train_epoch): samples is the whole dataset (encoded once, encoder frozen) and
+  // step s trains on the `batch` rows idx[s][0..batch) of it, gathered inside K4
+  const int B = idx ? batch : samples->J, H = c->desc.hidden_width, L = c->desc.hidden_layers;
   AB_CUDA(c, c->adapt_ws.ensure(adapt_ws_floats(B, H, L)));
   EncodeParams ep{};
   autobyte_status s = run_lstm(c, samples, &ep);
@@ -943,6 +946,7 @@ autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* sampl
   ap.params = c->params.ptr; ap.off = c->off; ap.ws = c->adapt_ws.ptr; ap.grads = c->grads.ptr;
   ap.loss_before = loss_before; ap.losses = losses; ap.barrier = c->barrier.ptr;
   ap.opt = opt; ap.beta1 = beta1; ap.beta2 = beta2; ap.eps = eps;
+  ap.idx = idx;
   if (opt == AB_OPT_ADAM) {
     if (!c->opt_m.ptr) {   // moments start at zero (blob layout; only the head part is used)
       AB_CUDA(c, c->opt_m.ensure(c->off.total));
@@ -1091,6 +1095,31 @@ autobyte_status autobyte_train(autobyte_ctx* c, const autobyte_job_stats* sample
             return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
           }));
   return AB_OK;
+}
+
+autobyte_status autobyte_train_epoch(autobyte_ctx* c, const autobyte_job_stats* dataset, const int64_t* sp_bytes,
+                                     const float* sc_mult, const float* v_obs, const int32_t* order, int32_t batch,
+                                     int32_t steps, const autobyte_optimizer* opt, float* losses) {
+  NvtxRange nvtx_range("autobyte_train_epoch");
+  if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
+  autobyte_status s = check_jobs_host(c, dataset);
+  if (s != AB_OK) return s;
+  if (!sp_bytes || !sc_mult || !v_obs || !order) return fail(c, AB_E_INVALID, "train_epoch input pointer is NULL");
+  if (!opt) return fail(c, AB_E_INVALID, "optimizer is NULL");
+  if (opt->kind != AB_OPT_SGD && opt->kind != AB_OPT_ADAM) return fail(c, AB_E_INVALID, "unknown optimizer kind");
+  if (batch < 1 || steps < 0) return fail(c, AB_E_SHAPE, "need batch >= 1 and steps >= 0");
+  if (!std::isfinite(opt->lr)) return fail(c, AB_E_INVALID, "lr must be finite");
+  if (opt->kind == AB_OPT_ADAM && !(opt->beta1 >= 0.f && opt->beta1 < 1.f && opt->beta2 >= 0.f && opt->beta2 < 1.f &&
+                                    opt->eps > 0.f && std::isfinite(opt->eps)))
+    return fail(c, AB_E_INVALID, "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
+  if (opt->scope != AB_SCOPE_HEAD)
+    return fail(c, AB_E_UNSUPPORTED, "train_epoch trains the head (the encoder is encoded once per call)");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, dataset, nullptr)) != AB_OK) return s;
+  if (steps == 0) return AB_OK;
+  return run_head_update(c, dataset, sp_bytes, sc_mult, v_obs, opt->kind, opt->lr, opt->beta1, opt->beta2, opt->eps,
+                         steps, nullptr, losses, order, batch);
 }
 
 autobyte_status autobyte_reset_optimizer(autobyte_ctx* c) {

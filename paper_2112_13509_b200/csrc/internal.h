@@ -109,6 +109,8 @@ struct AdaptParams {
   float* m;                // Adam first moments (blob layout, head part used) or null
   float* v;                // Adam second moments
   float* dz_out;           // [B][84] d objective / d [x | u] (encoder fine-tuning) or null
+  const int32_t* idx;      // [steps][B] dataset rows of each step's minibatch (train_epoch) or null:
+                           // then x / S_p / S_c / v_obs / n are the whole dataset's arrays
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)

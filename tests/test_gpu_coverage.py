@@ -317,3 +317,68 @@ def test_peer_exchange_timeout_is_an_error_not_a_trap():
     check_scores(gpu_scores(net, jobs, grid), s_ora, RTOL)
     bi, _, _ = net.debug_peer_loopback(keys, jobs.J, calls=2)
     assert np.array_equal(bi.cpu().numpy()[0], gpu_argmax(net, jobs, grid)[0])
+
+
+# ------------------------------------------------------------------------------------- NEXT 2 at scale
+def _dataset(N, seed):
+    jobs = synth.make_jobs(N, seed, ["alexnet", "vgg16", "transformer"], [0, 1], list(range(1, 17)), l_max=16)
+    return synth.make_adapt_batch(jobs, synth.log_grid(64, 64), seed + 1)
+
+
+def _orders(N, batch, steps, seed):
+    """The shuffle is an input of autobyte_train_epoch: consecutive permutations of [0, N) cut into
+    minibatches of `batch` rows (a tail shorter than a batch is dropped, as an epoch loader would)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    while len(rows) < steps:
+        perm = rng.permutation(N)
+        rows += [perm[i:i + batch] for i in range(0, N - batch + 1, batch)]
+    return np.stack(rows[:steps]).astype(np.int32)
+
+
+@pytest.mark.parametrize("opt,N,batch,steps", [("adam", 3000, 1000, 4), ("sgd", 2500, 700, 3), ("adam", 9000, 4096, 2)])
+def test_train_epoch_matches_oracle_over_minibatches(opt, N, batch, steps):
+    """autobyte_train_epoch (one K4 launch for all steps, minibatch rows gathered in-kernel) ==
+    oracle.train applied minibatch by minibatch with the optimiser state carried: per-step losses
+    and per-tensor updates; batch 4096 runs K4's 128x128 tile path."""
+    L, H = 3, 256
+    W = synth.make_weights(synth.NetDesc(L, H), seed=N + batch)
+    data = _dataset(N, 300 + batch)
+    order = _orders(N, batch, steps, 7)
+    kw = dict(lr=3e-4, beta1=0.9, beta2=0.99, eps=1e-6) if opt == "adam" else dict(lr=1e-2)
+    Wn, st, want = W, None, []
+    for s in range(steps):
+        mb = synth.AdaptBatch(data.jobs.subset(order[s]), data.S_p[order[s]], data.S_c[order[s]], data.V_bar[order[s]])
+        Wn, st, ls = oracle.train(Wn, mb, 1, opt, state=st, **kw)
+        want += ls
+    net = make(L, H, W)
+    got = net.train_epoch(*dev_batch(data), torch.as_tensor(order, device="cuda"), opt, **kw).cpu().numpy()
+    assert abs(got[0] - want[0]) <= 1e-4 * want[0]
+    np.testing.assert_allclose(got, np.array(want), rtol=1e-3)
+    check_update(W, Wn, net.get_weights(), 2e-3)
+    if opt == "adam":
+        assert net.optimizer_step == steps
+
+
+def test_train_epoch_learns_a_teacher():
+    """Dataset-level training at scale: 16384 samples labelled by a same-architecture teacher (its
+    per-worker speeds through the oracle), 80 epochs (320 steps) of shuffled 4096-sample minibatches
+    in one call with Adam; the last epoch's mean loss is at least 5x below the first step's."""
+    L, H = 3, 256
+    desc = synth.NetDesc(L, H)
+    W = synth.make_weights(desc, seed=1)
+    teacher = synth.make_weights(desc, seed=2)
+    for k in oracle.ENCODER_PARAMS:
+        teacher[k] = W[k]                 # the encoder is frozen: only the head can match
+    N, batch = 16384, 4096
+    data = _dataset(N, 900)
+    X = oracle.encode_jobs(teacher, data.jobs)
+    U = np.stack([oracle.encode_candidate(data.S_p[b], data.S_c[b]) for b in range(N)])
+    Vt = oracle.head_forward(teacher, np.concatenate([X, U], 1))
+    data.V_bar = (Vt * (np.arange(16)[None, :] < data.jobs.n[:, None])).astype(np.float32)
+    order = _orders(N, batch, 80 * (N // batch), 3)
+    net = make(L, H, W)
+    losses = net.train_epoch(*dev_batch(data), torch.as_tensor(order, device="cuda"), "adam", lr=1e-3).cpu().numpy()
+    last_epoch = losses[-(N // batch):].mean()
+    assert np.all(np.isfinite(losses)) and last_epoch < losses[0] / 5, (losses[0], last_epoch)
+    print(f"teacher fit: loss {losses[0]:.4f} -> {last_epoch:.4f} over {len(losses)} steps")
