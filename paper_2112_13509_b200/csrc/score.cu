@@ -33,6 +33,9 @@ namespace ab {
 #ifndef AB_KBS
 #define AB_KBS 2   // 64-wide K blocks per weight stage for CTA pairs
 #endif
+#ifndef AB_NT
+#define AB_NT 1    // tiles in flight per CTA on narrow bf16 heads (H <= 256); 2 measured slower (epilogue-bound)
+#endif
 
 // Optional cycle accounting (build with -DAB_STATS): where each warp role spends its time.
 #ifdef AB_STATS
@@ -72,6 +75,11 @@ __device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3
 template <int H, int CG, int P3 = 0>
 struct ScoreCfg {
   static constexpr bool SPILL = P3 && H == 512;
+  // NT tiles in flight per CTA (narrow bf16 heads): the issuer interleaves their chunks (layer g,
+  // chunk q, tile t), so one tile's layer-boundary epilogue latency hides behind the other tile's
+  // MMAs. Each tile has its own X (shared memory) and Y (TMEM, YS columns) buffers; at H <= 256 TMEM
+  // holds the two 128-column accumulators plus NT Y buffers.
+  static constexpr int NT = (!P3 && H <= 256) ? AB_NT : 1;
   static constexpr int NCH = P3 ? (SPILL ? 128 : 64) : (H >= 128 ? 128 : H);  // N of one MMA / accumulator chunk
   static constexpr int NP = P3 ? 2 : 1;           // operand planes (hi, lo)
   static constexpr int NQ = H / NCH;              // chunks per layer
@@ -90,13 +98,14 @@ struct ScoreCfg {
   static constexpr int G_CAP = SPILL ? 0 : (H == 512 ? 3 : 7);  // hidden-layer biases kept in shared memory
                                                   // (SPILL: none; the space deepens the weight ring)
   static constexpr uint32_t Y_LO = SPILL ? 0 : H / 2;   // TMEM column offset of the lo plane of buffer Y
-  static constexpr int AW_BYTES = 3 * H * 4;      // a_j, W1[:,82], W1[:,83] (structure of arrays)
+  static constexpr uint32_t YS = H / 2;           // TMEM columns between the Y buffers of the NT tiles
+  static constexpr int AW_BYTES = (NT + 2) * H * 4;   // a_j of each tile, W1[:,82], W1[:,83] (SoA)
   static constexpr int WV = H + 4;                // w_j | beta_j, 0, 0, 0 (one tile slot)
-  static constexpr int WHAT_BYTES = 2 * WV * 4;   // two tile slots
+  static constexpr int WHAT_BYTES = 2 * NT * WV * 4;   // (current, next) x NT tiles
   static constexpr int BIAS_BYTES = G_CAP * H * 4;
   static constexpr int PART_BYTES = NSPLIT * kTileM * 4;
   static constexpr int MISC_BYTES = 512;
-  static constexpr int FIXED = A_BYTES + AW_BYTES + WHAT_BYTES + BIAS_BYTES + PART_BYTES + MISC_BYTES;
+  static constexpr int FIXED = NT * A_BYTES + AW_BYTES + WHAT_BYTES + BIAS_BYTES + PART_BYTES + MISC_BYTES;
   static constexpr int BUDGET = 232448 - 1024;    // opt-in maximum minus the 1 KB alignment slack
   static constexpr int NS_FIT = (BUDGET - FIXED) / CTA_STAGE_BYTES;
 #ifdef AB_NS_MAX
@@ -112,6 +121,7 @@ struct ScoreCfg {
   static constexpr int SPILL_U32 = SPILL ? NQ * NSPLIT * (QC / 2) * NP : 0;   // scratch u32 per row (per CTA)
   static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
   static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(NT == 1 || Y_COL + NT * YS <= TMEM_COLS, "TMEM budget of the NT Y buffers");
   static_assert(CTA_STAGE_BYTES % 1024 == 0 && A_BYTES % 1024 == 0, "SW128 atoms need 1 KB alignment");
 };
 
@@ -198,19 +208,19 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   // 1 KB-aligned base derived by pointer arithmetic on the __shared__ array (no integer round trip),
   // so the compiler keeps every derived pointer in the shared window and emits LDS/STS, not generic loads
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = base;
-  uint8_t* sStage = sA + C::A_BYTES;
-  float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::CTA_STAGE_BYTES);   // [3][H]: a_j | W1c0 | W1c1
-  float* sWhat = sAw + 3 * H;                                                   // [2][WV]
-  float* sBias = sWhat + 2 * C::WV;                                             // [G_CAP][H]
+  uint8_t* sA = base;                                                           // [NT][A_BYTES]: X per tile
+  uint8_t* sStage = sA + C::NT * C::A_BYTES;
+  float* sAw = reinterpret_cast<float*>(sStage + C::NS * C::CTA_STAGE_BYTES);   // [NT+2][H]: a_j.. | W1c0 | W1c1
+  float* sWhat = sAw + (C::NT + 2) * H;                                         // [2][NT][WV]
+  float* sBias = sWhat + 2 * C::NT * C::WV;                                     // [G_CAP][H]
   float* sPart = sBias + C::G_CAP * H;                                          // [NSPLIT][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + C::NSPLIT * kTileM);
   uint64_t* full = bars;
   uint64_t* empty = full + C::NS;
   uint64_t* dfull = empty + C::NS;
   uint64_t* dempty = dfull + 2;
-  uint64_t* afull = dempty + 2;                                                 // [NQ]
-  uint64_t* vfull = afull + C::NQ;                                              // next tile's job vectors
+  uint64_t* afull = dempty + 2;                                                 // [NT][NQ]
+  uint64_t* vfull = afull + C::NT * C::NQ;                                      // next unit's job vectors
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(vfull + 1);
   unsigned long long* sWkey = reinterpret_cast<unsigned long long*>(sTmem + 2);
 
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::EPI_ARRIVALS); }
-    for (int q = 0; q < C::NQ; ++q) mbar_init(&afull[q], C::EPI_ARRIVALS);
+    for (int q = 0; q < C::NT * C::NQ; ++q) mbar_init(&afull[q], C::EPI_ARRIVALS);
     mbar_init(vfull, 1);
     fence_barrier_init();
   }
@@ -239,8 +249,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   if (warp >= 2) {
     const float* W1 = p.params + p.off.W[1];
     for (int k = threadIdx.x - 64; k < H; k += kEpiThreads) {
-      sAw[H + k] = W1[(size_t)k * kZDim + kXDim];
-      sAw[2 * H + k] = W1[(size_t)k * kZDim + kXDim + 1];
+      sAw[C::NT * H + k] = W1[(size_t)k * kZDim + kXDim];
+      sAw[(C::NT + 1) * H + k] = W1[(size_t)k * kZDim + kXDim + 1];
     }
     const int gs = G < C::G_CAP ? G : C::G_CAP;
     for (int e = threadIdx.x - 64; e < gs * H; e += kEpiThreads) sBias[e] = p.params[p.off.b[e / H + 2] + e % H];
@@ -249,8 +259,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sTmem;
-  // tile schedule: CG = 1 -> tile = first + i*stride; CG = 2 -> pair-tile pt, this CTA's tile 2*pt + rank
-  const long long n_units = CG == 2 ? (p.n_tiles + 1) / 2 : p.n_tiles;
+  // work unit u = NT tiles per CTA (of a pair): this CTA's tile t of unit u is (u*NT + t)*CG + rank;
+  // units are handed out round-robin: first + i*stride
+  const long long n_units = (p.n_tiles + CG * C::NT - 1) / (CG * C::NT);
   const long long first = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
   const long long stride = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
 
@@ -266,6 +277,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       for (long long u = first; u < n_units; u += stride)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
+            for (int t = 0; t < C::NT; ++t)   // every tile of the unit streams the same chunk weights
             for (int b = 0; b < C::NKB; b += C::KBS) {
               AB_T0(te);
               mbar_wait(&empty[s], ph ^ 1);
@@ -306,12 +318,14 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       int s = 0;
       uint32_t ph = 0, aph = 0, dbits = 0;
       int dq = 0, b0 = 0;
-      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sStage));
       for (long long u = first; u < n_units; u += stride) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
-          for (int q = 0; q < C::NQ; ++q) {
+          for (int q = 0; q < C::NQ; ++q)
+          for (int t = 0; t < C::NT; ++t) {   // chunks of the unit's tiles interleaved
+            const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA + t * C::A_BYTES));
+            const uint32_t y_t = tmem + C::Y_COL + t * C::YS;
             AB_T0(td);
             if (CG == 2) mbar_wait_cluster(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
             else mbar_wait(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
@@ -320,17 +334,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             dbits ^= 1u << dq;
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
-            uint64_t* aw = q == 0 ? afull : nullptr;
+            uint64_t* aw = q == 0 ? afull + t * C::NQ : nullptr;
 #if defined(AB_EXP) && (AB_EXP & 8)
             if (false)   // timing experiment: every layer reads A from TMEM
 #else
             if (C::SPILL || src == 0)
 #endif
               // (SPILL: every layer reads A hi from X and A lo from TMEM column Y_COL)
-              mma_chunk<C, CG, false>(d_t, a_desc0, C::SPILL ? tmem + C::Y_COL : 0u, b_desc0, full, empty, aw, aph, s,
+              mma_chunk<C, CG, false>(d_t, a_desc0, C::SPILL ? y_t : 0u, b_desc0, full, empty, aw, aph, s,
                                       ph, st, u == first + 2 * stride, g, q, trace_n);
             else
-              mma_chunk<C, CG, true>(d_t, 0ull, tmem + C::Y_COL, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
+              mma_chunk<C, CG, true>(d_t, 0ull, y_t, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
             if (elect_one()) {
               if (CG == 2) umma_commit2(&dfull[dq]);
               else umma_commit(&dfull[dq]);
@@ -351,13 +365,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16);
     const long long cshard = p.c_end - p.c_begin;
-    const float* w0s = sAw + H;
-    const float* w1s = sAw + 2 * H;
+    const float* w0s = sAw + C::NT * H;
+    const float* w1s = sAw + (C::NT + 1) * H;
     // the MMA issuer's barriers live in the leader CTA: every epilogue warp of the pair counts in
     // on its own (the leader's locally, the peer's with a remote arrive), so no warp waits for the
     // other warps of its CTA
     const uint32_t dempty_c[2] = {mapa_shared(smem_u32(&dempty[0]), 0), mapa_shared(smem_u32(&dempty[1]), 0)};
-    auto my_tile = [&](long long u) { return CG == 2 ? 2 * u + rank : u; };
+    auto my_tile = [&](long long u, int t) { return (u * C::NT + t) * CG + rank; };
     auto signal = [&](uint64_t* bar, uint32_t cluster_addr) {   // called by the whole warp after __syncwarp
       if (lane == 0) {
         if (CG == 2 && !leader) mbar_arrive_remote(cluster_addr);
@@ -370,20 +384,24 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       const long long tt = tile < p.n_tiles ? tile : p.n_tiles - 1;   // ghost tile of an odd pair
       return static_cast<int>(tt / tpj);
     };
-    // job vectors of `tile` -> a slot (single) and w|beta slot `slot`, synchronously
-    auto load_vecs = [&](int slot, long long tile) {
-      const float* v = p.jobvec + (size_t)job_of(tile) * jv;
-      for (int k = etid; k < H; k += kEpiThreads) sAw[k] = v[k];
-      for (int k = etid; k < C::WV; k += kEpiThreads) sWhat[slot * C::WV + k] = v[H + k];
+    // job vectors of unit u's tiles -> their a slots and w|beta slots `slot`, synchronously
+    auto load_vecs = [&](int slot, long long u) {
+      for (int t = 0; t < C::NT; ++t) {
+        const float* v = p.jobvec + (size_t)job_of(my_tile(u, t)) * jv;
+        for (int k = etid; k < H; k += kEpiThreads) sAw[t * H + k] = v[k];
+        for (int k = etid; k < C::WV; k += kEpiThreads) sWhat[(slot * C::NT + t) * C::WV + k] = v[H + k];
+      }
     };
-    // the same, as two TMA bulk copies completing on vfull (issued by one thread)
-    auto prefetch_vecs = [&](int slot, long long tile) {
+    // the same, as TMA bulk copies completing on vfull (issued by one thread)
+    auto prefetch_vecs = [&](int slot, long long u) {
       if (etid == 0) {
-        const float* v = p.jobvec + (size_t)job_of(tile) * jv;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(vfull, (H + C::WV) * 4);
-        bulk_g2s(sAw, v, H * 4, vfull, 0ull);
-        bulk_g2s(sWhat + slot * C::WV, v + H, C::WV * 4, vfull, 0ull);
+        mbar_arrive_expect_tx(vfull, C::NT * (H + C::WV) * 4);
+        for (int t = 0; t < C::NT; ++t) {
+          const float* v = p.jobvec + (size_t)job_of(my_tile(u, t)) * jv;
+          bulk_g2s(sAw + t * H, v, H * 4, vfull, 0ull);
+          bulk_g2s(sWhat + (slot * C::NT + t) * C::WV, v + H, C::WV * 4, vfull, 0ull);
+        }
       }
     };
     // candidate index and encoding (K0) of this thread's row of `tile`
@@ -397,41 +415,42 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       uc = uu.y;
     };
     // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
-    auto store_plane = [&](int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
+    auto store_plane = [&](int t, int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
 #if defined(AB_EXP) && (AB_EXP & 4)
       if (dst == 0) return;   // timing experiment: no shared-memory activation stores
 #endif
       if (dst == 0) {  // buffer X: SW128 K-major, 16-byte chunk j of row r stored at chunk j ^ (r % 8)
-        const uint32_t rowbase = smem_u32(sA) + plane * C::A_PLANE + (c0 >> 6) * 16384 + row * 128;
+        const uint32_t rowbase = smem_u32(sA + t * C::A_BYTES) + plane * C::A_PLANE + (c0 >> 6) * 16384 + row * 128;
         const int j0 = (c0 & 63) >> 3;
 #pragma unroll
         for (int u = 0; u < C::QC / 8; ++u)
           st_shared_v4(rowbase + (((j0 + u) ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       } else {         // buffer Y: TMEM, column = element pair index
-        tmem_st_cols<C::QC / 2>(lane_base + C::Y_COL + plane * C::Y_LO + (c0 >> 1), pk);
+        tmem_st_cols<C::QC / 2>(lane_base + C::Y_COL + t * C::YS + plane * C::Y_LO + (c0 >> 1), pk);
       }
     };
     // QC post-activation values v (fp32) of this thread's row -> the A operand of the next layer:
     // bf16 (P3 = 0, values already ReLU'd) or hi/lo bf16 planes (P3 = 1)
-    auto store_vals = [&](int dst, int c0, const float (&v)[C::QC]) {
+    auto store_vals = [&](int t, int dst, int c0, const float (&v)[C::QC]) {
       uint32_t hi[C::QC / 2];
 #pragma unroll
       for (int i = 0; i < C::QC / 2; ++i) hi[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-      store_plane(dst, c0, hi, 0);
+      store_plane(t, dst, c0, hi, 0);
       if (C::NP == 2) {
         uint32_t lo[C::QC / 2];
 #pragma unroll
         for (int i = 0; i < C::QC / 2; ++i)
           lo[i] = pack_bf16x2(v[2 * i] - __uint_as_float(hi[i] << 16), v[2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
-        store_plane(dst, c0, lo, 1);
+        store_plane(t, dst, c0, lo, 1);
       }
     };
-    // make this warp's part of A-chunk q visible to the tensor core and count the warp in
-    auto publish = [&](int dst, int q) {
+    // make this warp's part of A-chunk q of tile slot t visible to the tensor core and count the warp in
+    auto publish = [&](int t, int dst, int q) {
       if (dst == 0) fence_proxy_async_smem();
       else { tmem_st_wait(); tc_fence_before(); }
       __syncwarp();
-      signal(&afull[q], CG == 2 ? mapa_shared(smem_u32(&afull[q]), 0) : 0u);
+      uint64_t* bar = &afull[t * C::NQ + q];
+      signal(bar, CG == 2 ? mapa_shared(smem_u32(bar), 0) : 0u);
     };
     // SPILL: a layer input's piece q is complete in X (hi) and TMEM (lo) for this warp
     auto publish_both = [&](int q) {
@@ -449,8 +468,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         hi[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
         lo[i] = pack_bf16x2(v[2 * i] - __uint_as_float(hi[i] << 16), v[2 * i + 1] - __uint_as_float(hi[i] & 0xFFFF0000u));
       }
-      store_plane(0, c0, hi, 0);
-      store_plane(1, c0, lo, 1);
+      store_plane(0, 0, c0, hi, 0);
+      store_plane(0, 1, c0, lo, 1);
     };
     // SPILL scratch: this thread's (row, column group) share of chunk q, hi then lo, as 2*QC/8 16-byte
     // words; word i of the warp's 32 rows is 512 contiguous bytes (one coalesced access per warp
@@ -484,31 +503,38 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         lo[4 * i] = b.x; lo[4 * i + 1] = b.y; lo[4 * i + 2] = b.z; lo[4 * i + 3] = b.w;
       }
       const int c0 = q * C::NCH + grp * C::QC;
-      store_plane(0, c0, hi, 0);
-      store_plane(1, c0, lo, 1);
+      store_plane(0, 0, c0, hi, 0);
+      store_plane(0, 1, c0, lo, 1);
     };
-    // layer-1 activations h1 = ReLU(a_j + W1c u_c) for the 128-column piece q (this warp's columns)
-    auto build_piece = [&](int q, float up, float uc, int dst) {
+    // layer-1 activations h1 = ReLU(a_j + W1c u_c) of tile slot t for the 128-column piece q (this
+    // warp's columns)
+    auto build_piece = [&](int t, int q, float up, float uc, int dst) {
       const int c0 = q * C::NCH + grp * C::QC;
+      const float* aj = sAw + t * H;
 #if defined(AB_EXP) && (AB_EXP & 17)
-      if (true) { publish(dst, q); return; }   // timing experiment: no h1 build
+      if (true) { publish(t, dst, q); return; }   // timing experiment: no h1 build
 #endif
       if (C::NP == 1) {
         uint32_t pk[C::QC / 2];
 #pragma unroll
         for (int i = 0; i < C::QC / 4; ++i) {
-          const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+          const float4 a4 = *reinterpret_cast<const float4*>(aj + c0 + 4 * i);
           const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
           const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
-          pk[2 * i] = pack_relu_bf16x2(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)), fmaf(v4.y, uc, fmaf(u4.y, up, a4.y)));
-          pk[2 * i + 1] = pack_relu_bf16x2(fmaf(v4.z, uc, fmaf(u4.z, up, a4.z)), fmaf(v4.w, uc, fmaf(u4.w, up, a4.w)));
+          // fma(w1, uc, fma(w0, up, a)) per element, two elements per FFMA2 (bit-identical)
+          const float2 h01 = ffma2(make_float2(v4.x, v4.y), make_float2(uc, uc),
+                                   ffma2(make_float2(u4.x, u4.y), make_float2(up, up), make_float2(a4.x, a4.y)));
+          const float2 h23 = ffma2(make_float2(v4.z, v4.w), make_float2(uc, uc),
+                                   ffma2(make_float2(u4.z, u4.w), make_float2(up, up), make_float2(a4.z, a4.w)));
+          pk[2 * i] = pack_relu_bf16x2(h01.x, h01.y);
+          pk[2 * i + 1] = pack_relu_bf16x2(h23.x, h23.y);
         }
-        store_plane(dst, c0, pk, 0);
+        store_plane(t, dst, c0, pk, 0);
       } else {
         float v[C::QC];
 #pragma unroll
         for (int i = 0; i < C::QC / 4; ++i) {
-          const float4 a4 = *reinterpret_cast<const float4*>(sAw + c0 + 4 * i);
+          const float4 a4 = *reinterpret_cast<const float4*>(aj + c0 + 4 * i);
           const float4 u4 = *reinterpret_cast<const float4*>(w0s + c0 + 4 * i);
           const float4 v4 = *reinterpret_cast<const float4*>(w1s + c0 + 4 * i);
           v[4 * i] = relu(fmaf(v4.x, uc, fmaf(u4.x, up, a4.x)));
@@ -521,56 +547,104 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           publish_both(q);
           return;
         } else {
-          store_vals(dst, c0, v);
+          store_vals(t, dst, c0, v);
         }
       }
-      publish(dst, q);
+      publish(t, dst, q);
+    };
+
+    // score, arg-max key and per-job reduction of tile slot t (all epilogue threads)
+    auto reduce_tile = [&](float dot, int wslot, bool real, int j, long long c) {
+      AB_T0(tr);
+      sPart[grp * kTileM + row] = dot;
+      named_bar_sync(kEpiBar, kEpiThreads);
+      if (grp == 0) {
+        float score = sPart[row];
+#pragma unroll
+        for (int i = 1; i < C::NSPLIT; ++i) score += sPart[i * kTileM + row];
+        score += sWhat[wslot * C::WV + H];
+        const bool valid = real && c < p.c_end;
+        if (valid && p.scores) p.scores[(size_t)j * cshard + (c - p.c_begin)] = score;
+        const uint32_t o = ord32(score);
+        unsigned long long key = (valid && o) ? ((static_cast<unsigned long long>(o) << 32) |
+                                                 (0xFFFFFFFFu - static_cast<uint32_t>(c)))
+                                              : 0ull;
+        if (valid && o && p.cur_idx && c == p.cur_idx[j])
+          atomicMax(p.cur_keys + j, (static_cast<unsigned long long>(o) << 32) | 1ull);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, off);
+          key = other > key ? other : key;
+        }
+        if (lane == 0) sWkey[quad] = key;
+      }
+      named_bar_sync(kEpiBar, kEpiThreads);
+      if (etid == 0 && real) {
+        unsigned long long k = sWkey[0];
+        for (int i = 1; i < 4; ++i) k = sWkey[i] > k ? sWkey[i] : k;
+        if (k) atomicMax(p.keys + j, k);
+      }
+      AB_ACC(st, 4, tr);
     };
 
     int dq = 0, b0 = 0, it = 0;
     uint32_t dbits = 0, vph = 0;
     long long u = first;
-    if (u < n_units) load_vecs(0, my_tile(u));
+    if (u < n_units) load_vecs(0, u);
     named_bar_sync(kEpiBar, kEpiThreads);
     if (G > 0 && u < n_units) {
-      float up, uc;
-      long long c;
-      row_u(my_tile(u), up, uc, c);
+      for (int t = 0; t < C::NT; ++t) {
+        float up, uc;
+        long long c;
+        row_u(my_tile(u, t), up, uc, c);
 #pragma unroll 1
-      for (int q = 0; q < C::NQ; ++q) build_piece(q, up, uc, 0);
+        for (int q = 0; q < C::NQ; ++q) build_piece(t, q, up, uc, 0);
+      }
     }
-    named_bar_sync(kEpiBar, kEpiThreads);   // every thread is done with the a-slot before it is refilled
+    named_bar_sync(kEpiBar, kEpiThreads);   // every thread is done with the a-slots before they are refilled
     for (; u < n_units; u += stride, ++it) {
       const int slot = it & 1;
-      const long long t = my_tile(u);
       const bool has_next = u + stride < n_units;
-      const long long tn = my_tile(u + stride);
-      const bool real = t < p.n_tiles;
-      const int j = static_cast<int>((real ? t : p.n_tiles - 1) / tpj);
-      float up, uc;
-      long long c;
-      row_u(t, up, uc, c);
-      float up2 = 0.f, uc2 = 0.f;
-      if (G > 0 && has_next) {
-        // h1 of tile t is complete, so the a-slot is free: fetch the next tile's job vectors now
-        prefetch_vecs(slot ^ 1, tn);
-        long long c2;
-        row_u(tn, up2, uc2, c2);
+      float up[C::NT], uc[C::NT], up2[C::NT], uc2[C::NT], dot[C::NT];
+      long long c[C::NT];
+      bool real[C::NT];
+      int j[C::NT];
+#pragma unroll
+      for (int t = 0; t < C::NT; ++t) {
+        const long long tl = my_tile(u, t);
+        real[t] = tl < p.n_tiles;
+        j[t] = static_cast<int>((real[t] ? tl : p.n_tiles - 1) / tpj);
+        row_u(tl, up[t], uc[t], c[t]);
+        up2[t] = uc2[t] = dot[t] = 0.f;
       }
-      float dot = 0.f;
+      if (G > 0 && has_next) {
+        // h1 of this unit's tiles is complete, so the a-slots are free: fetch the next unit's job vectors
+        prefetch_vecs(slot ^ 1, u + stride);
+#pragma unroll
+        for (int t = 0; t < C::NT; ++t) {
+          long long c2;
+          row_u(my_tile(u + stride, t), up2[t], uc2[t], c2);
+        }
+      }
       if (G == 0) {
-        if (it > 0) { load_vecs(slot, t); named_bar_sync(kEpiBar, kEpiThreads); }
-        const float* wv = sWhat + slot * C::WV;
-        for (int k = grp * (H / C::NSPLIT); k < (grp + 1) * (H / C::NSPLIT); ++k)
-          dot = fmaf(relu(fmaf(w1s[k], uc, fmaf(w0s[k], up, sAw[k]))), wv[k], dot);
+        if (it > 0) { load_vecs(slot, u); named_bar_sync(kEpiBar, kEpiThreads); }
+#pragma unroll 1
+        for (int t = 0; t < C::NT; ++t) {
+          const float* wv = sWhat + (slot * C::NT + t) * C::WV;
+          const float* aj = sAw + t * H;
+          float d = 0.f;
+          for (int k = grp * (H / C::NSPLIT); k < (grp + 1) * (H / C::NSPLIT); ++k)
+            d = fmaf(relu(fmaf(w1s[k], uc[t], fmaf(w0s[k], up[t], aj[k]))), wv[k], d);
+          reduce_tile(d, slot * C::NT + t, real[t], j[t], c[t]);
+        }
       }
       for (int g = 0; g < G; ++g) {
         const int src = (b0 + g) & 1, dst = src ^ 1;
         const bool last = (g == G - 1);
         const float* gbias = p.params + p.off.b[g + 2];   // beyond G_CAP layers: read through L1
         if (last && has_next) {
-          // the next tile's h1 is built one 128-column piece per chunk of this layer into the
-          // buffer this layer does not read (free once chunk 0's MMAs, so every earlier MMA, are done)
+          // the next unit's h1 is built into the buffer this layer does not read (free once chunk
+          // 0's MMAs, so every earlier MMA of the tile, are done)
           AB_T0(th);
           mbar_wait(vfull, vph);
           vph ^= 1;
@@ -596,123 +670,102 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
               bq[4 * i] = v.x; bq[4 * i + 1] = v.y; bq[4 * i + 2] = v.z; bq[4 * i + 3] = v.w;
             }
           }
-          AB_T0(tw);
-          mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
-          AB_ACC(st, 0, tw);
-          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 20 + (warp == 17) * 10, g, q);
-          AB_T0(tl);
-          dbits ^= 1u << dq;
-          tc_fence_after();
-          uint32_t acc[C::QC];
-          tmem_ld_cols<C::QC>(lane_base + dq * C::NCH + grp * C::QC, acc);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          signal(&dempty[dq], dempty_c[dq]);
-          AB_ACC(st, 1, tl);
-          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
-          AB_T0(tc);
-          dq ^= 1;
+#pragma unroll 1
+          for (int t = 0; t < C::NT; ++t) {   // the issuer's order: chunk q of every tile of the unit
+            AB_T0(tw);
+            mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
+            AB_ACC(st, 0, tw);
+            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 20 + (warp == 17) * 10, g, q);
+            AB_T0(tl);
+            dbits ^= 1u << dq;
+            tc_fence_after();
+            uint32_t acc[C::QC];
+            tmem_ld_cols<C::QC>(lane_base + dq * C::NCH + grp * C::QC, acc);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            signal(&dempty[dq], dempty_c[dq]);
+            AB_ACC(st, 1, tl);
+            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
+            AB_T0(tc);
+            dq ^= 1;
 #if defined(AB_EXP) && (AB_EXP & 1)
-          if (false)   // timing experiment: no epilogue math or activation stores
+            if (false)   // timing experiment: no epilogue math or activation stores
 #endif
-          {
-            if (!last && C::SPILL) {   // bias + ReLU in fp32 -> scratch; the last chunk refills X / TMEM
-              float v[C::QC];
+            {
+              if (!last && C::SPILL) {   // bias + ReLU in fp32 -> scratch; the last chunk refills X / TMEM
+                float v[C::QC];
 #pragma unroll
-              for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
-              if (q < C::NQ - 1) {
-                spill_store(q, v);
-              } else {
-                // this chunk's accumulator is ready, so every MMA of the layer (all readers of X and
-                // of the TMEM lo plane) has completed: this chunk's piece goes straight in (freeing
-                // its registers), then the parked pieces come back in the order the next layer reads them
-                store_split(n0, v);
-                publish_both(q);
+                for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
+                if (q < C::NQ - 1) {
+                  spill_store(q, v);
+                } else {
+                  // this chunk's accumulator is ready, so every MMA of the layer (all readers of X and
+                  // of the TMEM lo plane) has completed: this chunk's piece goes straight in (freeing
+                  // its registers), then the parked pieces come back in the order the next layer reads them
+                  store_split(n0, v);
+                  publish_both(q);
 #pragma unroll 1
-                for (int pq = 0; pq < C::NQ - 1; ++pq) {
-                  spill_reload(pq);
-                  publish_both(pq);
+                  for (int pq = 0; pq < C::NQ - 1; ++pq) {
+                    spill_reload(pq);
+                    publish_both(pq);
+                  }
                 }
-              }
-            } else if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
-              float v[C::QC];
+              } else if (!last && C::NP == 2) {   // bias + ReLU in fp32, then hi/lo split
+                float v[C::QC];
 #pragma unroll
-              for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
-              store_vals(dst, n0, v);
-            } else if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
-              uint32_t pk[C::QC / 2];
+                for (int i = 0; i < C::QC; ++i) v[i] = relu(__uint_as_float(acc[i]) + bq[i]);
+                store_vals(t, dst, n0, v);
+              } else if (!last) {   // bias + ReLU + round to bf16 (cvt.rn.relu) -> next layer's A operand
+                uint32_t pk[C::QC / 2];
 #pragma unroll
-              for (int i = 0; i < C::QC / 2; ++i)
-                pk[i] = pack_relu_bf16x2(__uint_as_float(acc[2 * i]) + bq[2 * i], __uint_as_float(acc[2 * i + 1]) + bq[2 * i + 1]);
-              store_plane(dst, n0, pk, 0);
-            } else {       // last hidden layer stays fp32: dot with the folded output row w_j (R#16)
-              const float4* w4 = reinterpret_cast<const float4*>(sWhat + slot * C::WV + n0);
-              float d4[4] = {0.f, 0.f, 0.f, 0.f};   // four independent FMA chains
+                for (int i = 0; i < C::QC / 2; ++i) {
+                  const float2 z = fadd2(make_float2(__uint_as_float(acc[2 * i]), __uint_as_float(acc[2 * i + 1])),
+                                         make_float2(bq[2 * i], bq[2 * i + 1]));
+                  pk[i] = pack_relu_bf16x2(z.x, z.y);
+                }
+                store_plane(t, dst, n0, pk, 0);
+              } else {       // last hidden layer stays fp32: dot with the folded output row w_j (R#16)
+                const float4* w4 = reinterpret_cast<const float4*>(sWhat + (slot * C::NT + t) * C::WV + n0);
+                // four independent FMA chains (element 4i+k into chain k), two per FFMA2
+                float2 d01 = make_float2(0.f, 0.f), d23 = make_float2(0.f, 0.f);
 #if defined(AB_EXP) && (AB_EXP & 32)
-              if (false)   // timing experiment: no last-layer dot
+                if (false)   // timing experiment: no last-layer dot
 #endif
 #pragma unroll
-              for (int i = 0; i < C::QC / 4; ++i) {
-                const float4 ww = w4[i];
-                d4[0] = fmaf(relu(__uint_as_float(acc[4 * i]) + bq[4 * i]), ww.x, d4[0]);
-                d4[1] = fmaf(relu(__uint_as_float(acc[4 * i + 1]) + bq[4 * i + 1]), ww.y, d4[1]);
-                d4[2] = fmaf(relu(__uint_as_float(acc[4 * i + 2]) + bq[4 * i + 2]), ww.z, d4[2]);
-                d4[3] = fmaf(relu(__uint_as_float(acc[4 * i + 3]) + bq[4 * i + 3]), ww.w, d4[3]);
+                for (int i = 0; i < C::QC / 4; ++i) {
+                  const float4 ww = w4[i];
+                  float2 z01 = fadd2(make_float2(__uint_as_float(acc[4 * i]), __uint_as_float(acc[4 * i + 1])),
+                                     make_float2(bq[4 * i], bq[4 * i + 1]));
+                  float2 z23 = fadd2(make_float2(__uint_as_float(acc[4 * i + 2]), __uint_as_float(acc[4 * i + 3])),
+                                     make_float2(bq[4 * i + 2], bq[4 * i + 3]));
+                  z01.x = relu(z01.x); z01.y = relu(z01.y); z23.x = relu(z23.x); z23.y = relu(z23.y);
+                  d01 = ffma2(z01, make_float2(ww.x, ww.y), d01);
+                  d23 = ffma2(z23, make_float2(ww.z, ww.w), d23);
+                }
+                dot[t] += (d01.x + d01.y) + (d23.x + d23.y);
               }
-              dot += (d4[0] + d4[1]) + (d4[2] + d4[3]);
             }
-          }
-          if (!last && !C::SPILL) publish(dst, q);
-          AB_ACC(st, 2, tc);
-          AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
-          // (SPILL: only once the last chunk shows the layer's MMAs done, X and TMEM are free)
-          if (last && has_next && q == (C::SPILL ? C::NQ - 1 : 0)) {
-            // the next tile's h1, all pieces at once: once this warp has seen chunk 0 of the last
-            // layer, the issuer has consumed every afull phase of this tile, so publishing the
-            // next tile's phase cannot alias; building early takes h1 off the tile boundary
-            AB_T0(th);
+            if (!last && !C::SPILL) publish(t, dst, q);
+            AB_ACC(st, 2, tc);
+            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
+            // (SPILL: only once the last chunk shows the layer's MMAs done, X and TMEM are free)
+            if (last && has_next && q == (C::SPILL ? C::NQ - 1 : 0)) {
+              // the next unit's h1 of this tile slot, all pieces at once: once this warp has seen
+              // chunk 0 of the slot's last layer, the issuer has consumed every afull phase of the
+              // slot, so publishing the next unit's phase cannot alias; building early takes h1 off
+              // the tile boundary
+              AB_T0(th);
 #pragma unroll 1
-            for (int pq = 0; pq < C::NQ; ++pq) build_piece(pq, up2, uc2, src ^ 1);
-            AB_ACC(st, 3, th);
-            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
+              for (int pq = 0; pq < C::NQ; ++pq) build_piece(t, pq, up2[t], uc2[t], src ^ 1);
+              AB_ACC(st, 3, th);
+              AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
+            }
+            if (last && q == C::NQ - 1) reduce_tile(dot[t], slot * C::NT + t, real[t], j[t], c[t]);
           }
         }
       }
       if (G > 0) b0 = ((b0 + G - 1) & 1) ^ 1;
-
-      // ------------------------------------------------ score, arg-max key, per-job reduction
-      AB_T0(tr);
-      sPart[grp * kTileM + row] = dot;
-      named_bar_sync(kEpiBar, kEpiThreads);
-      if (grp == 0) {
-        float score = sPart[row];
-#pragma unroll
-        for (int i = 1; i < C::NSPLIT; ++i) score += sPart[i * kTileM + row];
-        score += sWhat[slot * C::WV + H];
-        const bool valid = real && c < p.c_end;
-        if (valid && p.scores) p.scores[(size_t)j * cshard + (c - p.c_begin)] = score;
-        const uint32_t o = ord32(score);
-        unsigned long long key = (valid && o) ? ((static_cast<unsigned long long>(o) << 32) |
-                                                 (0xFFFFFFFFu - static_cast<uint32_t>(c)))
-                                              : 0ull;
-        if (valid && o && p.cur_idx && c == p.cur_idx[j])
-          atomicMax(p.cur_keys + j, (static_cast<unsigned long long>(o) << 32) | 1ull);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, off);
-          key = other > key ? other : key;
-        }
-        if (lane == 0) sWkey[quad] = key;
-      }
-      named_bar_sync(kEpiBar, kEpiThreads);
-      if (etid == 0 && real) {
-        unsigned long long k = sWkey[0];
-        for (int i = 1; i < 4; ++i) k = sWkey[i] > k ? sWkey[i] : k;
-        if (k) atomicMax(p.keys + j, k);
-      }
-      AB_ACC(st, 4, tr);
-      AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 24 + (warp == 17) * 10, 0, 0);
     }
   }
 #ifdef AB_STATS
@@ -753,7 +806,7 @@ static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream
     if (e != cudaSuccess) return e;
     attr_done |= 1ull << (dev & 63);
   }
-  const long long units = CG == 2 ? (p.n_tiles + 1) / 2 : p.n_tiles;
+  const long long units = (p.n_tiles + CG * C::NT - 1) / (CG * C::NT);   // as score_kernel's n_units
   const long long max_units = num_sms / CG;
   const long long grid = (units < max_units ? units : max_units) * CG;
   if (grid < 1) return cudaSuccess;
