@@ -15,7 +15,7 @@ from paper_2112_13509_b200.build import STATS_LIB  # noqa: E402
 
 NAMES = ["prod.wait_empty", "prod.total", "mma.wait_dempty", "mma.wait_full", "mma.wait_afull", "mma.total",
          "epi.wait_dfull", "epi.ld", "epi.compute_store", "epi.build_h1", "epi.tile_reduce", "epi.total",
-         "peer.epi.wait_dfull", "peer.epi.ld", "peer.epi.compute_store", "peer.epi.build_h1"]
+         "peer.epi.wait_dfull", "peer.epi.ld", "peer.epi.compute_store", "peer.epi.build_h1", "epi.wait_vfull"]
 
 
 def main():
@@ -26,7 +26,7 @@ def main():
     lib = ab.load_library(os.environ.get("AUTOBYTE_LIB") or STATS_LIB)
     fn = lib.ab_debug_stats
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 20)()
     jobs = ab.DeviceJobs.from_host(synth.small_fleet(J, 1))
     grid = ab.DeviceGrid.from_host(synth.log_grid(64, 64))
     for cg in ((1, 2) if prec == "bf16" else ((2,) if H == 512 else (1,))):
