@@ -115,7 +115,8 @@ struct autobyte_ctx {
   DevBuf<float> enc_stash, enc_dz, enc_part;   // encoder fine-tuning: K1a stash, dX [B][84], K8 partials
   DevBuf<unsigned long long> topk_keys;   // [G][J][k] per-rank top-k keys
   long long opt_t = 0;               // Adam step count
-  DevBuf<float2> u;                  // [shard] candidate encodings (K0)
+  DevBuf<float> u;                   // [P + Q] candidate-grid axes u_p | u_c (K1b / K1s / K0)
+  DevBuf<unsigned int> done;         // K2's CTA completion counter (K5 folded into K2 at G = 1)
   DevBuf<unsigned long long> keys;   // [2J]: best keys then current-config keys
   DevBuf<unsigned long long> keys_all;   // [G][2J]: every rank's keys (all-gather exchange)
   bool exchange_allreduce = false;   // AUTOBYTE_EXCHANGE=allreduce: ncclAllReduce(max) instead
@@ -312,7 +313,11 @@ bool encode_range(const autobyte_ctx* c, int J, int* jb, int* je) {
   return shard;
 }
 
-autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, EncodeParams* out) {
+// proj (nullable): K1b's outputs; when the unsharded call runs K1s, K1s computes them too and
+// *projected is set (the caller then skips K1b).
+autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, EncodeParams* out,
+                         const EncodeParams* proj = nullptr, bool* projected = nullptr) {
+  if (projected) *projected = false;
   const int J = jobs->J;
   int jb = 0, je = J;
   const bool shard = encode_range(c, J, &jb, &je);
@@ -349,8 +354,17 @@ autobyte_status run_lstm(autobyte_ctx* c, const autobyte_job_stats* jobs, Encode
     *out = ep;
     return AB_OK;
   }
-  if (ep.j_end > ep.j_begin)
-    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(ep, c->num_sms, c->stream); }));
+  if (ep.j_end > ep.j_begin) {
+    EncodeParams lp = ep;
+    if (proj && !shard) {   // one kernel for the whole job prologue when K1s runs (few jobs, one rank)
+      lp.jv = proj->jv; lp.a_out = proj->a_out; lp.what_out = proj->what_out; lp.beta_out = proj->beta_out;
+      lp.keys = proj->keys; lp.cur_keys = proj->cur_keys;
+      lp.P = proj->P; lp.Q = proj->Q; lp.S_p = proj->S_p; lp.S_c = proj->S_c;
+      lp.up_out = proj->up_out; lp.uc_out = proj->uc_out;
+      lp.fuse_project = 1;
+    }
+    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_lstm(lp, c->num_sms, c->stream, projected); }));
+  }
   if (shard) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->profiling) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, c->stream); }
@@ -483,22 +497,41 @@ size_t staged_job_bytes(const autobyte_ctx* c, int J, int l_max) {
 }
 
 autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* jobs, const autobyte_grid* grid,
-                                     const int32_t* cur_idx, float* scores) {
+                                     const int32_t* cur_idx, float* scores, int32_t* best_idx = nullptr,
+                                     float* best_score = nullptr, float* cur_score = nullptr,
+                                     bool* finalized = nullptr) {
+  if (finalized) *finalized = false;
   const int J = jobs->J;
   autobyte_status st = ensure_job_ws(c, J);
   if (st != AB_OK) return st;
-  EncodeParams ep{};
-  if ((st = run_lstm(c, jobs, &ep)) != AB_OK) return st;
   const int H = c->desc.hidden_width;
-  ep.jv = 2 * H + 4;
-  ep.a_out = c->jobvec.ptr; ep.what_out = c->jobvec.ptr + H; ep.beta_out = c->jobvec.ptr + 2 * H;
-  ep.keys = c->keys.ptr; ep.cur_keys = c->keys.ptr + J;
-  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_project(ep, c->stream); }));
   const long long cs = grid->shard_end - grid->shard_begin;
+  // K1b's outputs and the grid axes (a-1): up[P] | uc[Q]
+  EncodeParams proj{};
+  proj.jv = 2 * H + 4;
+  proj.a_out = c->jobvec.ptr; proj.what_out = c->jobvec.ptr + H; proj.beta_out = c->jobvec.ptr + 2 * H;
+  proj.keys = c->keys.ptr; proj.cur_keys = c->keys.ptr + J;
+  proj.P = grid->P; proj.Q = grid->Q;
+  proj.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); proj.S_c = grid->credit_mult;
+  if (cs > 0) {
+    AB_CUDA(c, c->u.ensure((size_t)grid->P + grid->Q));
+    proj.up_out = c->u.ptr; proj.uc_out = c->u.ptr + grid->P;
+  }
+  EncodeParams ep{};
+  bool projected = false;
+  if ((st = run_lstm(c, jobs, &ep, &proj, &projected)) != AB_OK) return st;
+  if (!projected) {
+    ep.jv = proj.jv; ep.a_out = proj.a_out; ep.what_out = proj.what_out; ep.beta_out = proj.beta_out;
+    ep.keys = proj.keys; ep.cur_keys = proj.cur_keys;
+    ep.P = proj.P; ep.Q = proj.Q; ep.S_p = proj.S_p; ep.S_c = proj.S_c;
+    ep.up_out = proj.up_out; ep.uc_out = proj.uc_out;
+    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_project(ep, c->stream); }));
+  }
   if (cs == 0) return AB_OK;   // empty shard of a multi-rank partition: the keys stay 0 (K1b reset them)
-  // K0: candidate encodings u_c of this shard (§8(a) a-1), 8 bytes per candidate
-  AB_CUDA(c, c->u.ensure((size_t)cs));
-  AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_encode_grid(*grid, c->u.ptr, c->stream); }));
+  if ((long long)grid->P + grid->Q > kFusedAxes) {   // K0: large axes get their own launch
+    EncodeParams ap = proj;
+    AB_CUDA(c, timed(c, K_ENCODE, [&] { return launch_grid_axes(ap, c->stream); }));
+  }
 
   ScoreParams sp{};
   sp.J = J; sp.H = c->desc.hidden_width; sp.G = c->desc.hidden_layers - 1;
@@ -509,7 +542,7 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); sp.S_c = grid->credit_mult;
   sp.params = c->params.ptr; sp.off = c->off;
   sp.jobvec = c->jobvec.ptr;
-  sp.u = c->u.ptr;
+  sp.up = c->u.ptr; sp.uc = c->u.ptr + grid->P;
   sp.wpack = c->wpack.ptr;
   sp.wmap = c->wmap;
   sp.cta_group = c->planes == 2 ? (c->desc.hidden_width == 512 ? 2 : 1) : c->cta_group;
@@ -517,6 +550,12 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.precision3 = c->planes == 2 ? 1 : 0;
   sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
   sp.cur_idx = cur_idx; sp.scores = scores;
+  if (best_idx && !(c->comm && c->world > 1)) {   // single rank: K2's last CTA decodes the keys
+    sp.finalize = 1;
+    sp.done = c->done.ptr;
+    sp.best_idx = best_idx; sp.best_score = best_score; sp.cur_score = cur_score;
+    if (finalized) *finalized = true;
+  }
   AB_CUDA(c, timed(c, K_SCORE, [&] { return launch_score(sp, c->num_sms, c->stream); }));
   c->score_pairs += (double)J * (double)cs;
   return AB_OK;
@@ -652,6 +691,8 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
   const size_t wp = packed_weight_elems(desc->hidden_width, desc->hidden_layers, c->planes);
   if ((e = c->wpack.ensure(wp ? wp * kWeightReplicas : 1)) != cudaSuccess) return bail(e, "alloc wpack");
   if ((e = c->barrier.ensure(2)) != cudaSuccess) return bail(e, "alloc barrier");
+  if ((e = c->done.ensure(1)) != cudaSuccess) return bail(e, "alloc done counter");
+  if ((e = cudaMemsetAsync(c->done.ptr, 0, sizeof(unsigned int), c->stream)) != cudaSuccess) return bail(e, "memset done");
   // K2 variant: CTA pairs win when the head is deep and wide (4x512: 1158 vs 1133 TFLOP/s),
   // CTA pairs win from H = 256 up (C4 4x512: 1416 vs 1119 TFLOP/s; 3x256: 808 vs 757); single
   // CTAs on the narrow heads (3x128: 320 vs 314). AUTOBYTE_CTA_GROUP=1|2 overrides.
@@ -691,7 +732,7 @@ void autobyte_destroy(autobyte_ctx* c) {
   close_peer_window(c);
   if (c->comm) ncclCommDestroy(c->comm);
   c->params.release(); c->grads.release(); c->wpack.release(); c->spill.release(); c->barrier.release(); c->flag.release();
-  c->jobvec.release(); c->u.release(); c->x.release(); c->adapt_ws.release();
+  c->jobvec.release(); c->u.release(); c->done.release(); c->x.release(); c->adapt_ws.release();
   c->opt_m.release(); c->opt_v.release(); c->topk_scores.release(); c->topk_keys.release();
   c->enc_stash.release(); c->enc_dz.release(); c->enc_part.release();
   c->loss_tmp.release(); c->keys.release();
@@ -789,8 +830,11 @@ autobyte_status autobyte_argmax(autobyte_ctx* c, const autobyte_job_stats* jobs,
   if (!best_idx || !best_score) return fail(c, AB_E_INVALID, "best_idx / best_score is NULL");
   DeviceGuard guard(c->device);
   if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
-  if ((s = run_encode_and_score(c, jobs, grid, cur_idx, nullptr)) != AB_OK) return s;
+  bool finalized = false;
+  if ((s = run_encode_and_score(c, jobs, grid, cur_idx, nullptr, best_idx, best_score, cur_score, &finalized)) != AB_OK)
+    return s;
   const int J = jobs->J;
+  if (finalized) return AB_OK;   // one rank: K2's last CTA already decoded the keys (K5 folded in)
   // K3 (§8(a) a-7): the per-rank (score, index) keys are all-gathered over NVLink (one pass; the
   // per-job max is folded into K5), or with AUTOBYTE_EXCHANGE=allreduce reduced by ncclAllReduce(max)
   const unsigned long long* kin = c->keys.ptr;

@@ -14,6 +14,9 @@
 //   w_j = (1/n) sum_{w<n} W_o[w]  (worker-mean fold of the output layer, R#3)
 //   beta_j = (1/n) sum_{w<n} b_o[w], and resets the job's arg-max keys.
 // This is SIMT work (~1.6 MFLOP per job, 0.03% of C4).
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -363,6 +366,45 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(const __grid_consta
 constexpr int kProjJobs = 32;
 constexpr int kProjThreads = 256;
 
+// Candidate-grid axes (a-1; R#8): u_p[p] = (log2 S_p - 21) / 8 and
+// u_c[q] = (S_c - 8.5) / 8 in double, rounded once to fp32; K2 reads u_c = (up[c / Q], uc[c % Q]).
+__device__ void grid_axes(const EncodeParams& p, long long first, long long stride) {
+  for (long long i = first; i < (long long)p.P + p.Q; i += stride) {
+    if (i < p.P) p.up_out[i] = static_cast<float>((log2(static_cast<double>(p.S_p[i])) - 21.0) / 8.0);
+    else p.uc_out[i - p.P] = static_cast<float>((static_cast<double>(p.S_c[i - p.P]) - 8.5) / 8.0);
+  }
+}
+
+// K1b's per-job outputs for ONE job j whose x row is xs (shared memory), by `nthreads` threads:
+// the operations of project_kernel for that job in the same order (bit-identical): a[c] = (sum_k
+// fma(W1[c][k], x[k]) from 0) + b1[c]; w[c] = sum_w fma(W_o[w][c], m[w]) from 0, m = 1/n on valid
+// workers; beta = (sum_{w<n} b_o[w]) / n; keys reset.
+__device__ void project_one(const EncodeParams& p, int j, const float* xs, int tid, int nthreads) {
+  const float* P = p.params;
+  const int H = p.H, n = p.n[j];
+  if (tid == 0) {
+    if (p.beta_out) {
+      float acc = 0.f;
+      for (int w = 0; w < n; ++w) acc += P[p.off.b_o + w];
+      p.beta_out[(size_t)j * p.jv] = acc / static_cast<float>(n);
+    }
+    if (p.keys) p.keys[j] = 0ull;
+    if (p.cur_keys) p.cur_keys[j] = 0ull;
+  }
+  const float inv_n = 1.0f / static_cast<float>(n);
+  for (int col = tid; col < H; col += nthreads) {
+    const float* wr = P + p.off.W[1] + (size_t)col * kZDim;
+    float acc = 0.f;
+#pragma unroll 2
+    for (int k = 0; k < kXDim; ++k) acc = fmaf(wr[k], xs[k], acc);
+    p.a_out[(size_t)j * p.jv + col] = acc + P[p.off.b[1] + col];
+    float aw = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kNMax; ++ww) aw = fmaf(P[p.off.W_o + (size_t)ww * H + col], ww < n ? inv_n : 0.f, aw);
+    p.what_out[(size_t)j * p.jv + col] = aw;
+  }
+}
+
 __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_constant__ EncodeParams p) {
   __shared__ __align__(16) float sXt[kXDim][kProjJobs];    // transposed: 4 jobs per LDS.128
   __shared__ __align__(16) float sM[kNMax][kProjJobs];     // mask / n
@@ -378,6 +420,8 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const __grid_cons
     const int nj = (jj < jn) ? p.n[j0 + jj] : 1;
     sM[w][jj] = w < nj ? 1.0f / static_cast<float>(nj) : 0.f;
   }
+  if (p.up_out && (long long)p.P + p.Q <= kFusedAxes) grid_axes(p, (long long)blockIdx.x * kProjThreads + tid,
+                                                                   (long long)gridDim.x * kProjThreads);
   if (tid < jn) {
     const int j = j0 + tid, n = p.n[j];
     if (p.beta_out) {
@@ -471,10 +515,190 @@ int encode_jobs_per_half(int n, int num_sms) {
   return hj < 1 ? 1 : (hj > 16 ? 16 : hj);
 }
 
+// ---------------------------------------------------------------- K1s: latency encoder
+// One job per 256-thread CTA, for calls with few jobs (the paper's per-job use, PAPER.md:342,
+// :539-540: one job scored at a time). Warps 0-3 hold layer 1, warps 4-7 layer 2; lane 4k + gate of
+// a warp owns gate row `gate` of unit 8*(warp % 4) + k, weights in registers, so the four gates of a
+// cell sit in four adjacent lanes: a step is one gate row per thread (K1a's four accumulation
+// chains, bias on chain 0, then (a0 + a1) + (a2 + a3)), three shuffles, K1a's cell update on the
+// gate-0 lane, and ONE __syncthreads (h1 / h2 double-buffered by step parity) instead of K1a's two.
+// Same operations in the same order as K1a, so x is bit-identical (tested): the kernel choice never
+// changes a result. Embeddings e_i are formed 64 layers at a time.
+constexpr int kLatThreads = 256;
+constexpr int kLatChunk = 64;   // layers of T staged per chunk
+
+__global__ void __launch_bounds__(kLatThreads, 1) encode_latency_kernel(const __grid_constant__ EncodeParams p) {
+  __shared__ __align__(16) float sT[kLatChunk][kNMax];      // t' of the chunk
+  __shared__ __align__(16) float sE[kLatChunk][kEmbed];     // e_i of the chunk
+  __shared__ __align__(16) float sH1[2][kLstm];             // h1 by step parity
+  __shared__ __align__(16) float sH2[2][kLstm];             // h2 by step parity
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = p.j_begin + blockIdx.x;
+  const float* P = p.params;
+  const int n = p.n[j], l = p.l[j];
+  const bool l2 = warp >= 4;
+  const int u = (warp & 3) * 8 + (lane >> 2), gate = lane & 3;
+  const int g = gate * kLstm + u;                   // gate row of this thread's layer
+  float wx[kLstm], wh[kLstm];                       // layer 1: wx[0..15] = W_x row (over e)
+  {
+    const float4* a = reinterpret_cast<const float4*>(P + (l2 ? p.off.l2Wx + g * kLstm : p.off.l1Wx + g * kEmbed));
+    const float4* b = reinterpret_cast<const float4*>(P + (l2 ? p.off.l2Wh : p.off.l1Wh) + g * kLstm);
+    const bool al = ((p.off.l1Wx | p.off.l1Wh | p.off.l2Wx | p.off.l2Wh) & 3) == 0;
+#pragma unroll
+    for (int q = 0; q < kLstm / 4; ++q) {
+      if (q < kEmbed / 4 || l2) {
+        const float4 v = al ? __ldg(a + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        wx[4 * q] = v.x; wx[4 * q + 1] = v.y; wx[4 * q + 2] = v.z; wx[4 * q + 3] = v.w;
+      } else {
+        wx[4 * q] = wx[4 * q + 1] = wx[4 * q + 2] = wx[4 * q + 3] = 0.f;
+      }
+      const float4 w = al ? __ldg(b + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      wh[4 * q] = w.x; wh[4 * q + 1] = w.y; wh[4 * q + 2] = w.z; wh[4 * q + 3] = w.w;
+    }
+    if (!al) {   // (unaligned blob offsets: scalar loads)
+#pragma unroll
+      for (int d = 0; d < kLstm; ++d) {
+        wx[d] = l2 ? P[p.off.l2Wx + g * kLstm + d] : (d < kEmbed ? P[p.off.l1Wx + g * kEmbed + d] : 0.f);
+        wh[d] = P[(l2 ? p.off.l2Wh : p.off.l1Wh) + g * kLstm + d];
+      }
+    }
+  }
+  const float bias = P[(l2 ? p.off.l2b : p.off.l1b) + g];
+  // embedding outputs e[i][ed] for i = ei + 16 r (r < 4) of each chunk, W_e row ed in registers
+  const int ed = tid & (kEmbed - 1), ei = tid >> 4;
+  float we[kNMax];
+#pragma unroll
+  for (int w = 0; w < kNMax; ++w) we[w] = P[p.off.W_e + ed * kNMax + w];
+  const float be = P[p.off.b_e + ed];
+  if (tid < 2 * kLstm) {
+    (&sH1[0][0])[tid] = 0.f;
+    (&sH2[0][0])[tid] = 0.f;
+  }
+  float cst = 0.f;
+  for (int i0 = 0; i0 <= l; i0 += kLatChunk) {
+    const int len = min(kLatChunk, l - i0);
+    // t'_i[w] = log2(1 + T[i][w] / 1 ms) on valid workers, 0 on padding (R#7, R#8)
+#pragma unroll
+    for (int r = 0; r < kLatChunk * kNMax / kLatThreads; ++r) {
+      const int e = tid + r * kLatThreads, i = e >> 4, w = e & 15;
+      float v = 0.f;
+      if (i < len && w < n) v = log2f(1.0f + p.T[((size_t)j * p.l_max + i0 + i) * kNMax + w]);
+      sT[i][w] = v;
+    }
+    __syncthreads();
+    // e_i = W_e t'_i + b_e (R#4), the accumulation order of K1a
+#pragma unroll
+    for (int r = 0; r < kLatChunk * kEmbed / kLatThreads; ++r) {
+      const int i = ei + 16 * r;
+      if (i < len) {
+        float acc = be;
+#pragma unroll
+        for (int w = 0; w < kNMax; ++w) acc = fmaf(we[w], sT[i][w], acc);
+        sE[i][ed] = acc;
+      }
+    }
+    __syncthreads();
+    // wavefront: layer 1 at step t, layer 2 at step t - 1 (one past the last step for layer 2)
+    const int iend = i0 + kLatChunk > l ? l - i0 + 1 : kLatChunk;
+    for (int i = 0; i < iend; ++i) {
+      const int t = i0 + i;
+      const int step = l2 ? t - 1 : t;
+      const bool active = step >= 0 && step < l;
+      const int rd = (t & 1) ^ 1, wr = t & 1;       // h(t-1) / h(t-2) read, h written
+      float a0 = bias, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if (active) {
+        if (!l2) {
+          const float4* e4 = reinterpret_cast<const float4*>(sE[i]);
+          const float4* h4 = reinterpret_cast<const float4*>(sH1[rd]);
+#pragma unroll
+          for (int q = 0; q < kEmbed / 4; ++q) {
+            const float4 v = e4[q];
+            a0 = fmaf(wx[4 * q], v.x, a0); a1 = fmaf(wx[4 * q + 1], v.y, a1);
+            a2 = fmaf(wx[4 * q + 2], v.z, a2); a3 = fmaf(wx[4 * q + 3], v.w, a3);
+          }
+#pragma unroll
+          for (int q = 0; q < kLstm / 4; ++q) {
+            const float4 v = h4[q];
+            a0 = fmaf(wh[4 * q], v.x, a0); a1 = fmaf(wh[4 * q + 1], v.y, a1);
+            a2 = fmaf(wh[4 * q + 2], v.z, a2); a3 = fmaf(wh[4 * q + 3], v.w, a3);
+          }
+        } else {
+          const float4* x4 = reinterpret_cast<const float4*>(sH1[rd]);
+          const float4* h4 = reinterpret_cast<const float4*>(sH2[rd]);
+#pragma unroll
+          for (int q = 0; q < kLstm / 4; ++q) {
+            const float4 v = x4[q], w = h4[q];
+            a0 = fmaf(wx[4 * q], v.x, a0); a1 = fmaf(wx[4 * q + 1], v.y, a1);
+            a2 = fmaf(wx[4 * q + 2], v.z, a2); a3 = fmaf(wx[4 * q + 3], v.w, a3);
+            a0 = fmaf(wh[4 * q], w.x, a0); a1 = fmaf(wh[4 * q + 1], w.y, a1);
+            a2 = fmaf(wh[4 * q + 2], w.z, a2); a3 = fmaf(wh[4 * q + 3], w.w, a3);
+          }
+        }
+      }
+      const float z = (a0 + a1) + (a2 + a3);
+      const int base = lane & ~3;
+      const float zf = __shfl_sync(0xffffffffu, z, base + 1);
+      const float zg = __shfl_sync(0xffffffffu, z, base + 2);
+      const float zo = __shfl_sync(0xffffffffu, z, base + 3);
+      if (gate == 0) {
+        if (active) {
+          const float ig = sigmoidf_acc(z), fg = sigmoidf_acc(zf), gg = tanh_acc(zg), og = sigmoidf_acc(zo);
+          cst = fmaf(fg, cst, ig * gg);
+          (l2 ? sH2 : sH1)[wr][u] = og * tanh_acc(cst);
+        } else if (step >= l) {
+          (l2 ? sH2 : sH1)[wr][u] = (l2 ? sH2 : sH1)[rd][u];   // frozen after the job's last layer
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- feature vector x_j (Table 2; R#6-R#8): the top layer's h after its last step
+  __shared__ __align__(16) float sX[kXDim + 2];
+  const int hfin = l & 1;   // layer 2's step l - 1 ran at t = l, written to parity l & 1
+  if (tid < kXDim) {
+    const int i = tid;
+    float v;
+    if (i < kLstm) v = sH2[hfin][i];
+    else if (i < kLstm + kNMax) v = (i - kLstm) < n ? log2f(p.B_d[(size_t)j * kNMax + i - kLstm]) : 0.f;
+    else if (i < kLstm + 2 * kNMax) v = (i - kLstm - kNMax) < n ? log2f(p.B_u[(size_t)j * kNMax + i - kLstm - kNMax]) : 0.f;
+    else if (i == kLstm + 2 * kNMax) v = static_cast<float>(n) / 16.0f;
+    else if (i == kLstm + 2 * kNMax + 1) v = static_cast<float>(l) / 64.0f;
+    else if (i < kLstm + 2 * kNMax + 2 + kTypeEmbed) v = P[p.off.E_m + p.m[j] * kTypeEmbed + (i - kLstm - 2 * kNMax - 2)];
+    else v = P[p.off.E_arc + p.arc[j] * kTypeEmbed + (i - kLstm - 2 * kNMax - 2 - kTypeEmbed)];
+    p.x_out[(size_t)j * kXDim + i] = v;
+    sX[i] = v;
+  }
+  if (p.fuse_project) {   // K1b's work for this job (and the grid axes once), no extra launch
+    __syncthreads();
+    project_one(p, j, sX, tid, kLatThreads);
+    if (p.up_out && blockIdx.x == 0 && (long long)p.P + p.Q <= kFusedAxes) grid_axes(p, tid, kLatThreads);
+  }
+}
+
+// AUTOBYTE_ENCODER=batched|latency forces K1a / K1s (tests); default: K1s when the call has at most
+// one job per SM (and no stash / fused gather, which only K1a implements).
+int encoder_choice() {
+  const char* e = std::getenv("AUTOBYTE_ENCODER");
+  return (e && std::strcmp(e, "batched") == 0) ? 1 : (e && std::strcmp(e, "latency") == 0) ? 2 : 0;
+}
+
 // K1a over jobs [p.j_begin, p.j_end): writes rows of p.x_out (global job index).
-cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s) {
+cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s, bool* projected) {
+  if (projected) *projected = false;
   // (an empty range still launches one CTA when its flag must be raised for the x all-gather)
   if (p.j_end <= p.j_begin && p.xG <= 1) return cudaSuccess;
+  const int nj = p.j_end - p.j_begin;
+  const int ch = encoder_choice();
+  if (p.stash == nullptr && p.xG <= 1 && ch != 1 && (ch == 2 || nj <= num_sms)) {
+    encode_latency_kernel<<<nj, kLatThreads, 0, s>>>(p);
+    if (projected) *projected = p.fuse_project != 0;
+    return cudaGetLastError();
+  }
+  if (p.fuse_project) {   // K1a does not project: the caller runs K1b
+    EncodeParams q = p;
+    q.fuse_project = 0;
+    return launch_encode_lstm(q, num_sms, s, projected);
+  }
   switch (encode_jobs_per_half(p.j_end - p.j_begin, num_sms)) {
     case 1: return launch_lstm_hj<1>(p, s);
     case 2: return launch_lstm_hj<2>(p, s);
@@ -502,24 +726,16 @@ cudaError_t launch_project(const EncodeParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- K0: candidate encodings
-// u_c = ((log2 S_p - 21) / 8, (S_c - 8.5) / 8) for c = p*Q + q in [shard_begin, shard_end)
-// (R#8), computed in double and rounded once to fp32.
-__global__ void encode_grid_kernel(int Q, long long c0, long long n, const long long* __restrict__ S_p,
-                                   const float* __restrict__ S_c, float2* __restrict__ u) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long c = c0 + i;
-    const long long pi = c / Q, qi = c % Q;
-    u[i] = make_float2(static_cast<float>((log2(static_cast<double>(S_p[pi])) - 21.0) / 8.0),
-                       static_cast<float>((static_cast<double>(S_c[qi]) - 8.5) / 8.0));
-  }
+// ---------------------------------------------------------------- K0: candidate-grid axes
+// Only for grids with P + Q > kFusedAxes (otherwise K1b / K1s form the axes in their epilogue).
+__global__ void grid_axes_kernel(const __grid_constant__ EncodeParams p) {
+  grid_axes(p, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
-cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s) {
-  const long long n = g.shard_end - g.shard_begin;
+cudaError_t launch_grid_axes(const EncodeParams& p, cudaStream_t s) {
+  const long long n = (long long)p.P + p.Q;
   const long long blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
-  encode_grid_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
-      g.Q, g.shard_begin, n, reinterpret_cast<const long long*>(g.partition_bytes), g.credit_mult, u);
+  grid_axes_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -55,6 +55,12 @@ struct EncodeParams {
   unsigned long long* keys;      // [J] reset to 0, or null
   unsigned long long* cur_keys;  // [J] reset to 0, or null
   float* stash;        // [J][l_max][kEncStash] forward states for encoder fine-tuning, or null
+  // candidate-grid axes (a-1, R#8), formed by K1b (or K1s when it projects) when up_out != null:
+  // up_out[p] = (log2 S_p[p] - 21) / 8, uc_out[q] = (S_c[q] - 8.5) / 8, in double, rounded once
+  int P, Q;
+  const long long* S_p; const float* S_c;
+  float* up_out; float* uc_out;
+  int fuse_project;    // K1s: also K1b's per-job projections (a, w, beta, key reset) for its jobs
   // G > 1 with the peer-memory window: K1a also stores its x rows into every rank's window
   // (xg[r], row j at xg[r] + j*82; xg[rank] == x_out) and its last CTA raises xflag[r][rank] = epoch
   int xG, xrank;
@@ -78,13 +84,18 @@ struct alignas(64) ScoreParams {
   const float* params;          // fp32 masters (W1's u-columns, biases)
   ParamOffsets off;
   const float* jobvec;          // [J][2H+4]: a_j | w_j | beta_j, 0, 0, 0  (K1)
-  const float2* u;              // [c_end - c_begin] candidate encodings (K0)
+  const float* up;              // [P] partition-size encodings (R#8; K1b / K1s)
+  const float* uc;              // [Q] credit-size encodings
   const __nv_bfloat16* wpack;   // packed bf16 W_2..W_L (see pack_weights)
   unsigned long long* keys;     // [J]
   unsigned long long* cur_keys; // [J]
   const int32_t* cur_idx;       // [J] or null
   float* scores;                // [J][c_end - c_begin] or null
   uint32_t* spill;              // fp32 path at H = 512: [grid][128][spill_u32] activation scratch
+  // single-rank argmax: the last CTA to finish decodes the keys (K5 folded into K2)
+  int finalize;
+  unsigned int* done;           // CTA completion counter (zero between calls)
+  int32_t* best_idx; float* best_score; float* cur_score;
 };
 
 struct AdaptParams {
@@ -114,10 +125,12 @@ struct AdaptParams {
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)
-cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s);   // K1a
+// K1a / K1s; *projected = true when K1s also did K1b's work (p.fuse_project and the latency kernel ran)
+cudaError_t launch_encode_lstm(const EncodeParams& p, int num_sms, cudaStream_t s, bool* projected = nullptr);
 cudaError_t launch_project(const EncodeParams& p, cudaStream_t s);                    // K1b
 cudaError_t launch_score(const ScoreParams& p, int num_sms, cudaStream_t s);
-cudaError_t launch_encode_grid(const autobyte_grid& g, float2* u, cudaStream_t s);
+cudaError_t launch_grid_axes(const EncodeParams& p, cudaStream_t s);   // K0: only when P + Q is large
+constexpr int kFusedAxes = 8192;   // P + Q up to this: the axes are formed inside K1b / K1s
 cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_score, const int32_t* cur_idx,
                            const float* cur_score, const float* v_obs, float gain, float drift, int32_t* action,
                            cudaStream_t s);

@@ -410,9 +410,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       const int ct = static_cast<int>(tt % tpj);
       c = p.c_begin + (long long)ct * kTileM + row;
       const long long cc = c < p.c_end ? c : p.c_end - 1;
-      const float2 uu = p.u[cc - p.c_begin];
-      up = uu.x;
-      uc = uu.y;
+      // u_c = (u_p[c / Q], u_c[c % Q]) (a-1, R#8; axes from K1b / K1s); C < 2^31, so 32-bit division
+      const uint32_t ci = static_cast<uint32_t>(cc), qn = static_cast<uint32_t>(p.Q);
+      const uint32_t pi = ci / qn;
+      up = p.up[pi];
+      uc = p.uc[ci - pi * qn];
     };
     // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
     auto store_plane = [&](int t, int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
@@ -616,7 +618,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         const long long tl = my_tile(u, t);
         real[t] = tl < p.n_tiles;
         j[t] = static_cast<int>((real[t] ? tl : p.n_tiles - 1) / tpj);
-        row_u(tl, up[t], uc[t], c[t]);
+        // this tile's candidate index (its h1 was built earlier; only the G = 0 path reads u here)
+        const int ct = static_cast<int>((real[t] ? tl : p.n_tiles - 1) % tpj);
+        c[t] = p.c_begin + (long long)ct * kTileM + row;
+        up[t] = uc[t] = 0.f;
+        if (G == 0) row_u(tl, up[t], uc[t], c[t]);
         up2[t] = uc2[t] = dot[t] = 0.f;
       }
       if (G > 0 && has_next) {
@@ -795,6 +801,34 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     if (CG == 2) tmem_dealloc2(tmem, C::TMEM_COLS);
     else tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  if (p.finalize) {
+    // K5 folded in (single rank): the last CTA to finish decodes every job's keys. Each CTA's
+    // atomicMax updates happen before its fence + count; the last CTA reads the keys past L1.
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int j = threadIdx.x; j < p.J; j += blockDim.x) {
+        const unsigned long long k = __ldcg(p.keys + j);
+        if (k == 0ull) {
+          p.best_idx[j] = -1;
+          p.best_score[j] = __uint_as_float(0x7FC00000u);
+        } else {
+          p.best_idx[j] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFull));
+          p.best_score[j] = unord32(static_cast<uint32_t>(k >> 32));
+        }
+        if (p.cur_score) {
+          const unsigned long long ck = __ldcg(p.cur_keys + j);
+          p.cur_score[j] = ck ? unord32(static_cast<uint32_t>(ck >> 32)) : __uint_as_float(0x7FC00000u);
+        }
+      }
+      if (threadIdx.x == 0) *p.done = 0u;   // the next launch (stream-ordered) counts from zero
+    }
+  }
 }
 
 template <int H, int CG, int P3>
@@ -812,7 +846,7 @@ static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream
   const long long units = (p.n_tiles + CG * C::NT - 1) / (CG * C::NT);   // as score_kernel's n_units
   const long long max_units = num_sms / CG;
   const long long grid = (units < max_units ? units : max_units) * CG;
-  if (grid < 1) return cudaSuccess;
+  if (grid < 1) return cudaSuccess;   // (the caller only sets finalize when there is a tile)
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kScoreThreads);

@@ -382,3 +382,33 @@ def test_train_epoch_learns_a_teacher():
     last_epoch = losses[-(N // batch):].mean()
     assert np.all(np.isfinite(losses)) and last_epoch < losses[0] / 5, (losses[0], last_epoch)
     print(f"teacher fit: loss {losses[0]:.4f} -> {last_epoch:.4f} over {len(losses)} steps")
+
+
+# ------------------------------------------------------------------------------------- K1s latency encoder
+@pytest.mark.parametrize("J,lmax", [(1, 54), (7, 200), (150, 64), (33, 65)])
+def test_latency_encoder_is_bit_identical_to_batched(J, lmax):
+    """K1s (one job per 1024-thread CTA, used for calls with <= one job per SM) runs K1a's
+    accumulation chains and cell updates, so x must be bit-identical to K1a on any mix of lengths
+    (1..lmax, chunk boundaries at 64 and 128) and worker counts; both match the oracle."""
+    import os
+    L, H = 2, 64
+    W = synth.make_weights(synth.NetDesc(L, H), seed=77 + J)
+    rng = np.random.default_rng(J)
+    base = synth.small_fleet(J, 5 + J)
+    T = np.zeros((J, lmax, 16), np.float32)
+    l = rng.integers(1, lmax + 1, size=J).astype(np.int32)
+    l[0] = lmax
+    for j in range(J):
+        T[j, : l[j], : base.n[j]] = rng.uniform(0.01, 50.0, size=(l[j], base.n[j])).astype(np.float32)
+    jobs = synth.Jobs(T, base.B_d, base.B_u, base.n, l, base.m, base.arc)
+    net = make(L, H, W)
+    xs = {}
+    for mode in ("batched", "latency"):
+        os.environ["AUTOBYTE_ENCODER"] = mode
+        try:
+            xs[mode] = net.encode(dev(jobs)).cpu().numpy()
+        finally:
+            os.environ.pop("AUTOBYTE_ENCODER", None)
+    assert np.array_equal(xs["batched"], xs["latency"])
+    idx = np.unique([0, J - 1, J // 2])
+    np.testing.assert_allclose(xs["latency"][idx], oracle.encode_jobs(W, jobs, idx), rtol=1e-4, atol=2e-5)
