@@ -97,6 +97,7 @@ struct autobyte_ctx {
   int cta_group = 2;             // K2 variant: CTA pairs or single CTAs (AUTOBYTE_CTA_GROUP=1|2)
   int planes = 1;                // 2 for the fp32-accuracy path (bf16 hi + lo weight planes)
   CUtensorMap wmap{};            // tensor map over wpack for the CTA-pair TMA
+  CUtensorMap wcol[kMaxHidden + 1] = {};   // K4s column-slice maps over the fp32 masters
   cudaStream_t stream = nullptr;
   bool check = false;
   bool shard_encode = true;      // G > 1: K1a on 1/G of the jobs + all-gather of x (AUTOBYTE_SHARD_ENCODE=0 off)
@@ -179,7 +180,7 @@ cudaError_t device_status_word(int device, volatile int** out) {
     int* d = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0)) != cudaSuccess) return e;
     for (auto set : {set_status_adapt, set_status_encode, set_status_encoder_bwd, set_status_exchange,
-                     set_status_score, set_status_topk})
+                     set_status_score, set_status_topk, set_status_adapt_small})
       if ((e = set(d)) != cudaSuccess) return e;
     g_status_host[device] = h;
   }
@@ -705,6 +706,10 @@ autobyte_status autobyte_create(const autobyte_net_desc* desc, const void* blob,
     if ((e = c->spill.ensure((size_t)c->num_sms * kTileM * desc->hidden_width)) != cudaSuccess)
       return bail(e, "alloc fp32 scratch");
   }
+  if (!make_column_tmaps(c->wcol, c->params.ptr, c->off, desc->hidden_width, desc->hidden_layers)) {
+    autobyte_destroy(c);
+    return AB_E_CUDA;
+  }
   if (!make_weight_tmap(&c->wmap, c->wpack.ptr, desc->hidden_width, desc->hidden_layers, c->planes)) {
     autobyte_destroy(c);
     return AB_E_CUDA;
@@ -991,6 +996,8 @@ autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* sampl
   ap.loss_before = loss_before; ap.losses = losses; ap.barrier = c->barrier.ptr;
   ap.opt = opt; ap.beta1 = beta1; ap.beta2 = beta2; ap.eps = eps;
   ap.idx = idx;
+  ap.wpack = c->wpack.ptr; ap.planes = c->planes;
+  for (int k = 0; k <= kMaxHidden; ++k) ap.wcol[k] = c->wcol[k];
   if (opt == AB_OPT_ADAM) {
     if (!c->opt_m.ptr) {   // moments start at zero (blob layout; only the head part is used)
       AB_CUDA(c, c->opt_m.ensure(c->off.total));
@@ -1001,9 +1008,18 @@ autobyte_status run_head_update(autobyte_ctx* c, const autobyte_job_stats* sampl
     ap.m = c->opt_m.ptr; ap.v = c->opt_v.ptr; ap.t0 = c->opt_t;
   }
   int grid_used = 0;
-  AB_CUDA(c, timed(c, K_ADAPT, [&] { return launch_adapt(ap, c->num_sms, c->stream, &grid_used); }));
+  // small minibatches (the per-job online adaptation): one thread-block cluster (K4s,
+  // adapt_small.cu) instead of the grid-wide tcgen05 kernel; the choice depends on B only, so every
+  // replica and every entry point (adapt, train) runs the same kernel for the same minibatch
+  bool small_done = false;
+  AB_CUDA(c, timed(c, K_ADAPT, [&] {
+            cudaError_t e = launch_adapt_small(ap, c->stream);
+            if (e != cudaErrorNotSupported) { small_done = true; return e; }
+            cudaGetLastError();
+            return launch_adapt(ap, c->num_sms, c->stream, &grid_used);
+          }));
   if (opt == AB_OPT_ADAM) c->opt_t += steps;
-  if (steps > 0)
+  if (steps > 0 && !small_done)   // (K4s refreshed the shadows of what it updated in place)
     AB_CUDA(c, timed(c, K_PACK, [&] {
               return launch_pack(c->params.ptr, c->off, H, L, c->planes, c->wpack.ptr, c->stream);
             }));

@@ -392,15 +392,31 @@ __device__ void project_one(const EncodeParams& p, int j, const float* xs, int t
     if (p.cur_keys) p.cur_keys[j] = 0ull;
   }
   const float inv_n = 1.0f / static_cast<float>(n);
+  const bool vec = (p.off.W[1] & 3) == 0;
   for (int col = tid; col < H; col += nthreads) {
+    // the row of W1 and the column of W_o into registers first (all loads in flight together)
     const float* wr = P + p.off.W[1] + (size_t)col * kZDim;
+    float w[kZDim], wo[kNMax];
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < kZDim / 4; ++q) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(wr) + q);
+        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kZDim; ++k) w[k] = wr[k];
+    }
+#pragma unroll
+    for (int ww = 0; ww < kNMax; ++ww) wo[ww] = P[p.off.W_o + (size_t)ww * H + col];
+    const float b1 = P[p.off.b[1] + col];
     float acc = 0.f;
-#pragma unroll 2
-    for (int k = 0; k < kXDim; ++k) acc = fmaf(wr[k], xs[k], acc);
-    p.a_out[(size_t)j * p.jv + col] = acc + P[p.off.b[1] + col];
+#pragma unroll
+    for (int k = 0; k < kXDim; ++k) acc = fmaf(w[k], xs[k], acc);
+    p.a_out[(size_t)j * p.jv + col] = acc + b1;
     float aw = 0.f;
 #pragma unroll
-    for (int ww = 0; ww < kNMax; ++ww) aw = fmaf(P[p.off.W_o + (size_t)ww * H + col], ww < n ? inv_n : 0.f, aw);
+    for (int ww = 0; ww < kNMax; ++ww) aw = fmaf(wo[ww], ww < n ? inv_n : 0.f, aw);
     p.what_out[(size_t)j * p.jv + col] = aw;
   }
 }

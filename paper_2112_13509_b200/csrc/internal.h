@@ -98,7 +98,10 @@ struct alignas(64) ScoreParams {
   int32_t* best_idx; float* best_score; float* cur_score;
 };
 
-struct AdaptParams {
+struct alignas(64) AdaptParams {
+  // K4s: tensor maps of W_k (k = 2..L) as fp32 [H rows][H cols], box = [min(H, 256) rows][H/16 cols]
+  // (one CTA's column slice per 256 rows; adapt_small.cu)
+  CUtensorMap wcol[kMaxHidden + 1];
   int B, H, L, steps;
   float lr;
   const float* x;          // [B][82] frozen encoder output
@@ -122,6 +125,9 @@ struct AdaptParams {
   float* dz_out;           // [B][84] d objective / d [x | u] (encoder fine-tuning) or null
   const int32_t* idx;      // [steps][B] dataset rows of each step's minibatch (train_epoch) or null:
                            // then x / S_p / S_c / v_obs / n are the whole dataset's arrays
+  // K4s refreshes the bf16 shadows of W_2..W_L as it updates them (no separate pack launch)
+  __nv_bfloat16* wpack;    // packed shadows (kWeightReplicas copies of packed_weight_elems)
+  int planes;              // 1 = bf16, 2 = hi/lo (fp32 path)
 };
 
 // ---------------------------------------------------------------- launches (return cudaError_t)
@@ -157,13 +163,33 @@ cudaError_t launch_peer_wait(const unsigned long long* flags, int G, unsigned lo
                              unsigned long long timeout_ns, cudaStream_t s);
 cudaError_t launch_pack(const float* params, const ParamOffsets& off, int H, int L, int planes,
                         __nv_bfloat16* wpack, cudaStream_t s);
-__host__ __device__ size_t packed_weight_elems(int H, int L, int planes);   // one replica
-__host__ __device__ int packed_weight_nch(int H, int planes);              // rows per packed tile
+// elements of one replica of the packed bf16 shadows of W_2..W_L
+__host__ __device__ inline size_t packed_weight_elems(int H, int L, int planes) {
+  return (size_t)(L > 1 ? L - 1 : 0) * H * H * planes;
+}
+// rows per packed tile = N of K2's accumulator chunks (ScoreCfg::NCH)
+__host__ __device__ inline int packed_weight_nch(int H, int planes) {
+  return planes == 2 ? (H == 512 ? 128 : 64) : (H >= 128 ? 128 : H);
+}
+// Element index in the packed bf16 shadow (one replica) of W_{g+2}[n][k], plane 0 = hi, 1 = lo:
+// tile ((g*NQ + n/NCH)*NKB + k/64)*planes + plane of NCH rows x 64 (UMMA SW128 K-major: 16-byte
+// chunk j of row r stored at chunk j ^ (r % 8)) — the inverse of pack_kernel's walk (score.cu).
+__host__ __device__ inline size_t packed_weight_index(int H, int planes, int nch, int g, int n, int k, int plane) {
+  const int nq = H / nch, nkb = H / 64;
+  const int q = n / nch, nl = n - q * nch, b = k >> 6, kl = k & 63;
+  const int slot = ((((kl >> 3) ^ (nl & 7)) << 3) | (kl & 7));
+  const size_t tile = (((size_t)g * nq + q) * nkb + b) * planes + plane;
+  return tile * (size_t)nch * 64 + (size_t)nl * 64 + slot;
+}
 #ifndef AB_WREP
 #define AB_WREP 1   // L2 replicas of the packed bf16 weights (CTA pair i streams replica i % AB_WREP)
 #endif
 constexpr int kWeightReplicas = AB_WREP;
 cudaError_t launch_adapt(const AdaptParams& p, int num_sms, cudaStream_t s, int* grid_used);
+// K4s (adapt_small.cu): one thread-block cluster, for minibatches of at most kAdaptSmallMaxB samples
+// (no encoder gradient, no dataset index); cudaErrorNotSupported otherwise (run K4)
+constexpr int kAdaptSmallMaxB = 16;
+cudaError_t launch_adapt_small(const AdaptParams& p, cudaStream_t s);
 cudaError_t launch_encoder_bwd(const EncodeParams& p, const float* dX, int ldx, float* partial, int num_sms,
                                int* nparts, cudaStream_t s);                                   // K8
 cudaError_t launch_encoder_update(const EncodeParams& p, const float* dX, int ldx, int B, const float* partial,
@@ -180,6 +206,8 @@ cudaError_t launch_check(const autobyte_job_stats& jobs, int n_max, int n_model,
                          int* flag, cudaStream_t s);
 cudaError_t launch_check_grid(const autobyte_grid& g, int* flag, cudaStream_t s);
 bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L, int planes);
+// K4s column-slice maps over the fp32 masters (score.cu, next to the other tensor-map encoder)
+bool make_column_tmaps(CUtensorMap* maps, const float* params, const ParamOffsets& off, int H, int L);
 // device status word (ptx.cuh): each translation unit's copy of the pointer, set per device
 cudaError_t set_status_adapt(int* p);
 cudaError_t set_status_encode(int* p);
@@ -187,5 +215,6 @@ cudaError_t set_status_encoder_bwd(int* p);
 cudaError_t set_status_exchange(int* p);
 cudaError_t set_status_score(int* p);
 cudaError_t set_status_topk(int* p);
+cudaError_t set_status_adapt_small(int* p);
 
 }  // namespace ab

@@ -946,13 +946,7 @@ cudaError_t launch_trigger(int J, const int32_t* best_idx, const float* best_sco
 // NP contiguous NCH x 128-byte tiles (hi, then lo for the fp32 path) in UMMA SW128 K-major order
 // (row n at n*128 bytes, 16-byte chunk j stored at chunk j ^ (n % 8)) — exactly what one
 // cp.async.bulk drops into a pipeline stage.
-__host__ __device__ size_t packed_weight_elems(int H, int L, int planes) {
-  return (size_t)(L > 1 ? L - 1 : 0) * H * H * planes;
-}
-// rows per packed tile = N of K2's accumulator chunks (ScoreCfg::NCH)
-__host__ __device__ int packed_weight_nch(int H, int planes) {
-  return planes == 2 ? (H == 512 ? 128 : 64) : (H >= 128 ? 128 : H);
-}
+
 
 __global__ void pack_kernel(const float* __restrict__ params, ParamOffsets off, int H, int L, int planes,
                             __nv_bfloat16* __restrict__ wpack) {
@@ -1017,16 +1011,39 @@ namespace ab {
 #ifndef AB_TMAP_L2_PROMOTION
 #define AB_TMAP_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
-bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L, int planes) {
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess || !fn)
-      return false;
+      return nullptr;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+
+bool make_column_tmaps(CUtensorMap* maps, const float* params, const ParamOffsets& off, int H, int L) {
+  auto encode = tmap_encoder();
+  if (!encode) return false;
+  for (int k = 0; k <= kMaxHidden; ++k) std::memset(&maps[k], 0, sizeof(CUtensorMap));
+  for (int k = 2; k <= L; ++k) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(H)};   // cols, rows
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(H) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(H / 16), static_cast<cuuint32_t>(H < 256 ? H : 256)};
+    cuuint32_t estr[2] = {1, 1};
+    if (encode(&maps[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(params + off.W[k]), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+
+bool make_weight_tmap(CUtensorMap* map, const __nv_bfloat16* wpack, int H, int L, int planes) {
+  auto encode = tmap_encoder();
+  if (!encode) return false;
   const int NCH = packed_weight_nch(H, planes);
   const size_t rows = packed_weight_elems(H, L, planes) / 64 * kWeightReplicas;
   if (rows == 0) { std::memset(map, 0, sizeof(*map)); return true; }

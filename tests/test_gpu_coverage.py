@@ -412,3 +412,32 @@ def test_latency_encoder_is_bit_identical_to_batched(J, lmax):
     assert np.array_equal(xs["batched"], xs["latency"])
     idx = np.unique([0, J - 1, J // 2])
     np.testing.assert_allclose(xs["latency"][idx], oracle.encode_jobs(W, jobs, idx), rtol=1e-4, atol=2e-5)
+
+
+# ------------------------------------------------------------------------------------- K4s small minibatches
+@pytest.mark.parametrize("L,H,B,prec,opt", [(3, 256, 1, "bf16", "sgd"), (4, 512, 5, "bf16", "adam"),
+                                             (3, 512, 3, "fp32", "sgd"), (2, 64, 16, "bf16", "adam")])
+def test_small_batch_adapt_matches_oracle_and_refreshes_shadows(L, H, B, prec, opt):
+    """K4s (one thread-block cluster, B <= 16) against the oracle (loss, per-tensor updates), and the
+    bf16 shadows it rewrites in place during its update: scores after the adaptation must equal,
+    bit for bit, those of a fresh context packed from the adapted fp32 weights."""
+    from paper_2112_13509_b200.autobyte import AutoByte
+    W = synth.make_weights(synth.NetDesc(L, H), seed=B + H)
+    batch = synth.make_adapt_batch(synth.small_fleet(B, 60 + B), synth.log_grid(64, 64), 9)
+    net = AutoByte(L, H, W, device=0, precision=prec)
+    db = dev_batch(batch)
+    if opt == "sgd":
+        W_ora, loss_ora = oracle.adapt(W, batch, lr=1e-2, steps=2)
+        loss = net.adapt(*db, 1e-2, 2)
+        torch.cuda.synchronize()
+        assert abs(float(loss.item()) - loss_ora) <= 1e-4 * loss_ora
+        check_update(W, W_ora, net.get_weights(), 1e-3)
+    else:
+        kw = dict(lr=1e-3, beta1=0.9, beta2=0.99, eps=1e-6)
+        W_ora, _, l_ora = oracle.train(W, batch, 2, "adam", **kw)
+        got = net.train(*db, 2, "adam", **kw).cpu().numpy()
+        np.testing.assert_allclose(got, l_ora, rtol=1e-3)
+        check_update(W, W_ora, net.get_weights(), 5e-3)
+    jobs, grid = synth.small_fleet(3, 4), synth.log_grid(16, 9)
+    fresh = AutoByte(L, H, net.get_weights(), device=0, precision=prec)
+    assert np.array_equal(gpu_scores(net, jobs, grid), gpu_scores(fresh, jobs, grid))
