@@ -19,3 +19,4 @@ from .metanet import (  # noqa: F401
     HEAD_PARAMS, train, topk_rows, encoder_grad, ENCODER_PARAMS,
 )
 from .trigger import trigger_decide, KEEP, RECONFIGURE, ADAPT  # noqa: F401,E402
+from . import bytescheduler  # noqa: F401,E402  (NEXT 3: one ByteScheduler iteration per candidate)
