@@ -299,6 +299,33 @@ autobyte_status autobyte_trigger(autobyte_ctx* ctx, int32_t J, const int32_t* be
                                  const int32_t* cur_idx, const float* cur_score, const float* v_observed,
                                  float gain, float drift, int32_t* action);
 
+/* Ground-truth evaluator of the candidates (PAPER.md:213-255 mechanism,
+ * PAPER.md:534 grid search): the time of ONE training iteration of every job under every <S_p, S_c>
+ * of this rank's shard, simulated event by event, one GPU thread per (job, candidate):
+ *   - backward from the back layer: layer i's gradient is ready at sum_{k >= i} Tb[k], Tb[i] = the
+ *     slowest valid worker's T[i][w] (R#26);
+ *   - partitioning: a tensor of size b bytes becomes ceil(b / S_p) chunks;
+ *   - priority: the sender commits the next chunk of the front-most ready layer;
+ *   - credit: committed-but-unacknowledged chunks total at most S_c * S_p bytes and 64 chunks
+ *     (R#24);
+ *   - one link sends committed chunks in commit order, s * factor / bw + delta ms each, acknowledged
+ *     alpha ms later; factor 2 for PS (push + pull), 2 (n - 1) / n for ring all-reduce; bw = the
+ *     smallest B_down / B_up of the valid workers (R#25, R#26);
+ *   - the next forward runs front to back, layer i once its tensor is acknowledged.
+ * layer_bytes: DEVICE [J][l_max] fp32 tensor bytes per layer (not part of Table 2; model-profile
+ * input). fwd_ms: DEVICE [J][l_max] forward time per layer, or NULL for Tb / 2 (R#26). sp: HOST.
+ * iter_ms: DEVICE [J][shard_end - shard_begin] float64, column c - shard_begin. The iteration time is
+ * within 1e-12 relative of the float64 oracle (same operations; the forward pass as its max-plus
+ * form). Errors: as autobyte_score; negative or non-finite alpha / delta -> AB_E_INVALID; l_max too
+ * large for the per-thread state (> ~590 layers) -> AB_E_SHAPE. */
+typedef struct {
+  double alpha_ms;   /* per-chunk latency until acknowledgement (what stop-and-wait loses) */
+  double delta_ms;   /* per-chunk partition / scheduling overhead on the link */
+} autobyte_sim_params;
+autobyte_status autobyte_simulate(autobyte_ctx* ctx, const autobyte_job_stats* jobs, const float* layer_bytes,
+                                  const float* fwd_ms, const autobyte_grid* grid, const autobyte_sim_params* sp,
+                                  double* iter_ms);
+
 /* ---- end-to-end entry points (HOST pointers; copies inside; synchronising) ---------- */
 /* Same contracts as above with every array pointer in HOST memory. The library stages the
  * inputs into its own device workspace with cudaMemcpyAsync, runs the device path, copies

@@ -17,7 +17,8 @@ Mechanism, step by step (the order of the loop below):
      layer", P:221)
   4. credit: committed-but-unacknowledged chunks may total at most S_c * S_p bytes ("a sliding
      window ... allows the tensor in the credit window size to be transmitted in parallel", P:247;
-     credit 1X = stop-and-wait)                                            (R#24)
+     credit 1X = stop-and-wait), and at most MAX_INFLIGHT = 64 chunks (a send queue of
+     bounded depth; it only binds when many chunks are much smaller than S_p)       (R#24)
   5. the link sends committed chunks in commit order: a chunk of s bytes occupies it for
      s * factor / bw + delta (delta: per-chunk partition overhead, "the cost of tensor
      partition is not small enough to be ignored") and is acknowledged alpha later (per-chunk
@@ -43,6 +44,9 @@ def comm_factor(arch: int, n: int) -> float:
     if arch == 0:
         return 2.0
     return 2.0 * (n - 1) / n
+
+
+MAX_INFLIGHT = 64
 
 
 def iteration_time(Tb_ms, Tf_ms, size_bytes, bw_Bps: float, factor: float, S_p: float, S_c: float,
@@ -84,7 +88,7 @@ def iteration_time(Tb_ms, Tf_ms, size_bytes, bw_Bps: float, factor: float, S_p: 
             continue
         s = min(S_p, float(size_bytes[cand]) - sent[cand] * S_p)
         # 4. credit: wait for acknowledgements until the chunk fits (alone it always fits: S_c >= 1)
-        if window and inflight + s > credit:
+        if window and (inflight + s > credit or len(window) == MAX_INFLIGHT):
             done, b = window.pop(0)
             t = max(t, done)
             inflight = inflight - b

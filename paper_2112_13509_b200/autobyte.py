@@ -56,6 +56,11 @@ class Optimizer(ctypes.Structure):
 OPT_SGD, OPT_ADAM = 0, 1
 
 
+class SimParams(ctypes.Structure):
+    """autobyte_sim_params: per-chunk latency and overhead (ms) of the ByteScheduler evaluator."""
+    _fields_ = [("alpha_ms", ctypes.c_double), ("delta_ms", ctypes.c_double)]
+
+
 class Profile(ctypes.Structure):
     _fields_ = [("encode_ms", ctypes.c_double), ("encode_launches", ctypes.c_int64),
                 ("score_ms", ctypes.c_double), ("score_launches", ctypes.c_int64),
@@ -76,7 +81,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile",
            "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback",
-           "autobyte_debug_mem_check", "autobyte_train_epoch"]
+           "autobyte_debug_mem_check", "autobyte_train_epoch", "autobyte_simulate"]
 
 _lib = None
 
@@ -126,6 +131,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_debug_peer_loopback": (I32, [P, I32, I32, I32, I32, I32, P, P, P, P]),
         "autobyte_debug_mem_check": (I32, [P]),
         "autobyte_train_epoch": (I32, [P, P, P, P, P, P, I32, I32, P, P]),
+        "autobyte_simulate": (I32, [P, P, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -409,6 +415,22 @@ class AutoByte:
                                                   V_bar.data_ptr(), order.data_ptr(), batch, steps, ctypes.byref(opt),
                                                   losses.data_ptr() if losses is not None else None), "train_epoch")
         return losses[:steps] if losses is not None else None
+
+    def simulate(self, jobs: DeviceJobs, layer_bytes, grid: DeviceGrid, alpha_ms: float, delta_ms: float,
+                 fwd_ms=None, begin: int = 0, end: Optional[int] = None):
+        """Iteration time (ms, float64 [J][shard]) of every job under every candidate of the shard,
+        simulated under ByteScheduler's partitioning / priority / credit semantics (NEXT 3)."""
+        import torch
+        g = grid.struct(begin, end)
+        out = torch.empty((jobs.J, g.shard_end - g.shard_begin), dtype=torch.float64, device=self.torch_device)
+        sp = SimParams(float(alpha_ms), float(delta_ms))
+        js = jobs.struct()
+        lb = layer_bytes.to(torch.float32).contiguous()
+        fw = fwd_ms.to(torch.float32).contiguous() if fwd_ms is not None else None
+        self._check(self.lib.autobyte_simulate(self.ctx, ctypes.byref(js), lb.data_ptr(),
+                                               fw.data_ptr() if fw is not None else None, ctypes.byref(g),
+                                               ctypes.byref(sp), out.data_ptr()), "simulate")
+        return out
 
     def reset_optimizer(self):
         self._check(self.lib.autobyte_reset_optimizer(self.ctx), "reset_optimizer")

@@ -180,7 +180,7 @@ cudaError_t device_status_word(int device, volatile int** out) {
     int* d = nullptr;
     if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0)) != cudaSuccess) return e;
     for (auto set : {set_status_adapt, set_status_encode, set_status_encoder_bwd, set_status_exchange,
-                     set_status_score, set_status_topk, set_status_adapt_small})
+                     set_status_score, set_status_topk, set_status_adapt_small, set_status_simulate})
       if ((e = set(d)) != cudaSuccess) return e;
     g_status_host[device] = h;
   }
@@ -1180,6 +1180,29 @@ autobyte_status autobyte_train_epoch(autobyte_ctx* c, const autobyte_job_stats* 
   if (steps == 0) return AB_OK;
   return run_head_update(c, dataset, sp_bytes, sc_mult, v_obs, opt->kind, opt->lr, opt->beta1, opt->beta2, opt->eps,
                          steps, nullptr, losses, order, batch);
+}
+
+autobyte_status autobyte_simulate(autobyte_ctx* c, const autobyte_job_stats* jobs, const float* layer_bytes,
+                                  const float* fwd_ms, const autobyte_grid* grid, const autobyte_sim_params* sp,
+                                  double* iter_ms) {
+  NvtxRange nvtx_range("autobyte_simulate");
+  if (!c) return AB_E_INVALID;
+  if (autobyte_status ws = take_status(c)) return ws;
+  autobyte_status s = check_jobs_host(c, jobs);
+  if (s != AB_OK) return s;
+  if ((s = check_grid_host(c, grid)) != AB_OK) return s;
+  if (!layer_bytes || !sp || !iter_ms) return fail(c, AB_E_INVALID, "layer_bytes / params / iter_ms is NULL");
+  if (!(sp->alpha_ms >= 0.0) || !(sp->delta_ms >= 0.0) || !std::isfinite(sp->alpha_ms) || !std::isfinite(sp->delta_ms))
+    return fail(c, AB_E_INVALID, "alpha_ms and delta_ms must be finite and >= 0");
+  if (simulate_smem_bytes(jobs->l_max) > 227 * 1024)
+    return fail(c, AB_E_SHAPE, "l_max too large for the simulator's per-thread state (at most ~590 layers)");
+  DeviceGuard guard(c->device);
+  if ((s = device_checks(c, jobs, grid)) != AB_OK) return s;
+  if (grid->shard_end == grid->shard_begin) return AB_OK;
+  AB_CUDA(c, timed(c, K_OTHER, [&] {
+            return launch_simulate(*jobs, layer_bytes, fwd_ms, *grid, sp->alpha_ms, sp->delta_ms, iter_ms, c->stream);
+          }));
+  return AB_OK;
 }
 
 autobyte_status autobyte_reset_optimizer(autobyte_ctx* c) {

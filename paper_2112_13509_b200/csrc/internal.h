@@ -216,5 +216,10 @@ cudaError_t set_status_exchange(int* p);
 cudaError_t set_status_score(int* p);
 cudaError_t set_status_topk(int* p);
 cudaError_t set_status_adapt_small(int* p);
+cudaError_t set_status_simulate(int* p);
+// K10 (simulate.cu): one ByteScheduler iteration per (job, candidate) of the shard (NEXT 3)
+cudaError_t launch_simulate(const autobyte_job_stats& jobs, const float* layer_bytes, const float* fwd_ms,
+                            const autobyte_grid& g, double alpha_ms, double delta_ms, double* iter_ms, cudaStream_t s);
+size_t simulate_smem_bytes(int l_max);
 
 }  // namespace ab

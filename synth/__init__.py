@@ -315,6 +315,27 @@ def config(name: str, dyadic: bool = False) -> Config:
     raise KeyError(name)
 
 
+# parameter counts of the model profiles (public facts, not from the paper; fp32 gradients: 4 B each)
+MODEL_PARAMS = {"resnet50": 25.6e6, "vgg16": 138.4e6, "alexnet": 61.1e6, "transformer": 65.0e6}
+
+
+def layer_bytes(jobs: Jobs, seed: int = BASE_SEED + 500) -> np.ndarray:
+    """[J][l_max] fp32 gradient-tensor bytes per layer for the ByteScheduler evaluator (NEXT 3): the
+    job's model parameter count x 4 bytes split over its l layers by a fixed Dirichlet(0.7) draw per
+    model type (a few large layers, many small ones), zero on padded layers. Random numbers only."""
+    by_type = {mid: name for name, (_, _, mid) in MODEL_PROFILES.items()}
+    out = np.zeros((jobs.J, jobs.l_max), np.float32)
+    shares = {}
+    for j in range(jobs.J):
+        m, l = int(jobs.m[j]), int(jobs.l[j])
+        name = by_type.get(m, "resnet50")
+        if (m, l) not in shares:
+            rng = np.random.Generator(np.random.PCG64(seed + 31 * m + l))
+            shares[(m, l)] = rng.dirichlet(np.full(l, 0.7))
+        out[j, :l] = np.round(4.0 * MODEL_PARAMS[name] * shares[(m, l)]).astype(np.float32)
+    return out
+
+
 def small_fleet(J: int, seed: int, l_max: int = 54) -> Jobs:
     """A small mixed fleet for parity tests (all four model profiles, PS/AR, n in {1..16})."""
     return make_jobs(J, seed, list(MODEL_PROFILES), [0, 1], list(range(1, N_MAX + 1)), l_max=l_max)

@@ -441,3 +441,43 @@ def test_small_batch_adapt_matches_oracle_and_refreshes_shadows(L, H, B, prec, o
     jobs, grid = synth.small_fleet(3, 4), synth.log_grid(16, 9)
     fresh = AutoByte(L, H, net.get_weights(), device=0, precision=prec)
     assert np.array_equal(gpu_scores(net, jobs, grid), gpu_scores(fresh, jobs, grid))
+
+
+# ------------------------------------------------------------------------------------- NEXT 3 evaluator
+@pytest.mark.parametrize("with_fwd", [False, True])
+def test_simulate_matches_oracle(with_fwd):
+    """K10 (one thread per (job, candidate)) against the oracle's event loop: every iteration time
+    within 1e-12 relative (same float64 operations; the forward as its max-plus form) and the same
+    best candidate per job; PS and all-reduce jobs (incl. n = 1, no traffic), a zero-byte layer."""
+    from paper_2112_13509_b200.autobyte import DeviceGrid
+    from oracle import bytescheduler as bs
+    jobs = synth.make_jobs(7, 12, ["alexnet", "vgg16", "transformer"], [0, 1], [1, 2, 4, 8, 16], l_max=16)
+    lb = synth.layer_bytes(jobs)
+    lb[2, 1] = 0.0
+    grid = synth.Grid(np.array([1 << 16, 1 << 19, 3 << 20, 1 << 23, 5 << 23, 1 << 26], np.int64),
+                      np.array([1.0, 2.0, 3.5, 8.0, 16.0], np.float32))
+    rng = np.random.default_rng(3)
+    fwd = (rng.uniform(0.1, 4.0, lb.shape).astype(np.float32)) if with_fwd else None
+    net = make(2, 64, synth.make_weights(synth.NetDesc(2, 64)))
+    dj = dev(jobs)
+    got = net.simulate(dj, torch.as_tensor(lb, device="cuda"), DeviceGrid.from_host(grid), 0.1, 0.05,
+                       torch.as_tensor(fwd, device="cuda") if with_fwd else None).cpu().numpy()
+    want = bs.simulate_grid(jobs, lb, grid, 0.1, 0.05, fwd_ms=fwd)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+    assert np.array_equal(np.argmin(got, axis=1), np.argmin(want, axis=1))
+
+
+def test_simulate_resnet_shard_and_errors():
+    """A 54-layer job on a shard of a log grid (global candidate indices), and the argument checks."""
+    from paper_2112_13509_b200.autobyte import AutoByteError, DeviceGrid
+    from oracle import bytescheduler as bs
+    jobs = synth.config("C2").jobs
+    lb = synth.layer_bytes(jobs)
+    grid = synth.log_grid(16, 8, lo_exp=16.0, hi_exp=28.0)
+    net = make(2, 64, synth.make_weights(synth.NetDesc(2, 64)))
+    dj, dg, tl = dev(jobs), DeviceGrid.from_host(grid), torch.as_tensor(lb, device="cuda")
+    got = net.simulate(dj, tl, dg, 0.05, 0.02, None, 37, 101).cpu().numpy()
+    want = bs.simulate_grid(jobs, lb, grid, 0.05, 0.02, c_begin=37, c_end=101)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+    with pytest.raises(AutoByteError):
+        net.simulate(dj, tl, dg, -1.0, 0.0)
