@@ -386,8 +386,9 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
         asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
         if (cur != g) break;
         if ((i & 1023u) == 0) {   // watchdog (ptx.cuh): record, then run to the end instead of trapping
-          if (ab_aborted()) break;
-          if (clock64() - t0 > (1ll << 36)) { ab_raise(kStatusPipeline, blockIdx.x); break; }
+          const long long dt = clock64() - t0;
+          if (dt >= (1ll << 26) && ab_aborted()) break;   // (status word only once the wait is stuck)
+          if (dt > (1ll << 36)) { ab_raise(kStatusPipeline, blockIdx.x); break; }
         }
       }
     }

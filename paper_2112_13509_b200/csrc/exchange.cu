@@ -49,8 +49,9 @@ __device__ bool wait_flag(const unsigned long long* flag, unsigned long long epo
 #pragma unroll 1
   for (uint32_t i = 1; ld_acquire_sys(flag) < epoch; ++i) {
     if ((i & 255u) != 0) continue;
-    if (ab_aborted()) return false;
-    if (timeout_ns != 0 && global_ns() - t0 > timeout_ns) {
+    const unsigned long long dt = global_ns() - t0;
+    if (dt > 10000000ull && ab_aborted()) return false;   // status word only after 10 ms of waiting
+    if (timeout_ns != 0 && dt > timeout_ns) {
       ab_raise(code, peer);
       return false;
     }

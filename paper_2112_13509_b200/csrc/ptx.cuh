@@ -62,13 +62,25 @@ __device__ __forceinline__ uint32_t mbar_try(uint32_t addr, uint32_t parity) {
       : "memory");
   return done;
 }
-static __device__ __noinline__ void mbar_wait_slow(uint32_t addr, uint32_t parity) {
+__device__ __forceinline__ uint32_t mbar_try_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return done;
+}
+// Watchdog tail of a wait that already spun 2^20 tries (cold: only a stuck pipeline gets here).
+static __device__ __noinline__ void mbar_wait_watchdog(uint32_t addr, uint32_t parity, bool cluster) {
   const long long t0 = clock64();
 #pragma unroll 1
-  for (uint32_t i = 1; !mbar_try(addr, parity); ++i) {
+  for (uint32_t i = 1; !(cluster ? mbar_try_cluster(addr, parity) : mbar_try(addr, parity)); ++i) {
     if ((i & 1023u) != 0) continue;
+    const long long dt = clock64() - t0;
+    // the status word is mapped host memory (a PCIe round trip): checked once per 1024 tries
     if (ab_aborted()) return;
-    if (clock64() - t0 > (1ll << 36)) {
+    if (dt > (1ll << 36)) {
       printf("autobyte: mbarrier watchdog (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x, threadIdx.x, addr,
              parity);
       ab_raise(kStatusPipeline, blockIdx.x);
@@ -76,9 +88,19 @@ static __device__ __noinline__ void mbar_wait_slow(uint32_t addr, uint32_t parit
     }
   }
 }
+// Slow path of mbar_wait: a bare try_wait spin in a LEAF function (no calls, so entering it saves no
+// state; any bookkeeping here measurably delays K2's producer / issuer: +3-8 % K2 time at C4),
+// returning false after 2^20 tries; only then does the caller run the watchdog.
+static __device__ __noinline__ bool mbar_spin(uint32_t addr, uint32_t parity) {
+#pragma unroll 1
+  for (int k = 0; k < (1 << 20); ++k)
+    if (mbar_try(addr, parity)) return true;
+  return false;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  if (!mbar_try(addr, parity)) mbar_wait_slow(addr, parity);
+  if (mbar_try(addr, parity)) return;
+  if (!mbar_spin(addr, parity)) mbar_wait_watchdog(addr, parity, false);
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -222,30 +244,18 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-__device__ __forceinline__ uint32_t mbar_try_cluster(uint32_t addr, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(addr), "r"(parity)
-      : "memory");
-  return done;
+// wait with cluster-scope acquire: arrivals came from the peer CTA of the pair (the slow path is
+// out of line, as for mbar_wait, so the watchdog adds no code or registers to the callers)
+static __device__ __noinline__ bool mbar_spin_cluster(uint32_t addr, uint32_t parity) {
+#pragma unroll 1
+  for (int k = 0; k < (1 << 20); ++k)
+    if (mbar_try_cluster(addr, parity)) return true;
+  return false;
 }
-// wait with cluster-scope acquire: arrivals came from the peer CTA of the pair
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_cluster(addr, parity)) return;
-  const long long t0 = clock64();
-#pragma unroll 1
-  for (uint32_t i = 1; !mbar_try_cluster(addr, parity); ++i) {
-    if ((i & 1023u) != 0) continue;
-    if (ab_aborted()) return;
-    if (clock64() - t0 > (1ll << 36)) {
-      printf("autobyte: cluster mbarrier watchdog (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-      ab_raise(kStatusPipeline, blockIdx.x);
-      return;
-    }
-  }
+  if (!mbar_spin_cluster(addr, parity)) mbar_wait_watchdog(addr, parity, true);
 }
 // 2-D tensor TMA issued by either CTA of a pair; completion bytes land on the LEADER's barrier
 // (bit 24 of a shared::cta window address selects the peer; clearing it names CTA 0).
