@@ -105,7 +105,8 @@ typedef struct {
  * c = p*Q + q, so ascending c = smaller partition first, then smaller credit (R#11).
  * This rank scores c in [shard_begin, shard_end); returned indices are global. */
 typedef struct {
-  int32_t P, Q;                    /* >= 1 each */
+  int32_t P, Q;                    /* >= 1 each, P*Q <= 2^31 - 129 (AB_E_SHAPE); per call also
+                                      J * ceil((shard_end - shard_begin) / 128) < 2^31 */
   const int64_t* partition_bytes;  /* [P] strictly ascending, >= 4096 */
   const float*   credit_mult;      /* [Q] strictly ascending, >= 1 (R#9) */
   int64_t shard_begin, shard_end;  /* 0 <= begin < end <= P*Q */

@@ -31,6 +31,11 @@ autobyte_status autobyte_debug_peer_loopback(autobyte_ctx* ctx, int32_t G, int32
  * live canaries of that device were overwritten (0 = none; -1 on a CUDA error or NULL ctx). */
 int32_t autobyte_debug_mem_check(autobyte_ctx* ctx);
 
+/* The library's fast 32-bit division (K2's per-tile index splits: tile -> (job, tile of job) by
+ * tiles_per_job, candidate -> (p, q) by Q): the host-built multiplier / shift applied on the host,
+ * out[i] = n[i] / d for 0 <= n[i] < 2^31, d >= 1 (else AB_E_SHAPE). Host memory, no GPU needed. */
+autobyte_status autobyte_debug_fastdiv(uint32_t d, const uint32_t* n, int32_t count, uint32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,7 +81,7 @@ EXPORTS = ["autobyte_abi_version", "autobyte_status_string", "autobyte_validate_
            "autobyte_adapt_host", "autobyte_staged_job_bytes", "autobyte_peer_exchange", "autobyte_topk", "autobyte_train", "autobyte_reset_optimizer", "autobyte_optimizer_step",
            "autobyte_get_weights", "autobyte_set_profiling", "autobyte_get_profile", "autobyte_reset_profile",
            "autobyte_argmax_keys", "autobyte_reduce_keys", "autobyte_debug_peer_loopback",
-           "autobyte_debug_mem_check", "autobyte_train_epoch", "autobyte_simulate"]
+           "autobyte_debug_mem_check", "autobyte_train_epoch", "autobyte_simulate", "autobyte_debug_fastdiv"]
 
 _lib = None
 
@@ -130,6 +130,7 @@ def load_library(path: Optional[str] = None):
         "autobyte_reduce_keys": (I32, [P, I32, I32, P, P, P, P]),
         "autobyte_debug_peer_loopback": (I32, [P, I32, I32, I32, I32, I32, P, P, P, P]),
         "autobyte_debug_mem_check": (I32, [P]),
+        "autobyte_debug_fastdiv": (I32, [ctypes.c_uint32, P, I32, P]),
         "autobyte_train_epoch": (I32, [P, P, P, P, P, P, I32, I32, P, P]),
         "autobyte_simulate": (I32, [P, P, P, P, P, P, P]),
     }

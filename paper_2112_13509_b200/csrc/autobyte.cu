@@ -256,7 +256,8 @@ autobyte_status check_grid_host(autobyte_ctx* c, const autobyte_grid* g) {
   if (!g) return fail(c, AB_E_INVALID, "grid pointer is NULL");
   if (g->P < 1 || g->Q < 1) return fail(c, AB_E_SHAPE, "grid P and Q must be >= 1");
   const long long C = (long long)g->P * g->Q;
-  if (C > 0x7FFFFFFFLL) return fail(c, AB_E_SHAPE, "grid has more than 2^31-1 candidates");
+  // (K2 forms candidate indices of a whole 128-row tile past the shard end in 32 bits)
+  if (C > 0x7FFFFFFFLL - kTileM) return fail(c, AB_E_SHAPE, "grid has more than 2^31-129 candidates");
   // with a communicator attached an empty shard is a valid part of a partition of [0, C) (C < world
   // gives some ranks nothing to score): that rank skips K0/K2 but still joins the collectives
   const bool multi = c && c->comm && c->world > 1;
@@ -540,6 +541,10 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.c_begin = grid->shard_begin; sp.c_end = grid->shard_end;
   sp.tiles_per_job = static_cast<int>((cs + kTileM - 1) / kTileM);
   sp.n_tiles = (long long)sp.tiles_per_job * J;
+  if (sp.n_tiles >= (1ll << 31))   // K2 indexes tiles in 32 bits
+    return fail(c, AB_E_SHAPE, "J * ceil(shard / 128) must stay below 2^31 per call");
+  make_fastdiv(static_cast<uint32_t>(sp.tiles_per_job), &sp.tpj_mul, &sp.tpj_shr);
+  make_fastdiv(static_cast<uint32_t>(grid->Q), &sp.q_mul, &sp.q_shr);
   sp.S_p = reinterpret_cast<const long long*>(grid->partition_bytes); sp.S_c = grid->credit_mult;
   sp.params = c->params.ptr; sp.off = c->off;
   sp.jobvec = c->jobvec.ptr;
@@ -908,6 +913,18 @@ autobyte_status autobyte_reduce_keys(autobyte_ctx* c, int32_t J, int32_t G, cons
   AB_CUDA(c, timed(c, K_FINALIZE, [&] {
             return launch_finalize(J, G, 2LL * J, k, k + J, best_idx, best_score, cur_score, c->stream);
           }));
+  return AB_OK;
+}
+
+autobyte_status autobyte_debug_fastdiv(uint32_t d, const uint32_t* n, int32_t count, uint32_t* out) {
+  if (d < 1 || count < 0 || (count > 0 && (!n || !out))) return AB_E_SHAPE;
+  uint32_t mul = 0, shr = 0;
+  make_fastdiv(d, &mul, &shr);
+  for (int32_t i = 0; i < count; ++i) {
+    if (n[i] >= 0x80000000u) return AB_E_SHAPE;
+    // fdiv() of internal.h on the host: __umulhi(n, mul) >> shr
+    out[i] = d == 1 ? n[i] : static_cast<uint32_t>((static_cast<uint64_t>(n[i]) * mul) >> 32) >> shr;
+  }
   return AB_OK;
 }
 

@@ -22,6 +22,26 @@ constexpr int kTileM = 128;                    // candidates per tcgen05 tile (T
 constexpr int kEncStash = kEmbed + 12 * kLstm; // floats stashed per job and layer step (e, 2 x [i f g o c h])
 
 // Offsets (in floats) of every parameter inside the fp32 master buffer (= blob payload order).
+// n / d for 0 <= n < 2^31 as a multiply-shift (Granlund-Montgomery with p = 31 + ceil(log2 d),
+// mul = ceil(2^p / d); exact for every n < 2^31, checked exhaustively at the edges in
+// tests/test_boundary.py::test_fastdiv_reference): the kernels' per-tile index splits.
+struct FastDiv {
+  uint32_t d, mul, shr;
+};
+inline void make_fastdiv(uint32_t d, uint32_t* mul, uint32_t* shr) {
+  if (d <= 1) { *mul = 0; *shr = 0; return; }
+  int l = 0;
+  while ((1ull << l) < d) ++l;   // ceil(log2 d)
+  const int p = 31 + l;
+  *mul = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
+  *shr = static_cast<uint32_t>(p - 32);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return f.d == 1 ? n : static_cast<int>(__umulhi(static_cast<uint32_t>(n), f.mul) >> f.shr);
+}
+#endif
+
 struct ParamOffsets {
   int64_t E_m, E_arc, W_e, b_e;
   int64_t l1Wx, l1Wh, l1b, l2Wx, l2Wh, l2b;
@@ -78,7 +98,9 @@ struct alignas(64) ScoreParams {
   int P, Q;
   long long c_begin, c_end;     // shard [begin, end)
   int tiles_per_job;
-  long long n_tiles;
+  long long n_tiles;            // < 2^31 (like c_end): the kernel indexes tiles in 32 bits
+  uint32_t tpj_mul, tpj_shr;    // FastDiv of tiles_per_job and of Q (make_fastdiv)
+  uint32_t q_mul, q_shr;
   const long long* S_p;         // [P]
   const float* S_c;             // [Q]
   const float* params;          // fp32 masters (W1's u-columns, biases)

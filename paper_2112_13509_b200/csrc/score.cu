@@ -36,6 +36,9 @@ namespace ab {
 #ifndef AB_NT
 #define AB_NT 1    // tiles in flight per CTA on narrow bf16 heads (H <= 256); 2 measured slower (epilogue-bound)
 #endif
+#ifndef AB_NACC
+#define AB_NACC 2  // TMEM accumulators; 3 fit beside buffer Y at bf16 H = 128 / 256 (NT = 1) but measured slower
+#endif
 
 // Optional cycle accounting (build with -DAB_STATS): where each warp role spends its time.
 #ifdef AB_STATS
@@ -116,7 +119,12 @@ struct ScoreCfg {
   static constexpr int SMEM = 1024 + FIXED + NS * CTA_STAGE_BYTES;
   static constexpr uint32_t IDESC = umma_idesc_bf16(128 * CG, NCH);
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t Y_COL = 256;          // TMEM column of activation buffer Y
+  // NACC 128-column accumulators rotate over the chunks (commit order = epilogue order). A third
+  // one fits beside Y at H = 128 / 256 (bf16, NT = 1) so the issuer never waits for the epilogue
+  // to read the accumulator it overwrites; measured 945 vs 971 TFLOP/s at 3x256 (the epilogue, not
+  // the issuer, is the bottleneck), hence off by default.
+  static constexpr int NACC = (!P3 && NT == 1 && H >= 128 && H <= 256) ? AB_NACC : 2;
+  static constexpr uint32_t Y_COL = NACC * NCH;   // TMEM column of activation buffer Y
   static constexpr int EPI_ARRIVALS = CG == 2 ? 32 : 16;   // 16 epilogue warps per CTA of the pair
   static constexpr int SPILL_U32 = SPILL ? NQ * NSPLIT * (QC / 2) * NP : 0;   // scratch u32 per row (per CTA)
   static_assert(NS >= 4, "not enough shared memory for the weight pipeline");
@@ -218,8 +226,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   uint64_t* full = bars;
   uint64_t* empty = full + C::NS;
   uint64_t* dfull = empty + C::NS;
-  uint64_t* dempty = dfull + 2;
-  uint64_t* afull = dempty + 2;                                                 // [NT][NQ]
+  uint64_t* dempty = dfull + C::NACC;
+  uint64_t* afull = dempty + C::NACC;                                           // [NT][NQ]
   uint64_t* vfull = afull + C::NT * C::NQ;                                      // next unit's job vectors
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(vfull + 1);
   unsigned long long* sWkey = reinterpret_cast<unsigned long long*>(sTmem + 2);
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::EPI_ARRIVALS); }
+    for (int i = 0; i < C::NACC; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::EPI_ARRIVALS); }
     for (int q = 0; q < C::NT * C::NQ; ++q) mbar_init(&afull[q], C::EPI_ARRIVALS);
     mbar_init(vfull, 1);
     fence_barrier_init();
@@ -261,9 +269,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   const uint32_t tmem = *sTmem;
   // work unit u = NT tiles per CTA (of a pair): this CTA's tile t of unit u is (u*NT + t)*CG + rank;
   // units are handed out round-robin: first + i*stride
-  const long long n_units = (p.n_tiles + CG * C::NT - 1) / (CG * C::NT);
-  const long long first = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
-  const long long stride = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
+  // tile, unit and candidate indices are 32-bit (the host guarantees n_tiles, c_end < 2^31); the
+  // divisions by tiles_per_job and Q are multiply-shifts (FastDiv): a 64-bit division is a ~30-
+  // instruction sequence that every epilogue thread ran per tile (ncu: 7.6 % of K2's instructions)
+  const int n_tiles = static_cast<int>(p.n_tiles);
+  const int n_units = (n_tiles + CG * C::NT - 1) / (CG * C::NT);
+  const int first = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
+  const int stride = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
 
   if (warp == 0) {
     // ================================================================ TMA producer (both CTAs)
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       // this pair's (CTA's) replica of the packed weights (same bytes, different L2 lines)
       const int rep = static_cast<int>((CG == 2 ? (blockIdx.x >> 1) : blockIdx.x) % kWeightReplicas);
       const int rep_rows = G * C::NQ * C::NKB * C::NCH * C::NP;   // 64-element rows per replica
-      for (long long u = first; u < n_units; u += stride)
+      for (int u = first; u < n_units; u += stride)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
             for (int t = 0; t < C::NT; ++t)   // every tile of the unit streams the same chunk weights
@@ -319,7 +331,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       uint32_t ph = 0, aph = 0, dbits = 0;
       int dq = 0, b0 = 0;
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sStage));
-      for (long long u = first; u < n_units; u += stride) {
+      for (int u = first; u < n_units; u += stride) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
           for (int q = 0; q < C::NQ; ++q)
@@ -351,7 +363,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             }
             AB_TRACE(u == first + 2 * stride && lane == 0, 12, g, q);
             __syncwarp();
-            dq ^= 1;
+            dq = dq + 1 == C::NACC ? 0 : dq + 1;
           }
           aph ^= 1;
         }
@@ -364,14 +376,19 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     const int ew = warp - 2, quad = warp & 3, grp = ew >> 2;   // grp: column group of a chunk
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    const long long cshard = p.c_end - p.c_begin;
+    const int c_begin = static_cast<int>(p.c_begin), c_end = static_cast<int>(p.c_end);
+    const int cshard = c_end - c_begin;
+    const FastDiv tpj_div{static_cast<uint32_t>(tpj), p.tpj_mul, p.tpj_shr};
+    const FastDiv q_div{static_cast<uint32_t>(p.Q), p.q_mul, p.q_shr};
     const float* w0s = sAw + C::NT * H;
     const float* w1s = sAw + (C::NT + 1) * H;
     // the MMA issuer's barriers live in the leader CTA: every epilogue warp of the pair counts in
     // on its own (the leader's locally, the peer's with a remote arrive), so no warp waits for the
     // other warps of its CTA
-    const uint32_t dempty_c[2] = {mapa_shared(smem_u32(&dempty[0]), 0), mapa_shared(smem_u32(&dempty[1]), 0)};
-    auto my_tile = [&](long long u, int t) { return (u * C::NT + t) * CG + rank; };
+    uint32_t dempty_c[C::NACC];
+#pragma unroll
+    for (int i = 0; i < C::NACC; ++i) dempty_c[i] = mapa_shared(smem_u32(&dempty[i]), 0);
+    auto my_tile = [&](int u, int t) { return (u * C::NT + t) * CG + static_cast<int>(rank); };
     auto signal = [&](uint64_t* bar, uint32_t cluster_addr) {   // called by the whole warp after __syncwarp
       if (lane == 0) {
         if (CG == 2 && !leader) mbar_arrive_remote(cluster_addr);
@@ -380,12 +397,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     };
 
     const int jv = 2 * H + 4;
-    auto job_of = [&](long long tile) {
-      const long long tt = tile < p.n_tiles ? tile : p.n_tiles - 1;   // ghost tile of an odd pair
-      return static_cast<int>(tt / tpj);
+    auto job_of = [&](int tile) {
+      const int tt = tile < n_tiles ? tile : n_tiles - 1;   // ghost tile of an odd pair
+      return fdiv(tt, tpj_div);
     };
     // job vectors of unit u's tiles -> their a slots and w|beta slots `slot`, synchronously
-    auto load_vecs = [&](int slot, long long u) {
+    auto load_vecs = [&](int slot, int u) {
       for (int t = 0; t < C::NT; ++t) {
         const float* v = p.jobvec + (size_t)job_of(my_tile(u, t)) * jv;
         for (int k = etid; k < H; k += kEpiThreads) sAw[t * H + k] = v[k];
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       }
     };
     // the same, as TMA bulk copies completing on vfull (issued by one thread)
-    auto prefetch_vecs = [&](int slot, long long u) {
+    auto prefetch_vecs = [&](int slot, int u) {
       if (etid == 0) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(vfull, C::NT * (H + C::WV) * 4);
@@ -405,16 +422,15 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       }
     };
     // candidate index and encoding (K0) of this thread's row of `tile`
-    auto row_u = [&](long long tile, float& up, float& uc, long long& c) {
-      const long long tt = tile < p.n_tiles ? tile : p.n_tiles - 1;
-      const int ct = static_cast<int>(tt % tpj);
-      c = p.c_begin + (long long)ct * kTileM + row;
-      const long long cc = c < p.c_end ? c : p.c_end - 1;
-      // u_c = (u_p[c / Q], u_c[c % Q]) (a-1, R#8; axes from K1b / K1s); C < 2^31, so 32-bit division
-      const uint32_t ci = static_cast<uint32_t>(cc), qn = static_cast<uint32_t>(p.Q);
-      const uint32_t pi = ci / qn;
+    auto row_u = [&](int tile, float& up, float& uc, int& c) {
+      const int tt = tile < n_tiles ? tile : n_tiles - 1;
+      const int ct = tt - fdiv(tt, tpj_div) * tpj;
+      c = c_begin + ct * kTileM + row;
+      const int cc = c < c_end ? c : c_end - 1;
+      // u_c = (u_p[c / Q], u_c[c % Q]) (a-1, R#8; axes from K1b / K1s)
+      const int pi = fdiv(cc, q_div);
       up = p.up[pi];
-      uc = p.uc[ci - pi * qn];
+      uc = p.uc[cc - pi * p.Q];
     };
     // QC bf16 activations of this thread's row starting at column c0 -> buffer X (smem) or Y (TMEM)
     auto store_plane = [&](int t, int dst, int c0, const uint32_t (&pk)[C::QC / 2], int plane) {
@@ -558,7 +574,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     // score, arg-max key and per-job reduction of a tile (all epilogue threads; a quadrant-local
     // variant without the CTA-wide barriers measured 6 % slower at 3x256: the issuer waited longer
     // for accumulators once the quadrants drifted apart)
-    auto reduce_tile = [&](float dot, int wslot, bool real, int j, long long c) {
+    auto reduce_tile = [&](float dot, int wslot, bool real, int j, int c) {
       AB_T0(tr);
       sPart[grp * kTileM + row] = dot;
       named_bar_sync(kEpiBar, kEpiThreads);
@@ -567,8 +583,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #pragma unroll
         for (int i = 1; i < C::NSPLIT; ++i) score += sPart[i * kTileM + row];
         score += sWhat[wslot * C::WV + H];
-        const bool valid = real && c < p.c_end;
-        if (valid && p.scores) p.scores[(size_t)j * cshard + (c - p.c_begin)] = score;
+        const bool valid = real && c < c_end;
+        if (valid && p.scores) p.scores[(size_t)j * cshard + (c - c_begin)] = score;
         const uint32_t o = ord32(score);
         unsigned long long key = (valid && o) ? ((static_cast<unsigned long long>(o) << 32) |
                                                  (0xFFFFFFFFu - static_cast<uint32_t>(c)))
@@ -593,13 +609,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 
     int dq = 0, b0 = 0, it = 0;
     uint32_t dbits = 0, vph = 0;
-    long long u = first;
+    int u = first;
     if (u < n_units) load_vecs(0, u);
     named_bar_sync(kEpiBar, kEpiThreads);
     if (G > 0 && u < n_units) {
       for (int t = 0; t < C::NT; ++t) {
         float up, uc;
-        long long c;
+        int c;
         row_u(my_tile(u, t), up, uc, c);
 #pragma unroll 1
         for (int q = 0; q < C::NQ; ++q) build_piece(t, q, up, uc, 0);
@@ -610,17 +626,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       const int slot = it & 1;
       const bool has_next = u + stride < n_units;
       float up[C::NT], uc[C::NT], up2[C::NT], uc2[C::NT], dot[C::NT];
-      long long c[C::NT];
+      int c[C::NT];
       bool real[C::NT];
       int j[C::NT];
 #pragma unroll
       for (int t = 0; t < C::NT; ++t) {
-        const long long tl = my_tile(u, t);
-        real[t] = tl < p.n_tiles;
-        j[t] = static_cast<int>((real[t] ? tl : p.n_tiles - 1) / tpj);
+        const int tl = my_tile(u, t);
+        real[t] = tl < n_tiles;
+        const int tt = real[t] ? tl : n_tiles - 1;
+        j[t] = fdiv(tt, tpj_div);
         // this tile's candidate index (its h1 was built earlier; only the G = 0 path reads u here)
-        const int ct = static_cast<int>((real[t] ? tl : p.n_tiles - 1) % tpj);
-        c[t] = p.c_begin + (long long)ct * kTileM + row;
+        c[t] = c_begin + (tt - j[t] * tpj) * kTileM + row;
         up[t] = uc[t] = 0.f;
         if (G == 0) row_u(tl, up[t], uc[t], c[t]);
         up2[t] = uc2[t] = dot[t] = 0.f;
@@ -630,7 +646,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         prefetch_vecs(slot ^ 1, u + stride);
 #pragma unroll
         for (int t = 0; t < C::NT; ++t) {
-          long long c2;
+          int c2;
           row_u(my_tile(u + stride, t), up2[t], uc2[t], c2);
         }
       }
@@ -696,7 +712,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             AB_ACC(st, 1, tl);
             AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
             AB_T0(tc);
-            dq ^= 1;
+            dq = dq + 1 == C::NACC ? 0 : dq + 1;
 #if defined(AB_EXP) && (AB_EXP & 1)
             if (false)   // timing experiment: no epilogue math or activation stores
 #endif

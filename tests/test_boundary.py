@@ -122,3 +122,28 @@ def test_shard_bounds_partition():
             b = [ab.shard_bounds(C, r, G) for r in range(G)]
             assert b[0][0] == 0 and b[-1][1] == C
             assert all(b[i][1] == b[i + 1][0] for i in range(G - 1))
+
+
+def test_fastdiv_reference(lib):
+    """K2's multiply-shift division (internal.h make_fastdiv / fdiv) equals integer division for
+    every dividend below 2^31: divisors at and around powers of two, the bench's tiles_per_job and
+    Q values, random ones; dividends at the edges of each quotient step and near 2^31."""
+    rng = np.random.default_rng(5)
+    ds = [1, 2, 3, 5, 7, 31, 32, 33, 64, 127, 128, 129, 4095, 4096, 4097, 8192, 65535, 65536, 65537,
+          (1 << 20) + 1, (1 << 30) - 1, 1 << 30, (1 << 30) + 1, (1 << 31) - 1]
+    ds += [int(v) for v in rng.integers(1, 1 << 31, 300)]
+    for d in ds:
+        n = [0, 1, d - 1, d, d + 1, (1 << 31) - 1, (1 << 31) - 2, ((1 << 31) - 1) // d * d,
+             ((1 << 31) - 1) // d * d - 1]
+        n += [int(v) for v in rng.integers(0, 1 << 31, 200)]
+        n = np.array([v for v in n if 0 <= v < (1 << 31)], dtype=np.uint32)
+        out = np.zeros_like(n)
+        st = lib.autobyte_debug_fastdiv(ctypes.c_uint32(d), n.ctypes.data_as(ctypes.c_void_p), len(n),
+                                        out.ctypes.data_as(ctypes.c_void_p))
+        assert st == 0
+        np.testing.assert_array_equal(out, n // np.uint32(d), err_msg=f"d={d}")
+    bad = np.array([1 << 31], dtype=np.uint32)
+    assert lib.autobyte_debug_fastdiv(ctypes.c_uint32(3), bad.ctypes.data_as(ctypes.c_void_p), 1,
+                                      bad.ctypes.data_as(ctypes.c_void_p)) != 0
+    assert lib.autobyte_debug_fastdiv(ctypes.c_uint32(0), bad.ctypes.data_as(ctypes.c_void_p), 0,
+                                      bad.ctypes.data_as(ctypes.c_void_p)) != 0
