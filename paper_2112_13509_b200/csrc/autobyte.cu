@@ -556,9 +556,9 @@ autobyte_status run_encode_and_score(autobyte_ctx* c, const autobyte_job_stats* 
   sp.precision3 = c->planes == 2 ? 1 : 0;
   sp.keys = c->keys.ptr; sp.cur_keys = c->keys.ptr + J;
   sp.cur_idx = cur_idx; sp.scores = scores;
+  sp.done = c->done.ptr;   // CTA exit counter; the last CTA zeroes it
   if (best_idx && !(c->comm && c->world > 1)) {   // single rank: K2's last CTA decodes the keys
     sp.finalize = 1;
-    sp.done = c->done.ptr;
     sp.best_idx = best_idx; sp.best_score = best_score; sp.cur_score = cur_score;
     if (finalized) *finalized = true;
   }

@@ -43,6 +43,15 @@ namespace ab {
 // Optional cycle accounting (build with -DAB_STATS): where each warp role spends its time.
 #ifdef AB_STATS
 __device__ unsigned long long g_ab_stats[20];
+// per-CTA timeline (%globaltimer, ns): entry, prologue done, first MMA issued, first h1 published,
+// last MMA issued, epilogue done, exit (after the folded K5)
+__device__ unsigned long long g_ab_tl[256][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define AB_TL(i) do { if (blockIdx.x < 256) g_ab_tl[blockIdx.x][i] = gtimer(); } while (0)
 #define AB_T0(v) const long long v = clock64()
 #define AB_ACC(st, i, v) (st)[i] += clock64() - (v)
 __device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3][1024 events][code, clock]
@@ -63,6 +72,7 @@ __device__ unsigned long long g_ab_trace[8 * 1024 * 2];   // [cta 0/1][role 0..3
 #define AB_TRACE(on, ev, g, q)
 #define AB_T0(v)
 #define AB_ACC(st, i, v)
+#define AB_TL(i)
 #endif
 
 // P3 = 1 is the fp32-accuracy path (AB_PREC_FP32): every operand x is split into bf16 hi = rn(x) and
@@ -209,7 +219,10 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
 // (its A rows, its TMEM accumulators, its epilogue) and half of every weight stage (64 of the 128
 // output rows), and the leader issues M = 256 tcgen05.mma.cta_group::2 for both. Weight bytes
 // streamed from L2 per candidate are halved.
-template <int H, int CG, int P3>
+// BS: every hidden-layer bias fits the shared-memory copy (G <= G_CAP), so the global-load path of
+// the chunk epilogue is compiled out (as a run-time branch both paths were if-converted and issued:
+// the predicated-off global loads were 12 % of K2's instructions under ncu).
+template <int H, int CG, int P3, bool BS>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
   using C = ScoreCfg<H, CG, P3>;
   extern __shared__ uint8_t smem_raw[];
@@ -231,6 +244,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   uint64_t* vfull = afull + C::NT * C::NQ;                                      // next unit's job vectors
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(vfull + 1);
   unsigned long long* sWkey = reinterpret_cast<unsigned long long*>(sTmem + 2);
+  static_assert((2 * C::NS + 2 * C::NACC + C::NT * C::NQ + 1) * 8 + 8 + 32 <= C::MISC_BYTES, "barrier / scalar region");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.G;
@@ -241,6 +255,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   int trace_n = 0;
   (void)trace_n;
   AB_T0(t_start);
+  if (threadIdx.x == 0) AB_TL(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -266,6 +281,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) AB_TL(1);
   const uint32_t tmem = *sTmem;
   // work unit u = NT tiles per CTA (of a pair): this CTA's tile t of unit u is (u*NT + t)*CG + rank;
   // units are handed out round-robin: first + i*stride
@@ -286,7 +302,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       // this pair's (CTA's) replica of the packed weights (same bytes, different L2 lines)
       const int rep = static_cast<int>((CG == 2 ? (blockIdx.x >> 1) : blockIdx.x) % kWeightReplicas);
       const int rep_rows = G * C::NQ * C::NKB * C::NCH * C::NP;   // 64-element rows per replica
-      for (int u = first; u < n_units; u += stride)
+      for (int u = first, k = 0; u < n_units; u += stride, ++k)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
             for (int t = 0; t < C::NT; ++t)   // every tile of the unit streams the same chunk weights
@@ -294,7 +310,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
               AB_T0(te);
               mbar_wait(&empty[s], ph ^ 1);
               AB_ACC(st, 0, te);
-              AB_TRACE(u == first + 2 * stride && lane == 0, 40, g, q * 16 + b);
+              AB_TRACE(k == 2 && lane == 0, 40, g, q * 16 + b);
               if (elect_one()) {
                 const int ti = (g * C::NQ + q) * C::NKB + b;
 #if defined(AB_EXP) && (AB_EXP & 2)
@@ -331,7 +347,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       uint32_t ph = 0, aph = 0, dbits = 0;
       int dq = 0, b0 = 0;
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sStage));
-      for (int u = first; u < n_units; u += stride) {
+      for (int u = first, k = 0; u < n_units; u += stride, ++k) {
         for (int g = 0; g < G; ++g) {
           const int src = (b0 + g) & 1;
           for (int q = 0; q < C::NQ; ++q)
@@ -342,7 +358,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             if (CG == 2) mbar_wait_cluster(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
             else mbar_wait(&dempty[dq], ((dbits >> dq) & 1u) ^ 1u);
             AB_ACC(st, 0, td);
-            AB_TRACE(u == first + 2 * stride, 10, g, q);
+            AB_TRACE(k == 2, 10, g, q);
             dbits ^= 1u << dq;
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
@@ -354,14 +370,15 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #endif
               // (SPILL: every layer reads A hi from X and A lo from TMEM column Y_COL)
               mma_chunk<C, CG, false>(d_t, a_desc0, C::SPILL ? y_t : 0u, b_desc0, full, empty, aw, aph, s,
-                                      ph, st, u == first + 2 * stride, g, q, trace_n);
+                                      ph, st, k == 2, g, q, trace_n);
             else
-              mma_chunk<C, CG, true>(d_t, 0ull, y_t, b_desc0, full, empty, aw, aph, s, ph, st, u == first + 2 * stride, g, q, trace_n);
+              mma_chunk<C, CG, true>(d_t, 0ull, y_t, b_desc0, full, empty, aw, aph, s, ph, st, k == 2, g, q, trace_n);
             if (elect_one()) {
               if (CG == 2) umma_commit2(&dfull[dq]);
               else umma_commit(&dfull[dq]);
             }
-            AB_TRACE(u == first + 2 * stride && lane == 0, 12, g, q);
+            if (u == first && g == 0 && q == 0 && t == 0 && lane == 0) AB_TL(2);
+            AB_TRACE(k == 2 && lane == 0, 12, g, q);
             __syncwarp();
             dq = dq + 1 == C::NACC ? 0 : dq + 1;
           }
@@ -369,6 +386,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         }
         b0 = ((b0 + G - 1) & 1) ^ 1;
       }
+      if (lane == 0) AB_TL(4);
     }
   } else {
     // ================================================================ epilogue (256 threads)
@@ -610,9 +628,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     int dq = 0, b0 = 0, it = 0;
     uint32_t dbits = 0, vph = 0;
     int u = first;
-    if (u < n_units) load_vecs(0, u);
+    load_vecs(0, u);
     named_bar_sync(kEpiBar, kEpiThreads);
-    if (G > 0 && u < n_units) {
+    if (G > 0) {
       for (int t = 0; t < C::NT; ++t) {
         float up, uc;
         int c;
@@ -621,10 +639,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
         for (int q = 0; q < C::NQ; ++q) build_piece(t, q, up, uc, 0);
       }
     }
+    if (etid == 0) AB_TL(3);
     named_bar_sync(kEpiBar, kEpiThreads);   // every thread is done with the a-slots before they are refilled
     for (; u < n_units; u += stride, ++it) {
       const int slot = it & 1;
-      const bool has_next = u + stride < n_units;
+      const int u_next = u + stride;
+      const bool has_next = u_next < n_units;
       float up[C::NT], uc[C::NT], up2[C::NT], uc2[C::NT], dot[C::NT];
       int c[C::NT];
       bool real[C::NT];
@@ -643,11 +663,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       }
       if (G > 0 && has_next) {
         // h1 of this unit's tiles is complete, so the a-slots are free: fetch the next unit's job vectors
-        prefetch_vecs(slot ^ 1, u + stride);
+        prefetch_vecs(slot ^ 1, u_next);
 #pragma unroll
         for (int t = 0; t < C::NT; ++t) {
           int c2;
-          row_u(my_tile(u + stride, t), up2[t], uc2[t], c2);
+          row_u(my_tile(u_next, t), up2[t], uc2[t], c2);
         }
       }
       if (G == 0) {
@@ -679,7 +699,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           // hides behind it (they sat on the critical path of every chunk epilogue)
           const int n0 = q * C::NCH + grp * C::QC;
           float bq[C::QC];
-          if (g < C::G_CAP) {
+          if (BS || g < C::G_CAP) {
             const float4* s4 = reinterpret_cast<const float4*>(sBias + g * H + n0);
 #pragma unroll
             for (int i = 0; i < C::QC / 4; ++i) {
@@ -699,7 +719,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             AB_T0(tw);
             mbar_wait(&dfull[dq], (dbits >> dq) & 1u);
             AB_ACC(st, 0, tw);
-            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 20 + (warp == 17) * 10, g, q);
+            AB_TRACE(it == 2 && lane == 0 && (warp == 2 || warp == 17), 20 + (warp == 17) * 10, g, q);
             AB_T0(tl);
             dbits ^= 1u << dq;
             tc_fence_after();
@@ -710,7 +730,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             __syncwarp();
             signal(&dempty[dq], dempty_c[dq]);
             AB_ACC(st, 1, tl);
-            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
+            AB_TRACE(it == 2 && lane == 0 && (warp == 2 || warp == 17), 21 + (warp == 17) * 10, g, q);
             AB_T0(tc);
             dq = dq + 1 == C::NACC ? 0 : dq + 1;
 #if defined(AB_EXP) && (AB_EXP & 1)
@@ -772,7 +792,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             }
             if (!last && !C::SPILL) publish(t, dst, q);
             AB_ACC(st, 2, tc);
-            AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
+            AB_TRACE(it == 2 && lane == 0 && (warp == 2 || warp == 17), 22 + (warp == 17) * 10, g, q);
             // (SPILL: only once the last chunk shows the layer's MMAs done, X and TMEM are free)
             if (last && has_next && q == (C::SPILL ? C::NQ - 1 : 0)) {
               // the next unit's h1 of this tile slot, all pieces at once: once this warp has seen
@@ -783,7 +803,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
 #pragma unroll 1
               for (int pq = 0; pq < C::NQ; ++pq) build_piece(t, pq, up2[t], uc2[t], src ^ 1);
               AB_ACC(st, 3, th);
-              AB_TRACE(u == first + 2 * stride && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
+              AB_TRACE(it == 2 && lane == 0 && (warp == 2 || warp == 17), 23 + (warp == 17) * 10, g, q);
             }
             if (last && q == C::NQ - 1) reduce_tile(dot[t], slot * C::NT + t, real[t], j[t], c[t]);
           }
@@ -791,6 +811,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       }
       if (G > 0) b0 = ((b0 + G - 1) & 1) ^ 1;
     }
+    if (etid == 0) AB_TL(5);
   }
 #ifdef AB_STATS
   // slots: 0-3 producer/MMA/epilogue waits, see tools/kstats.py
@@ -817,16 +838,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
     if (CG == 2) tmem_dealloc2(tmem, C::TMEM_COLS);
     else tmem_dealloc(tmem, C::TMEM_COLS);
   }
-  if (p.finalize) {
-    // K5 folded in (single rank): the last CTA to finish decodes every job's keys. Each CTA's
-    // atomicMax updates happen before its fence + count; the last CTA reads the keys past L1.
+  {
+    // The last CTA to finish zeroes the exit counter for the next (stream-ordered) launch and,
+    // single rank, decodes every job's keys (K5 folded in). Each CTA's atomicMax updates happen
+    // before its fence + count; the last CTA reads the keys past L1.
     __shared__ int s_last;
     if (threadIdx.x == 0) {
       __threadfence();
       s_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (s_last) {
+    if (s_last && p.finalize) {
       __threadfence();
       for (int j = threadIdx.x; j < p.J; j += blockDim.x) {
         const unsigned long long k = __ldcg(p.keys + j);
@@ -842,20 +864,21 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
           p.cur_score[j] = ck ? unord32(static_cast<uint32_t>(ck >> 32)) : __uint_as_float(0x7FC00000u);
         }
       }
-      if (threadIdx.x == 0) *p.done = 0u;   // the next launch (stream-ordered) counts from zero
     }
+    if (s_last && threadIdx.x == 0) p.done[0] = 0u;
   }
+  if (threadIdx.x == 0) AB_TL(6);
 }
 
-template <int H, int CG, int P3>
-static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
+template <int H, int CG, int P3, bool BS>
+static cudaError_t launch_score_hcb(const ScoreParams& p, int num_sms, cudaStream_t s) {
   using C = ScoreCfg<H, CG, P3>;
   static unsigned long long attr_done = 0;   // per device: the > 48 KB opt-in is a per-device attribute
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (!(attr_done >> (dev & 63) & 1ull)) {
-    e = cudaFuncSetAttribute(score_kernel<H, CG, P3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    e = cudaFuncSetAttribute(score_kernel<H, CG, P3, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done |= 1ull << (dev & 63);
   }
@@ -875,7 +898,18 @@ static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG, P3>, p);
+  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG, P3, BS>, p);
+}
+
+template <int H, int CG, int P3>
+static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
+  using C = ScoreCfg<H, CG, P3>;
+  if constexpr (C::G_CAP >= kMaxHidden - 1) {   // every head this library accepts (H <= 256)
+    return launch_score_hcb<H, CG, P3, true>(p, num_sms, s);
+  } else {
+    if (p.G <= C::G_CAP) return launch_score_hcb<H, CG, P3, true>(p, num_sms, s);
+    return launch_score_hcb<H, CG, P3, false>(p, num_sms, s);
+  }
 }
 
 template <int H>
@@ -1009,6 +1043,10 @@ extern "C" int ab_debug_trace(unsigned long long* out, int n, int reset) {
   static unsigned long long z[8 * 1024 * 2];
   if (reset) cudaMemcpyToSymbol(ab::g_ab_trace, z, sizeof(z));
   return n;
+}
+extern "C" int ab_debug_timeline(unsigned long long* out) {   // [256][8] of the last K2 launch
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, ab::g_ab_tl, sizeof(unsigned long long) * 256 * 8) == cudaSuccess ? 0 : -1;
 }
 extern "C" int ab_debug_stats(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
