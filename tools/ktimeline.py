@@ -49,6 +49,13 @@ def main():
         v = rel[:, i][t[:, i] > 0]
         if len(v):
             print(f"  {c:10s} min {v.min():8.2f}  median {np.median(v):8.2f}  max {v.max():8.2f} us  (n={len(v)})")
+    # per pair (leader CTAs): last MMA issue time vs SM id, slowest and fastest
+    lead = [(rel[b, 4], int(buf[b, 7]), b) for b in range(0, n, 2) if t[b, 4] > 0]
+    lead.sort()
+    print("  fastest pairs (last_mma us, smid, block):", [(round(a, 1), s, b) for a, s, b in lead[:6]])
+    print("  slowest pairs (last_mma us, smid, block):", [(round(a, 1), s, b) for a, s, b in lead[-6:]])
+    sm = np.array([s for _, s, _ in lead]); tt = np.array([a for a, _, _ in lead])
+    print(f"  mean last_mma: smid < 72: {tt[sm < 72].mean():.1f} us, smid >= 72: {tt[sm >= 72].mean():.1f} us")
     net.close()
 
 
