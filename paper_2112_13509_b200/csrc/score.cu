@@ -256,6 +256,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   (void)trace_n;
   AB_T0(t_start);
   if (threadIdx.x == 0) AB_TL(0);
+#ifdef AB_STATS
+  if (threadIdx.x == 0 && blockIdx.x < 256) {   // the CTA's SM (tools/ktimeline.py)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_ab_tl[blockIdx.x][7] = smid;
+  }
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
