@@ -163,8 +163,10 @@ def test_exact_dyadic_bit_for_bit(L, H, cg):
 
 
 # ------------------------------------------------------------------------------------- random nets
+# (deep heads: 8x256 has exactly G_CAP = 7 tensor-core layers with shared-memory biases; 6x512 is past
+# H = 512's G_CAP = 3, i.e. K2's `BS = false` variant that reads the later biases from global memory)
 CASES = [(1, 64, 7, 9), (2, 64, 8, 8), (2, 128, 7, 13), (3, 128, 5, 31), (3, 256, 31, 9), (4, 256, 16, 16),
-         (2, 512, 9, 11), (4, 512, 33, 7)]
+         (2, 512, 9, 11), (4, 512, 33, 7), (8, 64, 5, 5), (8, 256, 8, 8), (6, 512, 9, 7)]
 
 
 @pytest.mark.parametrize("cg", [1, 2])
@@ -323,7 +325,8 @@ def test_weights_roundtrip_and_noop_adapt():
 
 
 @pytest.mark.parametrize("L,H,B,steps", [(1, 64, 7, 1), (2, 128, 33, 2), (3, 256, 256, 1), (4, 512, 100, 3),
-                                          (2, 64, 1, 2), (3, 256, 129, 1)])
+                                          (2, 64, 1, 2), (3, 256, 129, 1),
+                                          (8, 128, 5, 2), (6, 512, 40, 1)])   # deep heads: K4s / K4
 def test_adapt_matches_oracle(L, H, B, steps):
     W = synth.make_weights(synth.NetDesc(L, H), seed=L + H)
     jobs = synth.small_fleet(B, 17 + L)
