@@ -152,11 +152,11 @@ constexpr uint32_t kEpiBar = 1;
 // A comes from buffer X (SS: smem descriptor) or buffer Y (TS: TMEM address). For the first
 // chunk of a layer, K block b is only consumed once the epilogues have published the matching
 // 128-column piece of A (afull[b / KB_PER_Q]), so a layer starts before its input is complete.
-template <typename C, int CG, bool TS>
+template <typename C, int CG, bool TS, bool RES = false>
 __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32_t a_tmem0, uint64_t b_desc0,
                                           uint64_t* full, uint64_t* empty, uint64_t* afull, uint32_t aph,
                                           int& s, uint32_t& ph, long long* st, bool trace_on, int g, int q,
-                                          int& trace_n) {
+                                          int& trace_n, int spu = C::NS) {
   const int warp = 1;
   (void)warp;
 #pragma unroll 1
@@ -210,7 +210,11 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
       else umma_commit(&empty[s]);
     }
     __syncwarp();
-    if (++s == C::NS) { s = 0; ph ^= 1; }
+    if constexpr (RES) {   // resident weights: the unit's spu stages, loaded once (full stays complete)
+      if (++s == spu) s = 0;
+    } else {
+      if (++s == C::NS) { s = 0; ph ^= 1; }
+    }
   }
 }
 
@@ -222,7 +226,8 @@ __device__ __forceinline__ void mma_chunk(uint32_t d_t, uint64_t a_desc0, uint32
 // BS: every hidden-layer bias fits the shared-memory copy (G <= G_CAP), so the global-load path of
 // the chunk epilogue is compiled out (as a run-time branch both paths were if-converted and issued:
 // the predicated-off global loads were 12 % of K2's instructions under ncu).
-template <int H, int CG, int P3, bool BS>
+// RS: resident weights (one unit's weight stages fit the ring; see `spu` below), chosen on the host.
+template <int H, int CG, int P3, bool BS, bool RS>
 __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_constant__ ScoreParams p) {
   using C = ScoreCfg<H, CG, P3>;
   extern __shared__ uint8_t smem_raw[];
@@ -299,6 +304,14 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   const int n_units = (n_tiles + CG * C::NT - 1) / (CG * C::NT);
   const int first = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
   const int stride = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
+  // Resident weights: when one unit's weight stages (G layers x NQ chunks x NKB / KBS) fit the ring
+  // (3x256 / 2x256 with CTA pairs: 8 / 4 of 9 stages; 3x128: 4 of 11), the producer loads them once
+  // into slots 0..spu-1 and stops, and the issuer cycles over those slots for every unit without
+  // waiting (their full barriers stay complete) — the weights stay in shared memory for the whole
+  // launch instead of being re-streamed from L2 every unit (P:402 dense layers; north star: "weights
+  // resident in shared memory").
+  const int spu = G * C::NQ * C::NT * (C::NKB / C::KBS);
+  constexpr bool resident = RS;   // (the host launches RS = true exactly when spu <= NS)
 
   if (warp == 0) {
     // ================================================================ TMA producer (both CTAs)
@@ -309,7 +322,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
       // this pair's (CTA's) replica of the packed weights (same bytes, different L2 lines)
       const int rep = static_cast<int>((CG == 2 ? (blockIdx.x >> 1) : blockIdx.x) % kWeightReplicas);
       const int rep_rows = G * C::NQ * C::NKB * C::NCH * C::NP;   // 64-element rows per replica
-      for (int u = first, k = 0; u < n_units; u += stride, ++k)
+      const int u_end = resident ? first + 1 : n_units;   // (first < n_units)
+      for (int u = first, k = 0; u < u_end; u += stride, ++k)
         for (int g = 0; g < G; ++g)
           for (int q = 0; q < C::NQ; ++q)
             for (int t = 0; t < C::NT; ++t)   // every tile of the unit streams the same chunk weights
@@ -370,16 +384,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
             tc_fence_after();
             const uint32_t d_t = tmem + dq * C::NCH;
             uint64_t* aw = q == 0 ? afull + t * C::NQ : nullptr;
-#if defined(AB_EXP) && (AB_EXP & 8)
-            if (false)   // timing experiment: every layer reads A from TMEM
-#else
+            // (SPILL: every layer reads A hi from X and A lo from TMEM column Y_COL)
             if (C::SPILL || src == 0)
-#endif
-              // (SPILL: every layer reads A hi from X and A lo from TMEM column Y_COL)
-              mma_chunk<C, CG, false>(d_t, a_desc0, C::SPILL ? y_t : 0u, b_desc0, full, empty, aw, aph, s,
-                                      ph, st, k == 2, g, q, trace_n);
+              mma_chunk<C, CG, false, RS>(d_t, a_desc0, C::SPILL ? y_t : 0u, b_desc0, full, empty, aw, aph, s,
+                                          ph, st, k == 2, g, q, trace_n, spu);
             else
-              mma_chunk<C, CG, true>(d_t, 0ull, y_t, b_desc0, full, empty, aw, aph, s, ph, st, k == 2, g, q, trace_n);
+              mma_chunk<C, CG, true, RS>(d_t, 0ull, y_t, b_desc0, full, empty, aw, aph, s, ph, st, k == 2, g, q,
+                                         trace_n, spu);
             if (elect_one()) {
               if (CG == 2) umma_commit2(&dfull[dq]);
               else umma_commit(&dfull[dq]);
@@ -877,7 +888,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const __grid_co
   if (threadIdx.x == 0) AB_TL(6);
 }
 
-template <int H, int CG, int P3, bool BS>
+template <int H, int CG, int P3, bool BS, bool RS>
 static cudaError_t launch_score_hcb(const ScoreParams& p, int num_sms, cudaStream_t s) {
   using C = ScoreCfg<H, CG, P3>;
   static unsigned long long attr_done = 0;   // per device: the > 48 KB opt-in is a per-device attribute
@@ -885,7 +896,7 @@ static cudaError_t launch_score_hcb(const ScoreParams& p, int num_sms, cudaStrea
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (!(attr_done >> (dev & 63) & 1ull)) {
-    e = cudaFuncSetAttribute(score_kernel<H, CG, P3, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    e = cudaFuncSetAttribute(score_kernel<H, CG, P3, BS, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done |= 1ull << (dev & 63);
   }
@@ -905,17 +916,27 @@ static cudaError_t launch_score_hcb(const ScoreParams& p, int num_sms, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG, P3, BS>, p);
+  return cudaLaunchKernelEx(&cfg, score_kernel<H, CG, P3, BS, RS>, p);
+}
+
+template <int H, int CG, int P3, bool BS>
+static cudaError_t launch_score_hcbr(const ScoreParams& p, int num_sms, cudaStream_t s) {
+  using C = ScoreCfg<H, CG, P3>;
+  // resident weights need spu = G * NQ * NT * NKB / KBS <= NS (possible only on small heads)
+  if constexpr (!P3 && H <= 256) {
+    if (p.G * C::NQ * C::NT * (C::NKB / C::KBS) <= C::NS) return launch_score_hcb<H, CG, P3, BS, true>(p, num_sms, s);
+  }
+  return launch_score_hcb<H, CG, P3, BS, false>(p, num_sms, s);
 }
 
 template <int H, int CG, int P3>
 static cudaError_t launch_score_hc(const ScoreParams& p, int num_sms, cudaStream_t s) {
   using C = ScoreCfg<H, CG, P3>;
   if constexpr (C::G_CAP >= kMaxHidden - 1) {   // every head this library accepts (H <= 256)
-    return launch_score_hcb<H, CG, P3, true>(p, num_sms, s);
+    return launch_score_hcbr<H, CG, P3, true>(p, num_sms, s);
   } else {
-    if (p.G <= C::G_CAP) return launch_score_hcb<H, CG, P3, true>(p, num_sms, s);
-    return launch_score_hcb<H, CG, P3, false>(p, num_sms, s);
+    if (p.G <= C::G_CAP) return launch_score_hcbr<H, CG, P3, true>(p, num_sms, s);
+    return launch_score_hcbr<H, CG, P3, false>(p, num_sms, s);
   }
 }
 
