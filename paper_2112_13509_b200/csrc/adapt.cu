@@ -198,8 +198,12 @@ struct TcState {
   uint64_t* full;        // [kMaxBufs]: the 8 worker warps have written plane buffer b
   uint64_t* empty;       // [kMaxBufs]: the MMAs that read plane buffer b have completed (tcgen05.commit)
   uint64_t* acc_free;    // the epilogue has read the accumulators of the last MMA tile
-  uint32_t fills[3];     // workers: times buffer b has been filled
-  uint32_t issued[3];    // issuer: fills of buffer b consumed
+  // plane buffers are used round-robin over all tiles of the launch: slice n (counted from the
+  // launch start) goes to buffer n % kBufs as its (n / kBufs)-th fill, so the phase bookkeeping is
+  // one counter per role (per-buffer counters indexed by a rotating b lived in local memory: a
+  // load and a store per K slice on both the workers' and the issuer's critical path)
+  uint32_t wsl;          // workers: slices filled
+  uint32_t isl;          // issuer: slices consumed
   uint32_t tiles;        // issuer: MMA tiles issued
 };
 
@@ -244,11 +248,11 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
     if (nk == 0) return;
     if (ts.tiles > 0) mbar_wait(ts.acc_free, (ts.tiles - 1) & 1);   // previous tile's epilogue has read TMEM
     for (int it = 0; it < nk; ++it) {
-      const int b = it % kBufs;
+      const uint32_t n = ts.isl + it;
+      const int b = static_cast<int>(n % kBufs);
       AB_TR(1, it, 0);
-      mbar_wait(&ts.full[b], ts.issued[b] & 1);
+      mbar_wait(&ts.full[b], (n / kBufs) & 1u);
       AB_TR(1, it, 1);
-      ++ts.issued[b];
       tc_fence_after();
       if (elect_one()) {
         const uint32_t buf = pbase + b * kPlaneBuf;
@@ -268,6 +272,7 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
       __syncwarp();
       AB_TR(1, it, 2);
     }
+    ts.isl += nk;
     ++ts.tiles;
     return;
   }
@@ -288,14 +293,15 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
 #pragma unroll
   for (int i = 0; i < kStages - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
-    const int b = it % kBufs;
+    const uint32_t n = ts.wsl + it;
+    const int b = static_cast<int>(n % kBufs);
     AB_TR(0, it, 0);
     cp_async_wait<kStages - 2>();
     AB_TR(0, it, 1);
     named_bar_sync(kWorkBar, kWorkThreads);   // slice `it` landed for every worker
     AB_TR(0, it, 2);
     issue(it + kStages - 1);
-    if (ts.fills[b] > 0) mbar_wait(&ts.empty[b], (ts.fills[b] - 1) & 1);   // MMAs on buffer b's last fill done
+    if (n >= kBufs) mbar_wait(&ts.empty[b], (n / kBufs - 1) & 1u);   // MMAs on buffer b's last fill done
     AB_TR(0, it, 3);
     uint8_t* buf = smem + b * kPlaneBuf;
     split_slice<kTM>(rawA(it % kStages), a_kc, buf, buf + kPlaneA);
@@ -303,12 +309,12 @@ __device__ void gemm_tile(const Gemm& g, int work, uint8_t* smem, TcState& ts) {
     fence_proxy_async_smem();   // generic-proxy plane writes -> visible to the tensor core
     __syncwarp();
     if (lane == 0) mbar_arrive(&ts.full[b]);
-    ++ts.fills[b];
   }
+  ts.wsl += nk;
   cp_async_wait<0>();
   if (nk > 0) {   // the last commit completes after every MMA of the tile
-    const int bl = (nk - 1) % kBufs;
-    mbar_wait(&ts.empty[bl], (ts.fills[bl] - 1) & 1);
+    const uint32_t nl = ts.wsl - 1;
+    mbar_wait(&ts.empty[nl % kBufs], (nl / kBufs) & 1u);
   }
   tc_fence_after();
   // epilogue: warp w reads TMEM lane quadrant w % 4 (rows) and column groups w / 4, w / 4 + 2 (32
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  TcState ts{s_tmem, &s_bar[0], &s_bar[3], &s_bar[6], {0u, 0u, 0u}, {0u, 0u, 0u}, 0u};
+  TcState ts{s_tmem, &s_bar[0], &s_bar[3], &s_bar[6], 0u, 0u, 0u};
   const bool big = p.B >= kBigBatch;   // uniform: every CTA takes the same tile width
   auto tiles = [&](const Gemm& g) { return big ? g.tiles<128>() : g.tiles<64>(); };
   auto gemm = [&](const Gemm& g, int t) {
