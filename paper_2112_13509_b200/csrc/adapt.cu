@@ -372,25 +372,25 @@ __device__ long long g_adapt_sub[1024][5];   // per block, phase B_{L-1}: start,
 #else
 #define AB_SUB(i) do { } while (0)
 #endif
-__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) {
+// Grid barrier on a 64-bit arrival counter that only ever grows (never reset, so no "last arriver"
+// step): barrier k of a launch completes when the counter reaches base + k * gridDim. One release
+// atomic per CTA, then acquire polls; `target` is the next barrier's completion value.
+__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long& target) {
 #ifdef AB_STATS
   if (blockIdx.x == 0 && threadIdx.x == 0 && g_adapt_nphase < 64) g_adapt_phase[g_adapt_nphase++] = clock64();
 #endif
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned int g = gen;
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      unsigned int cur;
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+    if (old + 1 < target) {
+      unsigned long long cur;
       const long long t0 = clock64();
 #pragma unroll 1
       for (uint32_t i = 1;; ++i) {
-        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-        if (cur != g) break;
+        asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+        if (cur >= target) break;
         if ((i & 1023u) == 0) {   // watchdog (ptx.cuh): record, then run to the end instead of trapping
           const long long dt = clock64() - t0;
           if (dt >= (1ll << 26) && ab_aborted()) break;   // (status word only once the wait is stuck)
@@ -398,8 +398,7 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& gen) 
         }
       }
     }
-    gen = g + 1;
-    __threadfence();
+    target += gridDim.x;
   }
   __syncthreads();
 }
@@ -593,11 +592,15 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
   };
   const int B = p.B, H = p.H, L = p.L;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
-  unsigned int gen = 0;
+  // grid barrier: every launch on this ctx has the same grid, so the counter is a multiple of it
+  // between launches, and a CTA reading it before its own first arrival sees base .. base + grid - 1
+  // (the first barrier cannot complete without it)
+  unsigned long long* const gbar = reinterpret_cast<unsigned long long*>(p.barrier);
+  unsigned long long gen = 0;
   if (threadIdx.x == 0) {
-    unsigned int cur;
-    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(p.barrier + 1) : "memory");
-    gen = cur;
+    unsigned long long cur;
+    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(gbar) : "memory");
+    gen = cur - cur % gridDim.x + gridDim.x;
   }
   float* P = p.params;
   float* Gr = p.grads;
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
     }
   };
   build_Z(0);
-  grid_sync(p.barrier, gen);
+  grid_sync(gbar, gen);
 
   const int nsteps = p.steps > 0 ? p.steps : 0;
   for (int step = 0; step <= nsteps; ++step) {
@@ -631,7 +634,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
     if (fwd_only && !(nsteps == 0 && p.loss_before)) break;
     if (p.idx && step > 0) {   // the previous step's last update (W1, b1) ran before this barrier
       build_Z(step);
-      grid_sync(p.barrier, gen);
+      grid_sync(gbar, gen);
     }
     // ---------------- forward with stash
     for (int k = 1; k <= L; ++k) {
@@ -651,11 +654,11 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
         g_adapt_blk[blockIdx.x][2] = clock64();
       }
 #endif
-      grid_sync(p.barrier, gen);
+      grid_sync(gbar, gen);
     }
     out_rows(Hk(L), P + p.off.W_o, P + p.off.b_o, p.v_obs, p.n, p.idx ? p.idx + (size_t)step * B : nullptr,
              1.0f / static_cast<float>(B), B, H, R, ring);
-    grid_sync(p.barrier, gen);
+    grid_sync(gbar, gen);
     if (((step == 0 && p.loss_before) || (p.losses && !fwd_only)) && blockIdx.x == 0) {
       // mean over b of the Eq. 2 norm ||mask (V_hat - V_bar)||_2; R holds residual / B
       __shared__ float s_norm[kAdaptThreads];
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       Gemm gd{B, H, kNMax, R, kNMax, 1, P + p.off.W_o, H, 1, D[L & 1], H, 1, nullptr, Hk(L), H};
       gemm_pair(gw, gd);
       colsum_split(R, B, kNMax, kNMax, Gr + p.off.b_o, p.off.total);
-      grid_sync(p.barrier, gen);
+      grid_sync(gbar, gen);
     }
     // ---------------- backward: hidden layers L..1
     for (int k = L; k >= 1; --k) {
@@ -706,12 +709,12 @@ __global__ void __launch_bounds__(kAdaptThreads, 1) adapt_kernel(const __grid_co
       if (k == L) update_range(p, p.off.W_o, p.off.total, step);
       else update_range(p, p.off.W[k + 1], p.off.b[k + 1] + H, step);
       AB_SUB(3);
-      grid_sync(p.barrier, gen);
+      grid_sync(gbar, gen);
       AB_SUB(4);
     }
     // ---------------- SGD of layer 1 (W1, b1); the kernel exit orders it after the last step
     update_range(p, p.off.W[1], p.off.b[1] + H, step);
-    if (step + 1 < nsteps) grid_sync(p.barrier, gen);
+    if (step + 1 < nsteps) grid_sync(gbar, gen);
   }
   tc_fence_before();
   __syncthreads();

@@ -137,7 +137,7 @@ struct alignas(64) AdaptParams {
   float* grads;            // [head params] gradient buffer
   float* loss_before;      // [1] or null
   float* losses;           // [steps] or null: mean Eq. 2 norm before each step
-  unsigned int* barrier;   // grid barrier counter (2 words)
+  unsigned int* barrier;   // grid barrier: one 64-bit arrival counter (2 words, never reset)
   // optimiser (autobyte_train; autobyte_adapt = SGD with no state)
   int opt;                 // AB_OPT_SGD / AB_OPT_ADAM
   float beta1, beta2, eps;
