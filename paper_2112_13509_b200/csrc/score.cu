@@ -14,13 +14,16 @@
 //   warp 0      TMA producer: streams 64-wide K blocks of the packed bf16 weights into an
 //               NS-stage shared-memory ring (cp.async.bulk, or 2-D tensor-map copies with
 //               .cta_group::2 for CTA pairs; L2 evict_last: every CTA re-reads the same 1.5 MB
-//               at 4x512, so they stay L2-resident).
+//               at 4x512, so they stay L2-resident). When one unit's stages fit the ring (small
+//               heads, kernel variant RS) it loads them once and the weights stay resident.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer.
 //   warps 2..17 epilogue: 4 warps per TMEM lane quadrant, each owning a quarter of the columns.
 // Activations ping-pong between buffer X (shared memory, UMMA SW128 K-major layout, used as
 // the A operand of SS-MMAs) and buffer Y (TMEM columns 256.., packed bf16 pairs, A operand
 // of TS-MMAs); accumulators are two 128-column TMEM chunks so the epilogue of chunk q
 // overlaps the MMAs of chunk q+1. The next tile's h1 is built during the last layer.
+// Kernel variants: <H, CG, P3 (fp32 path), BS (every bias in shared memory), RS (resident
+// weights)>. Tile / unit / candidate indices are 32-bit with multiply-shift divisions (FastDiv).
 #include <cudaTypedefs.h>
 
 #include <cstring>
