@@ -201,6 +201,9 @@ autobyte_status take_status(autobyte_ctx* c) {
     return fail(c, AB_E_NCCL, std::string(code == kStatusPeerKeys ? "peer key exchange" : "peer x all-gather") +
                                   " timed out waiting for rank " + std::to_string(detail) +
                                   " (AUTOBYTE_PEER_TIMEOUT_S); the results of that call are invalid");
+  // an aborted K4 may leave its grid-barrier counter off a multiple of its grid: zero it, stream-
+  // ordered after the aborted launch and before any later one
+  if (c->barrier.ptr) cudaMemsetAsync(c->barrier.ptr, 0, 2 * sizeof(unsigned int), c->stream);
   return fail(c, AB_E_CUDA, "kernel pipeline watchdog fired in block " + std::to_string(detail) +
                                 " (an internal wait exceeded ~2^36 cycles); the results of that call are invalid");
 }
